@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark: batched biased token-passing Viterbi on B200.
+
+Default workload (N=1): BASELINE configs[2] ("C3"): G_large = 5M states /
+20M arcs (build_benchmark_graph semantics, seed 421, L = 2000), 1024 channels
+x 500 frames as 4 utterance segments of 125 frames with a context switch at
+every segment boundary (contexts drawn from a pool of 256 pre-registered
+20-word unigram contexts, discount -2.0), beam 13, max_active 7000,
+partial_every 10.  One step = the whole 1024 x 500 decode.
+
+  value  frames/s with scores resident in HBM (device-timed with CUDA events on
+         the decode stream, max over ranks)
+  e2e    frames/s through the C ABI with scores in pinned host memory, H2D
+         inside the timed region, hypotheses read back to the host
+  roofline  algorithmic bytes (16 N + 16 A_e + 12 A_eps, device
+         counters) / decode-kernel time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the CPU oracle (C port of the reference decoder) on a bounded
+         sample of the same workload, 1 thread
+
+``--impl reference`` times the CPU oracle with every host thread (the
+reference ships no native code) on the same metric.
+Multi-GPU: launched under torchrun, each rank decodes its own 1024 channels
+(weak scaling, no collective on the data path).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L = 2000
+CTX_POOL = 256
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--workload", choices=["c3", "c1", "c2", "c4"], default="c3")
+    p.add_argument("--channels", type=int, default=None)
+    p.add_argument("--frames", type=int, default=500)
+    p.add_argument("--segments", type=int, default=None)
+    p.add_argument("--states", type=int, default=None)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
+    return p.parse_args()
+
+
+def workload(args):
+    w = args.workload
+    if w == "c3" or w == "c4":
+        cfg = dict(states=5_000_000, channels=1024, segments=4, partial_every=10)
+    elif w == "c2":
+        cfg = dict(states=10_000, channels=64, segments=1, partial_every=1)
+    else:  # c1
+        cfg = dict(states=10_000, channels=1, segments=1, partial_every=10)
+    if args.channels:
+        cfg["channels"] = args.channels
+    if args.segments:
+        cfg["segments"] = args.segments
+    if args.states:
+        cfg["states"] = args.states
+    cfg["frames"] = args.frames
+    return cfg
+
+
+# ----------------------------------------------------------------- distributed
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "b200":
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ workload
+
+def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense=None):
+    from paper_2306_15685_b200 import synth
+
+    t0 = time.time()
+    csr = synth.benchmark_graph(W["states"], 4, L, seed=421, f32_weights=True)
+    pool = []
+    if want_contexts:
+        if dense is not None:
+            pool = [synth.dense_context(csr, dense, 2000 + i) for i in range(8)]
+        else:
+            n_pool = CTX_POOL if W["channels"] > 1 else 1
+            pool = [synth.unigram_context(csr, 20, 1000 + i, num_labels=L) for i in range(n_pool)]
+    t1 = time.time()
+    C, T = W["channels"], W["frames"]
+    scores = np.empty((C, T, L), dtype=np.float32)
+    for c in range(C):
+        scores[c] = synth.channel_scores(seed_base, channel_base + c, T, L)
+    return csr, pool, scores, {"graph_s": t1 - t0, "scores_s": time.time() - t1}
+
+
+def ctx_index(c: int, seg: int, n_pool: int) -> int:
+    return (c * 131 + seg * 17) % n_pool
+
+
+def oracle_decode_sample(csr, pool, scores, W, cfg, budget_s: float, threads: int = 1,
+                         channels=None):
+    """CPU oracle over channels' first segment until the time budget is spent."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import OracleGraph, decode_stream
+
+    og = OracleGraph.from_csr(csr)
+    Tseg = W["frames"] // W["segments"]
+    C = W["channels"]
+    order = list(channels) if channels is not None else list(range(C))
+    results = {}
+    frames_done = 0
+    t0 = time.perf_counter()
+
+    def one(c):
+        ctx = pool[ctx_index(c, 0, len(pool))] if pool else None
+        hyps, rc = decode_stream(og, scores[c, :Tseg].astype(np.float64), ctx, cfg)
+        return c, hyps, rc
+
+    i = 0
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        while i < len(order) and (time.perf_counter() - t0 < budget_s or frames_done == 0):
+            batch = order[i:i + threads]
+            i += len(batch)
+            for c, hyps, rc in ex.map(one, batch):
+                results[c] = (hyps, rc)
+                frames_done += Tseg
+    dt = time.perf_counter() - t0
+    return results, frames_done, dt
+
+
+def run_b200(args, W, world, rank, local):
+    import torch
+
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import _lib
+    from paper_2306_15685_b200.device import BatchDecoder, Capacity, DeviceGraph
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    C, T, S = W["channels"], W["frames"], W["segments"]
+    Tseg = T // S
+    assert Tseg * S == T
+    dense = args.density if args.workload == "c4" else None
+    csr, pool, scores_np, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, max_epsilon_expansion=20,
+                           partial_every=W["partial_every"])
+    t0 = time.time()
+    dg = DeviceGraph(csr, device=local)
+    handles = [dg.register_context(c.arc_indices, c.discount) for c in pool]
+    big = W["states"] > 1_000_000
+    records_per_frame = 45_000 if big else 12_000
+    cap = Capacity(arena_records=int(records_per_frame * (Tseg + 2) * 1.15))
+    dec = BatchDecoder(dg, C, cap)
+    prep["upload_s"] = time.time() - t0
+    scores_dev = torch.from_numpy(scores_np).to(dev)
+    scores_host = torch.from_numpy(scores_np).pin_memory()
+    stream = torch.cuda.Stream(device=dev)
+    slots = np.arange(C, dtype=np.int32)
+
+    def ctxs(seg, variant):
+        if variant == "none" or not handles:
+            return np.full(C, -1, dtype=np.int32)
+        return np.array([handles[ctx_index(c, seg, len(handles))] for c in range(C)], dtype=np.int32)
+
+    def step(on_device=True, variant="biased", collect=False):
+        kernel_ms = 0.0
+        launches = 0
+        out = {}
+        dec.init_channels(slots, ctxs(0, variant))
+        for seg in range(S):
+            if seg:
+                dec.set_contexts(slots, ctxs(seg, variant))
+            offs = np.arange(C, dtype=np.int64) * (T * L) + seg * Tseg * L
+            if on_device:
+                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_dev.data_ptr(), L, cfg,
+                           _lib.AB_MODE_STREAM, scores_on_device=True, scores_dtype=_lib.AB_F32,
+                           stream=stream.cuda_stream)
+            else:
+                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_host.numpy(), L, cfg,
+                           _lib.AB_MODE_STREAM, stream=stream.cuda_stream)
+            nh, er, hyps, stride, words = dec.results(C)
+            if er.any():
+                raise RuntimeError(f"device errors in segment {seg}: {np.unique(er)}")
+            kernel_ms += dec.last_kernel_ms()
+            launches += dec.last_launch_count()
+            if collect and seg == 0:
+                out["seg0"] = (nh.copy(), hyps, stride, words.copy())
+            out["d2h_bytes"] = out.get("d2h_bytes", 0) + int(nh.sum()) * 48 + int(words.nbytes)
+        infos = dec.get_many(slots)
+        out["counters"] = (sum(i.tok_expansions for i in infos), sum(i.emit_arcs for i in infos),
+                           sum(i.eps_arcs for i in infos))
+        out["kernel_ms"] = kernel_ms
+        out["launches"] = launches
+        return out
+
+    def timed(k, **kw):
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        outs = [step(**kw) for _ in range(k)]
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        return e0.elapsed_time(e1), outs
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, outs = timed(args.steps)
+    clk = clocks.stop()
+    first = step(collect=True)
+    ms_max = max_over_ranks(ms, world, dev)
+    frames_total = C * T * args.steps * world
+    value = frames_total / (ms_max / 1000.0)
+    n_tok, a_e, a_x = outs[-1]["counters"]
+    alg_bytes = 16 * n_tok + 16 * a_e + 12 * a_x
+    kms = outs[-1]["kernel_ms"]
+    peak, peak_kind = hbm_peak()
+    achieved = alg_bytes / (kms / 1000.0) / 1e9
+    result = {
+        "metric": "decoded frames/sec with biasing (1024-channel biased config, C3)",
+        "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 accumulate (f32 weights/scores)",
+        "data": "synthetic (benchmark_graph seed 421; scores U[0,6) default_rng([7, c]))",
+        "config": {"workload": f"{args.workload}: G {W['states']} states x 4 arcs, L={L}, "
+                               f"{C} channels/GPU x {T} frames, {S} segments with context switch, "
+                               f"partial_every {W['partial_every']}, beam 13, max_active 7000",
+                   "channels_per_gpu": C, "frames": T, "segments": S,
+                   "parallelism": f"channels sharded, {world} GPU(s), no collective",
+                   "l2": "inputs (4 GB scores + 0.36 GB graph) exceed L2"},
+        "gpu_launches": outs[-1]["launches"] * args.steps,
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "kernel": "decode_kernel (whole frame loop; expand + epsilon + prune fused)",
+                     "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": kms,
+                     "per_channel_frame": {"N": n_tok / (C * T), "A_e": a_e / (C * T),
+                                           "A_eps": a_x / (C * T)}},
+        "prep_s": prep,
+    }
+    if not args.no_e2e:
+        for _ in range(1):
+            step(on_device=False)
+        ems, eouts = timed(args.steps, on_device=False)
+        ems = max_over_ranks(ems, world, dev)
+        result["e2e"] = {"value": frames_total / (ems / 1000.0), "unit": "frames/s",
+                         "h2d_bytes_per_step": int(scores_np.nbytes),
+                         "d2h_bytes_per_step": int(eouts[-1]["d2h_bytes"]),
+                         "path": "C ABI ab_decode with pinned host scores (BatchDecoder.decode)"}
+    if rank == 0 and not args.no_cpu:
+        # CPU oracle on a bounded sample of the same workload + parity on that sample
+        res, nfr, dt = oracle_decode_sample(csr, pool, scores_np, W, cfg, args.cpu_seconds, 1)
+        nh, hyps, stride, words = first["seg0"]
+        ok = True
+        for c, (oh, rc) in res.items():
+            last, got = [], []
+            for q in range(int(nh[c])):
+                x = hyps[c * stride + q]
+                w = last[:x.shared] + words[x.words_off:x.words_off + x.n_words - x.shared].tolist()
+                last = w if x.kind == 0 else []
+                got.append((w, x.cost, x.hits))
+            ok &= rc == 0 and got == [(h.words, h.cost, h.hits) for h in oh]
+        result["cpu_baseline"] = {"value": nfr / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+                                  "sample": f"{len(res)} channel(s) x {T // S} frames (segment 0) "
+                                            f"of the same workload, C oracle, 1 thread",
+                                  "parity_with_gpu": bool(ok)}
+    return result
+
+
+def run_reference(args, W, world, rank):
+    if rank != 0:
+        return None
+    import paper_2306_15685_b200 as ab
+
+    W = dict(W)
+    threads = os.cpu_count() or 1
+    budget = max(5.0, args.cpu_seconds)
+    # bounded sample: enough channels for all threads; scores for those only
+    W["channels"] = min(W["channels"], max(threads * 2, 1))
+    csr, pool, scores_np, prep = build_inputs(W, seed_base=7, channel_base=0)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=W["partial_every"])
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_decode_sample(csr, pool, scores_np, W, cfg, 0.0, threads, channels=[0])
+    t_all, f_all = 0.0, 0
+    for _ in range(args.steps):
+        _, nfr, dt = oracle_decode_sample(csr, pool, scores_np, W, cfg, budget / args.steps, threads)
+        t_all += dt
+        f_all += nfr
+    v = f_all / t_all
+    return {
+        "metric": "decoded frames/sec with biasing (1024-channel biased config, C3)",
+        "value": v, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * t_all / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} (bounded CPU sample)", "threads": threads},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{W['channels']} channels x {W['frames'] // W['segments']} "
+                                   "frames per step, C oracle (restatement of the reference "
+                                   "decoder), one channel per thread"},
+        "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    W = workload(args)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        out = run_reference(args, W, world, rank)
+    else:
+        out = run_b200(args, W, world, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * arcboost-b200 C ABI — batched biased token-passing Viterbi on sm_100a.
+ *
+ * This is the drop-in boundary for the reference decode path
+ * (/root/reference/pkg/src/arcboost/decoder.py).  The reference has no FFI;
+ * its boundary is the Python API re-exported from arcboost/__init__.py:21-35.
+ * Each entry point below names the reference interface it replaces; the
+ * Python package paper_2306_15685_b200 binds these through ctypes and
+ * re-exposes the reference names.
+ *
+ * Conventions: every function returns 0 on success or an AB_ERR_* code; the
+ * message of the last failure on the calling thread is ab_last_error().
+ * Host input buffers are copied; the caller keeps ownership.  Device memory
+ * is owned by the library.  One decoder per device; calls on one decoder must
+ * be serialised by the caller (different decoders may run on different host
+ * threads).  No torch types cross this boundary.
+ */
+#ifndef ARCBOOST_B200_H
+#define ARCBOOST_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  AB_OK = 0,
+  AB_ERR_INVALID = 1,      /* bad argument (ValueError on the Python side) */
+  AB_ERR_CUDA = 2,         /* CUDA runtime failure / no device */
+  AB_ERR_DEAD = 3,         /* "decode failure, no active tokens" (decoder.py:419-420, 438-439) */
+  AB_ERR_STATUS = 4,       /* lifecycle misuse (decoder.py:352-353, 430-433) */
+  AB_ERR_CAPACITY = 5,     /* a device capacity (token table, arena, output) was exceeded */
+  AB_ERR_UNKNOWN_CTX = 6,  /* UnknownContextError (biasing.py:27) */
+  AB_ERR_WIDTH = 7         /* frame width != emitting-label count (decoder.py:354-359) */
+};
+
+enum { AB_IDLE = 0, AB_DECODING = 1, AB_ENDPOINTED = 2, AB_FINISHED = 3 };
+enum { AB_PARTIAL = 0, AB_FINAL = 1 };
+enum { AB_F32 = 0, AB_F64 = 1 };
+/* ab_decode modes */
+enum {
+  AB_MODE_ADVANCE = 0, /* advance_frame only, T frames (decoder.py:341-411) */
+  AB_MODE_STREAM = 1   /* _decode_one: partial cadence, endpointing, final (decoder.py:474-501) */
+};
+/* context lookup representation (ab_context_register mode) */
+enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2 };
+
+typedef struct ab_graph ab_graph;
+typedef struct ab_decoder ab_decoder;
+
+/* DecoderConfig (decoder.py:33-48). */
+typedef struct ab_config {
+  double beam;
+  int32_t max_active;
+  int32_t max_epsilon_expansion;
+  int32_t partial_every;
+  int32_t endpoint_silence_frames;
+  int32_t silence_ilabel;
+  int32_t pad_;
+} ab_config;
+
+/* Device capacities per channel; 0 selects a default derived from the graph. */
+typedef struct ab_capacity {
+  int64_t table_slots;   /* token-table slots (power of two) */
+  int64_t frontier_rows; /* epsilon-frontier log rows per frame */
+  int64_t arena_records; /* emission records per utterance */
+  int64_t path_words;    /* longest hypothesis path */
+} ab_capacity;
+
+/* Channel fields (decoder.py:119-139) mirrored between host and device. */
+typedef struct ab_channel_info {
+  int32_t status;
+  int32_t fresh;
+  int64_t frame_index;
+  int64_t total_frames;
+  int64_t utterance_index;
+  int64_t trailing_silence;
+  int64_t eps_truncations;
+  int32_t context;     /* context handle, -1 = unbiased */
+  int32_t num_active;  /* len(_states) */
+  int64_t store_len;   /* len(store) */
+  int32_t error;       /* last device error code for this channel */
+  int32_t pad_;
+  /* work counters accumulated by the device: token expansions,
+     emitting arcs, epsilon arcs */
+  uint64_t tok_expansions;
+  uint64_t emit_arcs;
+  uint64_t eps_arcs;
+} ab_channel_info;
+
+/* One hypothesis as produced on the device (Hypothesis, decoder.py:110-116).
+   Words are prefix-shared: the hypothesis' words are the first `shared` words
+   of the channel's previous hypothesis followed by n_words - shared words
+   stored at words_off in the batch word pool. */
+typedef struct ab_hyp {
+  double cost;
+  int64_t frame;
+  int32_t kind;
+  int32_t fallback;
+  int32_t hits; /* boosted arcs on the hypothesis path */
+  int32_t shared;
+  int32_t n_words;
+  int32_t pad_;
+  int64_t words_off;
+} ab_hyp;
+
+/* One batched decode call (decode_batch, decoder.py:504-526). */
+typedef struct ab_decode_args {
+  int32_t n;                 /* channels in the batch */
+  const int32_t *channels;   /* [n] channel slots (host) */
+  const int32_t *frames;     /* [n] frames per channel (host) */
+  const int64_t *score_offsets; /* [n] element offset of each channel's [T, L] block */
+  const void *scores;        /* f32 or f64 [*, L] rows */
+  int32_t scores_on_device;  /* 1: device pointer; 0: host pointer (copied inside the call) */
+  int32_t scores_dtype;      /* AB_F32 / AB_F64 */
+  int32_t width;             /* L, must equal the graph's emitting-label count */
+  int32_t mode;              /* AB_MODE_* */
+  ab_config config;
+  void *stream;              /* cudaStream_t, NULL = library stream */
+} ab_decode_args;
+
+const char *ab_last_error(void);
+int ab_device_count(int32_t *count);
+
+/* build_csr (fst.py:165-191) → device CSR split into emitting / epsilon SoA. */
+int ab_graph_create(int32_t device, int32_t start, int32_t num_states, int64_t num_arcs,
+                    const int64_t *row_offsets, const int32_t *ilabels, const int32_t *olabels,
+                    const int32_t *next_states, const double *weights, int32_t num_finals,
+                    const int32_t *final_states, const double *final_costs, ab_graph **out);
+void ab_graph_destroy(ab_graph *g);
+/* num_emitting_labels (fst.py:141-145) and storage facts. */
+int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels, int32_t *weights_f32,
+                   int64_t *device_bytes);
+
+/* BiasingContext (biasing.py:86-117) → device context store entry.  arc_indices
+   must be strictly increasing and non-negative (indices >= num_arcs never match). */
+int ab_context_register(ab_graph *g, const int64_t *arc_indices, int64_t k, double discount,
+                        int32_t mode, int32_t *handle);
+int ab_context_release(ab_graph *g, int32_t handle);
+
+int ab_decoder_create(ab_graph *g, const ab_capacity *cap, int32_t max_channels,
+                      ab_decoder **out);
+void ab_decoder_destroy(ab_decoder *d);
+int ab_decoder_query(const ab_decoder *d, ab_capacity *cap, int64_t *device_bytes);
+
+/* init_channel (decoder.py:162-174): fresh IDLE channel in slot ch. */
+int ab_channel_init(ab_decoder *d, int32_t ch, int32_t context);
+/* switch_context (decoder.py:177-193); rejects a mid-utterance switch. */
+int ab_channel_set_context(ab_decoder *d, int32_t ch, int32_t context);
+int ab_channel_get(ab_decoder *d, int32_t ch, ab_channel_info *info);
+/* Host-side lifecycle edits (status / trailing_silence / fresh) pushed to the device. */
+int ab_channel_put(ab_decoder *d, int32_t ch, const ab_channel_info *info);
+/* Batched forms for large channel counts (one transfer each). */
+int ab_channels_init(ab_decoder *d, int32_t n, const int32_t *slots, const int32_t *contexts);
+int ab_channels_set_context(ab_decoder *d, int32_t n, const int32_t *slots,
+                            const int32_t *contexts);
+int ab_channels_get(ab_decoder *d, int32_t n, const int32_t *slots, ab_channel_info *infos);
+/* Active token table: states/costs/hits (any pointer may be NULL). Returns count in *n. */
+int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, double *costs, int32_t *hits,
+                      int32_t cap, int32_t *n);
+
+/* advance_frame × T / _decode_one for a batch; results stay on the device. */
+int ab_decode(ab_decoder *d, const ab_decode_args *args);
+/* Results of the last ab_decode: per batch entry the hypothesis count and the
+   first device error (0 = none) plus the frame index at which it occurred. */
+int ab_read_results(ab_decoder *d, int32_t *n_hyps, int32_t *errors, ab_hyp *hyps,
+                    int32_t hyp_stride, int32_t *words, int64_t words_cap, int64_t *words_used);
+/* partial_hypothesis (decoder.py:414-423) / finalize (decoder.py:426-460) for one channel. */
+int ab_partial(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words, int32_t words_cap);
+int ab_finalize(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words, int32_t words_cap);
+/* Device time of the last ab_decode's decode kernels in milliseconds (CUDA
+   events on the launching stream) and the number of kernels it launched. */
+int ab_last_kernel_ms(ab_decoder *d, float *ms);
+int ab_last_launch_count(ab_decoder *d, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

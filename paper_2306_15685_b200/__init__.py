@@ -1,0 +1,44 @@
+"""arcboost-b200: batched, lattice-free token-passing Viterbi over a WFST with
+per-channel contextual biasing, on NVIDIA B200 (sm_100a).
+
+Drop-in for the decode path of the reference package ``arcboost``
+(arcboost/__init__.py:21-35): the decoder and context names below keep the
+reference's signatures and error behaviour; the work runs in the CUDA library
+``libarcboost_b200.so`` (C ABI in include/arcboost_b200.h).
+"""
+
+from .biasing import (
+    BiasingCompileError,
+    BiasingContext,
+    ContextRegistry,
+    UnknownContextError,
+    effective_weight,
+    sorted_contains,
+)
+from .decoder import (
+    Channel,
+    ChannelResult,
+    ChannelStatus,
+    DecodeError,
+    DecoderConfig,
+    Hypothesis,
+    advance_frame,
+    decode_batch,
+    detect_endpoint,
+    finalize,
+    init_channel,
+    partial_hypothesis,
+    switch_context,
+)
+from .device import BatchDecoder, Capacity, DeviceGraph, device_graph
+from .fst import EPSILON, Arc, CsrFst, Fst, build_csr, csr_from_arrays, parse_text_fst
+from .scores import ScoreMatrix
+
+__all__ = [
+    "EPSILON", "Arc", "BatchDecoder", "BiasingCompileError", "BiasingContext", "Capacity",
+    "Channel", "ChannelResult", "ChannelStatus", "ContextRegistry", "CsrFst", "DecodeError",
+    "DecoderConfig", "DeviceGraph", "Fst", "Hypothesis", "ScoreMatrix", "UnknownContextError",
+    "advance_frame", "build_csr", "csr_from_arrays", "decode_batch", "detect_endpoint",
+    "device_graph", "effective_weight", "finalize", "init_channel", "parse_text_fst",
+    "partial_hypothesis", "sorted_contains", "switch_context",
+]

@@ -1,0 +1,1076 @@
+// arcboost-b200: C ABI (include/arcboost_b200.h) over the sm_100a decode kernels.
+//
+// Host responsibilities: build the device graph (split emitting / epsilon CSR,
+// fst.py:165-191), the context store (biasing.py:86-117), per-channel device
+// pools, launch the batch kernel, relaunch channels that paused for output
+// space, pack hypotheses and words into one contiguous D2H transfer.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "decode_kernel.cuh"
+
+using namespace ab;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(AB_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T> static cudaError_t dmalloc(T **p, size_t count, size_t &acc) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  acc += bytes;
+  return cudaMalloc((void **)p, bytes);
+}
+
+struct HostCtx {
+  bool live = false;
+  double discount = 0.0;
+  u32 k = 0;
+  int mode = AB_CTX_LIST;
+  u32 *d_list = nullptr;
+  u32 *d_bits = nullptr;
+};
+
+struct ab_graph {
+  int device = 0;
+  int start = 0;
+  int num_states = 0;
+  int64_t num_arcs = 0;
+  int L = 0;
+  bool w32 = true;
+  u32 *e_off = nullptr, *x_off = nullptr;
+  void *e_arcs = nullptr, *x_arcs = nullptr;
+  int2 *arc_meta = nullptr;
+  double *final_cost = nullptr;
+  size_t bytes = 0;
+  std::vector<HostCtx> ctxs;
+  CtxDesc *d_ctxs = nullptr;
+  size_t d_ctxs_cap = 0;
+  cudaStream_t stream = nullptr;
+};
+
+struct ab_decoder {
+  ab_graph *g = nullptr;
+  int max_ch = 0;
+  ab_capacity cap{};
+  u32 table_cap = 0;
+  int hashed = 0;
+  u32 tok_cap = 0, flog_cap = 0, arena_cap = 0, path_cap = 0;
+  size_t bytes = 0;
+  ChanState *chans = nullptr;
+  Entry *table = nullptr;
+  u32 *tok_state = nullptr;
+  double *tok_cost = nullptr;
+  TokInfo *tok_info = nullptr;
+  u32 *flog_state = nullptr;
+  double *flog_cost = nullptr;
+  TokInfo *flog_info = nullptr;
+  u32 *all_list = nullptr, *app_list = nullptr;
+  u64 *scr_key = nullptr;
+  u32 *scr_slot = nullptr;
+  int2 *arena = nullptr;
+  int *path_rec = nullptr, *path_words = nullptr;
+  // per-call buffers (grown on demand)
+  size_t batch_cap = 0;
+  int *d_slots = nullptr, *d_frames = nullptr, *d_nhyps = nullptr, *d_errors = nullptr,
+      *d_done = nullptr;
+  long long *d_soff = nullptr, *d_wused = nullptr;
+  size_t hyps_cap = 0;
+  DevHyp *d_hyps = nullptr;
+  size_t words_cap = 0;
+  int *d_words = nullptr;
+  size_t packh_cap = 0, packw_cap = 0;
+  DevHyp *d_packh = nullptr;
+  int *d_packw = nullptr;
+  long long *d_packoff = nullptr; // [2n]
+  size_t stage_cap = 0;
+  void *d_stage = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  int last_launches = 0;
+  size_t info_cap = 0;
+  ab_channel_info *d_infos = nullptr;
+  int *d_islots = nullptr;
+  // accumulated results of the last ab_decode
+  std::vector<int> res_nhyps, res_err;
+  std::vector<std::vector<ab_hyp>> res_hyps;
+  std::vector<std::vector<int32_t>> res_words;
+};
+
+extern "C" const char *ab_last_error(void) { return g_err.c_str(); }
+
+extern "C" int ab_device_count(int32_t *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(AB_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return AB_OK;
+}
+
+// ------------------------------------------------------------------ graph
+
+extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states,
+                               int64_t num_arcs, const int64_t *row_offsets,
+                               const int32_t *ilabels, const int32_t *olabels,
+                               const int32_t *next_states, const double *weights,
+                               int32_t num_finals, const int32_t *final_states,
+                               const double *final_costs, ab_graph **out) {
+  *out = nullptr;
+  if (num_states < 1) return fail(AB_ERR_INVALID, "graph must have at least one state");
+  if (num_arcs < 0 || num_arcs >= (int64_t)0xFFFFFFFFll)
+    return fail(AB_ERR_INVALID, "num_arcs %lld out of range", (long long)num_arcs);
+  if (start < 0 || start >= num_states)
+    return fail(AB_ERR_INVALID, "start state %d out of range for %d states", start, num_states);
+  if (row_offsets[0] != 0 || row_offsets[num_states] != num_arcs)
+    return fail(AB_ERR_INVALID, "row_offsets must start at 0 and end at num_arcs");
+  for (int s = 0; s < num_states; ++s)
+    if (row_offsets[s + 1] < row_offsets[s])
+      return fail(AB_ERR_INVALID, "row_offsets not monotone at state %d", s);
+  int L = 0;
+  bool w32 = true;
+  std::vector<u32> e_cnt(num_states + 1, 0), x_cnt(num_states + 1, 0);
+  for (int s = 0; s < num_states; ++s) {
+    for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
+      if (ilabels[a] < 0 || olabels[a] < 0)
+        return fail(AB_ERR_INVALID, "negative label on arc %lld", (long long)a);
+      if (next_states[a] < 0 || next_states[a] >= num_states)
+        return fail(AB_ERR_INVALID, "arc %lld to nonexistent state %d", (long long)a,
+                    next_states[a]);
+      if (!std::isfinite(weights[a]))
+        return fail(AB_ERR_INVALID, "non-finite weight on arc %lld", (long long)a);
+      if ((double)(float)weights[a] != weights[a]) w32 = false;
+      L = std::max(L, ilabels[a]);
+      if (ilabels[a] != 0) e_cnt[s + 1]++;
+      else x_cnt[s + 1]++;
+    }
+  }
+  for (int s = 0; s < num_states; ++s) {
+    e_cnt[s + 1] += e_cnt[s];
+    x_cnt[s + 1] += x_cnt[s];
+  }
+  const u32 n_e = e_cnt[num_states], n_x = x_cnt[num_states];
+  std::vector<int2> meta(std::max<int64_t>(num_arcs, 1));
+  std::vector<double> fin(num_states, std::nan(""));
+  for (int i = 0; i < num_finals; ++i) {
+    int s = final_states[i];
+    if (s < 0 || s >= num_states) return fail(AB_ERR_INVALID, "final state %d out of range", s);
+    if (!std::isfinite(final_costs[i]))
+      return fail(AB_ERR_INVALID, "non-finite final weight at state %d", s);
+    fin[s] = final_costs[i];
+  }
+  ab_graph *g = new ab_graph();
+  g->device = device;
+  g->start = start;
+  g->num_states = num_states;
+  g->num_arcs = num_arcs;
+  g->L = L;
+  g->w32 = w32;
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    delete g;
+    return fail(AB_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
+  }
+  // build the split arc arrays (arc order inside each state preserved)
+  size_t esz = w32 ? sizeof(EArc<float>) : sizeof(EArc<double>);
+  size_t xsz = w32 ? sizeof(XArc<float>) : sizeof(XArc<double>);
+  std::vector<unsigned char> eh(std::max<size_t>(n_e, 1) * esz, 0), xh(std::max<size_t>(n_x, 1) * xsz, 0);
+  for (int s = 0; s < num_states; ++s) {
+    u32 pe = e_cnt[s], px = x_cnt[s];
+    for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
+      meta[a] = make_int2(olabels[a], ilabels[a]);
+      if (ilabels[a] != 0) {
+        if (w32) {
+          EArc<float> r{(u32)next_states[a], (u32)ilabels[a], (u32)a, (float)weights[a]};
+          memcpy(&eh[(size_t)pe * esz], &r, esz);
+        } else {
+          EArc<double> r{(u32)next_states[a], (u32)ilabels[a], (u32)a, 0u, weights[a]};
+          memcpy(&eh[(size_t)pe * esz], &r, esz);
+        }
+        pe++;
+      } else {
+        if (w32) {
+          XArc<float> r{(u32)next_states[a], (u32)a, (float)weights[a], 0u};
+          memcpy(&xh[(size_t)px * xsz], &r, xsz);
+        } else {
+          XArc<double> r{(u32)next_states[a], (u32)a, weights[a]};
+          memcpy(&xh[(size_t)px * xsz], &r, xsz);
+        }
+        px++;
+      }
+    }
+  }
+  size_t acc = 0;
+  unsigned char *de = nullptr, *dx = nullptr;
+  if (dmalloc(&g->e_off, num_states + 1, acc) || dmalloc(&g->x_off, num_states + 1, acc) ||
+      dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
+      dmalloc(&g->arc_meta, meta.size(), acc) || dmalloc(&g->final_cost, num_states, acc)) {
+    ab_graph_destroy(g);
+    return fail(AB_ERR_CUDA, "device allocation for the graph failed (%zu bytes)", acc);
+  }
+  g->e_arcs = de;
+  g->x_arcs = dx;
+  g->bytes = acc;
+  if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMemcpy(g->e_off, e_cnt.data(), (num_states + 1) * sizeof(u32), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->x_off, x_cnt.data(), (num_states + 1) * sizeof(u32), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(de, eh.data(), eh.size(), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(dx, xh.data(), xh.size(), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->arc_meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->final_cost, fin.data(), num_states * sizeof(double), cudaMemcpyHostToDevice)) {
+    ab_graph_destroy(g);
+    return fail(AB_ERR_CUDA, "graph upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = g;
+  return AB_OK;
+}
+
+extern "C" void ab_graph_destroy(ab_graph *g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  for (auto &c : g->ctxs) {
+    cudaFree(c.d_list);
+    cudaFree(c.d_bits);
+  }
+  cudaFree(g->d_ctxs);
+  cudaFree(g->e_off);
+  cudaFree(g->x_off);
+  cudaFree(g->e_arcs);
+  cudaFree(g->x_arcs);
+  cudaFree(g->arc_meta);
+  cudaFree(g->final_cost);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+extern "C" int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels,
+                              int32_t *weights_f32, int64_t *device_bytes) {
+  if (!g) return fail(AB_ERR_INVALID, "null graph");
+  if (num_emitting_labels) *num_emitting_labels = g->L;
+  if (weights_f32) *weights_f32 = g->w32 ? 1 : 0;
+  if (device_bytes) *device_bytes = (int64_t)g->bytes;
+  return AB_OK;
+}
+
+// ---------------------------------------------------------------- contexts
+
+static int sync_ctx_table(ab_graph *g) {
+  std::vector<CtxDesc> h(g->ctxs.size());
+  for (size_t i = 0; i < g->ctxs.size(); ++i) {
+    const HostCtx &c = g->ctxs[i];
+    h[i].discount = c.discount;
+    h[i].k = c.live ? c.k : 0;
+    h[i].mode = c.mode;
+    h[i].list = c.d_list;
+    h[i].bits = c.d_bits;
+  }
+  if (h.size() > g->d_ctxs_cap) {
+    cudaFree(g->d_ctxs);
+    g->d_ctxs = nullptr;
+    size_t nc = std::max<size_t>(64, h.size() * 2);
+    CK(cudaMalloc(&g->d_ctxs, nc * sizeof(CtxDesc)));
+    g->d_ctxs_cap = nc;
+  }
+  if (!h.empty()) CK(cudaMemcpy(g->d_ctxs, h.data(), h.size() * sizeof(CtxDesc), cudaMemcpyHostToDevice));
+  return AB_OK;
+}
+
+extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int64_t k,
+                                   double discount, int32_t mode, int32_t *handle) {
+  if (!g) return fail(AB_ERR_INVALID, "null graph");
+  if (!std::isfinite(discount)) return fail(AB_ERR_INVALID, "non-finite discount");
+  for (int64_t i = 0; i < k; ++i) {
+    if (arc_indices[i] < 0) return fail(AB_ERR_INVALID, "negative arc index");
+    if (i && arc_indices[i] <= arc_indices[i - 1])
+      return fail(AB_ERR_INVALID, "arc_indices must be strictly increasing");
+  }
+  CK(cudaSetDevice(g->device));
+  // indices outside the graph can never match an expanded arc (biasing.py:108-117)
+  std::vector<u32> list;
+  list.reserve(k);
+  for (int64_t i = 0; i < k; ++i)
+    if (arc_indices[i] < g->num_arcs) list.push_back((u32)arc_indices[i]);
+  HostCtx c;
+  c.live = true;
+  c.discount = discount;
+  c.k = (u32)list.size();
+  if (mode == AB_CTX_AUTO) mode = c.k <= (u32)CTX_SMEM_MAX ? AB_CTX_LIST : AB_CTX_BITSET;
+  if (mode != AB_CTX_LIST && mode != AB_CTX_BITSET) return fail(AB_ERR_INVALID, "bad context mode %d", mode);
+  c.mode = mode;
+  CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
+  if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
+  if (mode == AB_CTX_BITSET) {
+    size_t words = ((size_t)g->num_arcs + 31) / 32 + 1;
+    std::vector<u32> bits(words, 0);
+    for (u32 a : list) bits[a >> 5] |= 1u << (a & 31);
+    CK(cudaMalloc(&c.d_bits, words * sizeof(u32)));
+    CK(cudaMemcpy(c.d_bits, bits.data(), words * sizeof(u32), cudaMemcpyHostToDevice));
+  }
+  int h = -1;
+  for (size_t i = 0; i < g->ctxs.size(); ++i)
+    if (!g->ctxs[i].live) {
+      h = (int)i;
+      break;
+    }
+  if (h < 0) {
+    h = (int)g->ctxs.size();
+    g->ctxs.push_back(c);
+  } else {
+    g->ctxs[h] = c;
+  }
+  int rc = sync_ctx_table(g);
+  if (rc) return rc;
+  *handle = h;
+  return AB_OK;
+}
+
+extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
+  if (!g || handle < 0 || handle >= (int)g->ctxs.size() || !g->ctxs[handle].live)
+    return fail(AB_ERR_UNKNOWN_CTX, "unknown context handle %d", handle);
+  CK(cudaSetDevice(g->device));
+  HostCtx &c = g->ctxs[handle];
+  cudaFree(c.d_list);
+  cudaFree(c.d_bits);
+  c = HostCtx();
+  return sync_ctx_table(g);
+}
+
+// ----------------------------------------------------------------- decoder
+
+static u32 next_pow2(uint64_t v) {
+  u32 p = 16;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t max_channels,
+                                 ab_decoder **out) {
+  *out = nullptr;
+  if (!g) return fail(AB_ERR_INVALID, "null graph");
+  if (max_channels < 1) return fail(AB_ERR_INVALID, "max_channels must be >= 1");
+  CK(cudaSetDevice(g->device));
+  ab_capacity cap = capin ? *capin : ab_capacity{};
+  ab_decoder *d = new ab_decoder();
+  d->g = g;
+  d->max_ch = max_channels;
+  uint64_t ts = cap.table_slots;
+  if (ts <= 0) ts = (g->num_states <= (1 << 20)) ? (uint64_t)g->num_states : (1ull << 17);
+  d->table_cap = next_pow2(ts);
+  if (d->table_cap > (1u << 23)) {
+    delete d;
+    return fail(AB_ERR_INVALID, "table_slots too large (max 2^23)");
+  }
+  d->hashed = d->table_cap < (u32)g->num_states ? 1 : 0;
+  d->tok_cap = d->table_cap;
+  d->flog_cap = (u32)(cap.frontier_rows > 0 ? cap.frontier_rows
+                                            : std::max<uint64_t>(65536, 2ull * d->table_cap));
+  d->arena_cap = (u32)(cap.arena_records > 0 ? cap.arena_records : (1ll << 22));
+  d->path_cap = (u32)(cap.path_words > 0 ? cap.path_words : (1ll << 16));
+  d->cap.table_slots = d->table_cap;
+  d->cap.frontier_rows = d->flog_cap;
+  d->cap.arena_records = d->arena_cap;
+  d->cap.path_words = d->path_cap;
+  const size_t C = (size_t)max_channels;
+  size_t &acc = d->bytes;
+  if (dmalloc(&d->chans, C, acc) || dmalloc(&d->table, C * d->table_cap, acc) ||
+      dmalloc(&d->tok_state, C * d->tok_cap, acc) || dmalloc(&d->tok_cost, C * d->tok_cap, acc) ||
+      dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
+      dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
+      dmalloc(&d->flog_cost, C * d->flog_cap, acc) ||
+      dmalloc(&d->flog_info, C * d->flog_cap, acc) ||
+      dmalloc(&d->all_list, C * d->table_cap, acc) ||
+      dmalloc(&d->app_list, C * d->table_cap, acc) ||
+      dmalloc(&d->scr_key, C * d->table_cap, acc) ||
+      dmalloc(&d->scr_slot, C * d->table_cap, acc) ||
+      dmalloc(&d->arena, C * d->arena_cap, acc) ||
+      dmalloc(&d->path_rec, C * d->path_cap, acc) ||
+      dmalloc(&d->path_words, C * d->path_cap, acc)) {
+    size_t need = acc;
+    ab_decoder_destroy(d);
+    return fail(AB_ERR_CUDA, "device allocation for %d channels failed (%zu bytes requested)",
+                max_channels, need);
+  }
+  if (cudaMemset(d->table, 0, C * d->table_cap * sizeof(Entry)) != cudaSuccess ||
+      cudaMemset(d->chans, 0, C * sizeof(ChanState)) != cudaSuccess ||
+      cudaEventCreate(&d->ev0) != cudaSuccess || cudaEventCreate(&d->ev1) != cudaSuccess) {
+    ab_decoder_destroy(d);
+    return fail(AB_ERR_CUDA, "decoder init failed");
+  }
+  std::vector<ChanState> init(C);
+  for (auto &c : init) {
+    memset(&c, 0, sizeof(c));
+    c.info.status = AB_IDLE;
+    c.info.fresh = 1;
+    c.info.context = -1;
+  }
+  if (cudaMemcpy(d->chans, init.data(), C * sizeof(ChanState), cudaMemcpyHostToDevice) !=
+      cudaSuccess) {
+    ab_decoder_destroy(d);
+    return fail(AB_ERR_CUDA, "decoder init copy failed");
+  }
+  *out = d;
+  return AB_OK;
+}
+
+extern "C" void ab_decoder_destroy(ab_decoder *d) {
+  if (!d) return;
+  cudaSetDevice(d->g->device);
+  void *ptrs[] = {d->chans,     d->table,     d->tok_state, d->tok_cost, d->tok_info,
+                  d->flog_state, d->flog_cost, d->flog_info, d->all_list, d->app_list,
+                  d->scr_key,   d->scr_slot,  d->arena,     d->path_rec, d->path_words,
+                  d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
+                  d->d_soff,    d->d_wused,   d->d_hyps,    d->d_words,  d->d_packh,
+                  d->d_packw,   d->d_packoff, d->d_stage, d->d_infos, d->d_islots};
+  for (void *p : ptrs) cudaFree(p);
+  if (d->ev0) cudaEventDestroy(d->ev0);
+  if (d->ev1) cudaEventDestroy(d->ev1);
+  delete d;
+}
+
+extern "C" int ab_decoder_query(const ab_decoder *d, ab_capacity *cap, int64_t *device_bytes) {
+  if (!d) return fail(AB_ERR_INVALID, "null decoder");
+  if (cap) *cap = d->cap;
+  if (device_bytes) *device_bytes = (int64_t)d->bytes;
+  return AB_OK;
+}
+
+static int check_slot(ab_decoder *d, int ch) {
+  if (!d) return fail(AB_ERR_INVALID, "null decoder");
+  if (ch < 0 || ch >= d->max_ch)
+    return fail(AB_ERR_INVALID, "channel slot %d out of range [0, %d)", ch, d->max_ch);
+  return AB_OK;
+}
+
+static int check_ctx(ab_decoder *d, int ctx) {
+  if (ctx < 0) return AB_OK;
+  if (ctx >= (int)d->g->ctxs.size() || !d->g->ctxs[ctx].live)
+    return fail(AB_ERR_UNKNOWN_CTX, "unknown context handle %d", ctx);
+  return AB_OK;
+}
+
+extern "C" int ab_channel_init(ab_decoder *d, int32_t ch, int32_t context) {
+  int rc;
+  if ((rc = check_slot(d, ch)) || (rc = check_ctx(d, context))) return rc;
+  CK(cudaSetDevice(d->g->device));
+  ab_channel_info info;
+  memset(&info, 0, sizeof(info));
+  info.status = AB_IDLE;
+  info.fresh = 1;
+  info.context = context;
+  // the epoch and path fields stay: epochs must never repeat within a slot
+  CK(cudaMemcpy(&d->chans[ch].info, &info, sizeof(info), cudaMemcpyHostToDevice));
+  int zero[2] = {0, 0};
+  CK(cudaMemcpy(&d->chans[ch].path_len, zero, sizeof(zero), cudaMemcpyHostToDevice));
+  return AB_OK;
+}
+
+extern "C" int ab_channel_get(ab_decoder *d, int32_t ch, ab_channel_info *info) {
+  int rc;
+  if ((rc = check_slot(d, ch))) return rc;
+  CK(cudaSetDevice(d->g->device));
+  CK(cudaMemcpy(info, &d->chans[ch].info, sizeof(*info), cudaMemcpyDeviceToHost));
+  return AB_OK;
+}
+
+extern "C" int ab_channel_put(ab_decoder *d, int32_t ch, const ab_channel_info *info) {
+  int rc;
+  if ((rc = check_slot(d, ch)) || (rc = check_ctx(d, info->context))) return rc;
+  CK(cudaSetDevice(d->g->device));
+  CK(cudaMemcpy(&d->chans[ch].info, info, sizeof(*info), cudaMemcpyHostToDevice));
+  return AB_OK;
+}
+
+extern "C" int ab_channel_set_context(ab_decoder *d, int32_t ch, int32_t context) {
+  int rc;
+  if ((rc = check_slot(d, ch)) || (rc = check_ctx(d, context))) return rc;
+  ab_channel_info info;
+  if ((rc = ab_channel_get(d, ch, &info))) return rc;
+  if (info.status != AB_IDLE && info.status != AB_FINISHED)
+    return fail(AB_ERR_STATUS, "context switch mid-utterance (status %d)", info.status);
+  info.context = context;
+  if (info.status == AB_FINISHED) info.status = AB_IDLE;
+  return ab_channel_put(d, ch, &info);
+}
+
+__global__ void gather_infos(int n, const int *slots, const ChanState *chans,
+                             ab_channel_info *out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = chans[slots[i]].info;
+}
+
+__global__ void scatter_infos(int n, const int *slots, ChanState *chans,
+                              const ab_channel_info *in, int reset_path) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    chans[slots[i]].info = in[i];
+    if (reset_path) {
+      chans[slots[i]].path_len = 0;
+      chans[slots[i]].max_depth = 0;
+    }
+  }
+}
+
+static int ensure_infos(ab_decoder *d, int n) {
+  if ((size_t)n <= d->info_cap) return AB_OK;
+  cudaFree(d->d_infos);
+  cudaFree(d->d_islots);
+  size_t nc = std::max<size_t>(n, 64);
+  CK(cudaMalloc(&d->d_infos, nc * sizeof(ab_channel_info)));
+  CK(cudaMalloc(&d->d_islots, nc * sizeof(int)));
+  d->info_cap = nc;
+  return AB_OK;
+}
+
+extern "C" int ab_channels_get(ab_decoder *d, int32_t n, const int32_t *slots,
+                               ab_channel_info *infos) {
+  if (!d || n < 0) return fail(AB_ERR_INVALID, "bad arguments");
+  if (n == 0) return AB_OK;
+  int rc;
+  for (int i = 0; i < n; ++i)
+    if ((rc = check_slot(d, slots[i]))) return rc;
+  CK(cudaSetDevice(d->g->device));
+  if ((rc = ensure_infos(d, n))) return rc;
+  cudaStream_t st = d->g->stream;
+  CK(cudaMemcpyAsync(d->d_islots, slots, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  gather_infos<<<(n + 127) / 128, 128, 0, st>>>(n, d->d_islots, d->chans, d->d_infos);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(infos, d->d_infos, n * sizeof(ab_channel_info), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return AB_OK;
+}
+
+static int put_infos(ab_decoder *d, int n, const int32_t *slots, const ab_channel_info *infos,
+                     int reset_path) {
+  int rc;
+  CK(cudaSetDevice(d->g->device));
+  if ((rc = ensure_infos(d, n))) return rc;
+  cudaStream_t st = d->g->stream;
+  CK(cudaMemcpyAsync(d->d_islots, slots, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d->d_infos, infos, n * sizeof(ab_channel_info), cudaMemcpyHostToDevice, st));
+  scatter_infos<<<(n + 127) / 128, 128, 0, st>>>(n, d->d_islots, d->chans, d->d_infos, reset_path);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return AB_OK;
+}
+
+extern "C" int ab_channels_init(ab_decoder *d, int32_t n, const int32_t *slots,
+                                const int32_t *contexts) {
+  if (!d || n < 0) return fail(AB_ERR_INVALID, "bad arguments");
+  int rc;
+  std::vector<ab_channel_info> v(n);
+  for (int i = 0; i < n; ++i) {
+    if ((rc = check_slot(d, slots[i])) || (rc = check_ctx(d, contexts ? contexts[i] : -1))) return rc;
+    memset(&v[i], 0, sizeof(ab_channel_info));
+    v[i].status = AB_IDLE;
+    v[i].fresh = 1;
+    v[i].context = contexts ? contexts[i] : -1;
+  }
+  return n ? put_infos(d, n, slots, v.data(), 1) : AB_OK;
+}
+
+extern "C" int ab_channels_set_context(ab_decoder *d, int32_t n, const int32_t *slots,
+                                       const int32_t *contexts) {
+  if (!d || n < 0) return fail(AB_ERR_INVALID, "bad arguments");
+  if (n == 0) return AB_OK;
+  int rc;
+  std::vector<ab_channel_info> v(n);
+  if ((rc = ab_channels_get(d, n, slots, v.data()))) return rc;
+  for (int i = 0; i < n; ++i) {
+    if ((rc = check_ctx(d, contexts[i]))) return rc;
+    if (v[i].status != AB_IDLE && v[i].status != AB_FINISHED)
+      return fail(AB_ERR_STATUS, "channel slot %d: context switch mid-utterance (status %d)",
+                  slots[i], v[i].status);
+    v[i].context = contexts[i];
+    if (v[i].status == AB_FINISHED) v[i].status = AB_IDLE;
+  }
+  return put_infos(d, n, slots, v.data(), 0);
+}
+
+extern "C" int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, double *costs,
+                                 int32_t *hits, int32_t cap, int32_t *n) {
+  int rc;
+  if ((rc = check_slot(d, ch))) return rc;
+  ab_channel_info info;
+  if ((rc = ab_channel_get(d, ch, &info))) return rc;
+  *n = info.num_active;
+  int m = std::min(cap, info.num_active);
+  if (m <= 0) return AB_OK;
+  const size_t base = (size_t)ch * d->tok_cap;
+  if (states) CK(cudaMemcpy(states, d->tok_state + base, m * sizeof(u32), cudaMemcpyDeviceToHost));
+  if (costs) CK(cudaMemcpy(costs, d->tok_cost + base, m * sizeof(double), cudaMemcpyDeviceToHost));
+  if (hits) {
+    std::vector<TokInfo> ti(m);
+    CK(cudaMemcpy(ti.data(), d->tok_info + base, m * sizeof(TokInfo), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) hits[i] = ti[i].hits;
+  }
+  return AB_OK;
+}
+
+// ------------------------------------------------------------------ launch
+
+template <typename T> static int grow(T **p, size_t &cap, size_t need, size_t &acc) {
+  if (need <= cap) return AB_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  size_t nc = std::max(need, cap * 2);
+  if (cudaMalloc((void **)p, nc * sizeof(T)) != cudaSuccess) {
+    cap = 0;
+    return fail(AB_ERR_CUDA, "device allocation of %zu bytes failed", nc * sizeof(T));
+  }
+  acc += (nc - cap) * sizeof(T);
+  cap = nc;
+  return AB_OK;
+}
+
+static int ensure_batch(ab_decoder *d, size_t n) {
+  if (n <= d->batch_cap) return AB_OK;
+  cudaFree(d->d_slots);
+  cudaFree(d->d_frames);
+  cudaFree(d->d_nhyps);
+  cudaFree(d->d_errors);
+  cudaFree(d->d_done);
+  cudaFree(d->d_soff);
+  cudaFree(d->d_wused);
+  cudaFree(d->d_packoff);
+  size_t nc = std::max<size_t>(n, 64);
+  CK(cudaMalloc(&d->d_slots, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_frames, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_nhyps, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_errors, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_done, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_soff, nc * sizeof(long long)));
+  CK(cudaMalloc(&d->d_wused, nc * sizeof(long long)));
+  CK(cudaMalloc(&d->d_packoff, 2 * nc * sizeof(long long)));
+  d->batch_cap = nc;
+  return AB_OK;
+}
+
+static void fill_params(ab_decoder *d, DecodeParams &P) {
+  ab_graph *g = d->g;
+  memset(&P, 0, sizeof(P));
+  P.e_off = g->e_off;
+  P.e_arcs = g->e_arcs;
+  P.x_off = g->x_off;
+  P.x_arcs = g->x_arcs;
+  P.arc_meta = g->arc_meta;
+  P.final_cost = g->final_cost;
+  P.start = g->start;
+  P.num_states = g->num_states;
+  P.L = g->L;
+  P.ctxs = g->d_ctxs;
+  P.num_ctxs = (int)g->ctxs.size();
+  P.chans = d->chans;
+  P.table = d->table;
+  P.table_cap = d->table_cap;
+  P.table_mask = d->table_cap - 1;
+  int lg = 0;
+  while ((1u << lg) < d->table_cap) ++lg;
+  P.hash_shift = 32 - lg;
+  P.hashed = d->hashed;
+  P.tok_state = d->tok_state;
+  P.tok_cost = d->tok_cost;
+  P.tok_info = d->tok_info;
+  P.tok_cap = d->tok_cap;
+  P.flog_state = d->flog_state;
+  P.flog_cost = d->flog_cost;
+  P.flog_info = d->flog_info;
+  P.flog_cap = d->flog_cap;
+  P.all_list = d->all_list;
+  P.app_list = d->app_list;
+  P.scr_key = d->scr_key;
+  P.scr_slot = d->scr_slot;
+  P.arena = d->arena;
+  P.arena_cap = d->arena_cap;
+  P.path_rec = d->path_rec;
+  P.path_words = d->path_words;
+  P.path_cap = d->path_cap;
+}
+
+static int pick_block(int n) {
+  const char *env = getenv("AB_BLOCK");
+  if (env) {
+    int b = atoi(env);
+    if (b == 128 || b == 256 || b == 512) return b;
+  }
+  if (n >= 512) return 128;
+  if (n >= 148) return 256;
+  return 512;
+}
+
+template <int BLOCK, typename W, typename S>
+static cudaError_t launch_decode(const DecodeParams &P, int grid, size_t smem, cudaStream_t st) {
+  decode_kernel<BLOCK, W, S><<<grid, BLOCK, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename W, typename S>
+static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, size_t smem,
+                                   cudaStream_t st) {
+  switch (block) {
+  case 128: return launch_decode<128, W, S>(P, grid, smem, st);
+  case 256: return launch_decode<256, W, S>(P, grid, smem, st);
+  default: return launch_decode<512, W, S>(P, grid, smem, st);
+  }
+}
+
+template <int BLOCK, typename W, typename S>
+static cudaError_t launch_hyp(const DecodeParams &P, int which, size_t smem, cudaStream_t st) {
+  hyp_kernel<BLOCK, W, S><<<1, BLOCK, smem, st>>>(P, which);
+  return cudaGetLastError();
+}
+
+// Packs the per-channel hypothesis rows and word regions into contiguous
+// buffers (one D2H each); words_off is rewritten to the packed offset.
+__global__ void pack_kernel(int n, const int *n_hyps, const long long *wused, const DevHyp *hyps,
+                            int hyp_stride, const int *words, long long words_stride,
+                            DevHyp *out_h, int *out_w, long long *offs) {
+  const int b = blockIdx.x;
+  __shared__ long long sh_h, sh_w;
+  if (threadIdx.x == 0) {
+    sh_h = 0;
+    sh_w = 0;
+  }
+  __syncthreads();
+  long long ph = 0, pw = 0;
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    ph += n_hyps[c];
+    pw += wused[c];
+  }
+  atomicAdd((unsigned long long *)&sh_h, (unsigned long long)ph);
+  atomicAdd((unsigned long long *)&sh_w, (unsigned long long)pw);
+  __syncthreads();
+  const long long hb = sh_h, wb = sh_w;
+  const int nh = n_hyps[b];
+  const long long nw = wused[b];
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+    DevHyp h = hyps[(size_t)b * hyp_stride + i];
+    h.words_off = wb + (h.words_off - (long long)b * words_stride);
+    out_h[hb + i] = h;
+  }
+  for (long long i = threadIdx.x; i < nw; i += blockDim.x)
+    out_w[wb + i] = words[(size_t)b * words_stride + i];
+  if (threadIdx.x == 0) {
+    offs[2 * b] = hb;
+    offs[2 * b + 1] = wb;
+  }
+}
+
+static size_t dyn_smem(int L, bool s64) {
+  size_t row = (size_t)L * (s64 ? 8 : 4);
+  if (row > (size_t)SCORE_SMEM_MAX_BYTES) row = 0;
+  return CTX_SMEM_MAX * sizeof(u32) + row;
+}
+
+extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
+  if (!d || !a) return fail(AB_ERR_INVALID, "null argument");
+  ab_graph *g = d->g;
+  const int n = a->n;
+  if (n < 0) return fail(AB_ERR_INVALID, "negative batch size");
+  d->res_nhyps.assign(n, 0);
+  d->res_err.assign(n, 0);
+  d->res_hyps.assign(n, {});
+  d->res_words.assign(n, {});
+  d->last_ms = 0.f;
+  d->last_launches = 0;
+  if (n == 0) return AB_OK;
+  if (a->width != g->L)
+    return fail(AB_ERR_WIDTH, "frame width %d does not match the graph's emitting-label count %d",
+                a->width, g->L);
+  if (a->scores_dtype != AB_F32 && a->scores_dtype != AB_F64)
+    return fail(AB_ERR_INVALID, "scores_dtype must be AB_F32 or AB_F64");
+  const ab_config &cf = a->config;
+  if (!(cf.beam > 0)) return fail(AB_ERR_INVALID, "beam must be positive");
+  if (cf.max_active < 1) return fail(AB_ERR_INVALID, "max_active must be >= 1");
+  if (cf.partial_every < 1) return fail(AB_ERR_INVALID, "partial_every must be >= 1");
+  if (cf.max_epsilon_expansion < 0 || cf.max_epsilon_expansion > 255)
+    return fail(AB_ERR_INVALID, "max_epsilon_expansion must be in [0, 255]");
+  std::vector<int> slots(a->channels, a->channels + n), frames(a->frames, a->frames + n);
+  std::vector<long long> soff(a->score_offsets, a->score_offsets + n);
+  int64_t maxT = 0, rows = 0;
+  for (int i = 0; i < n; ++i) {
+    int rc;
+    if ((rc = check_slot(d, slots[i]))) return rc;
+    if (frames[i] < 0) return fail(AB_ERR_INVALID, "negative frame count");
+    maxT = std::max<int64_t>(maxT, frames[i]);
+    rows = std::max<int64_t>(rows, (soff[i] / std::max(1, g->L)) + frames[i]);
+  }
+  {
+    std::vector<int> s2 = slots;
+    std::sort(s2.begin(), s2.end());
+    if (std::adjacent_find(s2.begin(), s2.end()) != s2.end())
+      return fail(AB_ERR_INVALID, "a channel appears twice in one batch");
+  }
+  CK(cudaSetDevice(g->device));
+  cudaStream_t st = a->stream ? (cudaStream_t)a->stream : g->stream;
+  const bool s64 = a->scores_dtype == AB_F64;
+  const size_t esz = s64 ? 8 : 4;
+  const void *scores = a->scores;
+  int rc;
+  if (!a->scores_on_device) {
+    // e2e path: host rows -> device staging inside the call
+    size_t need = (size_t)rows * g->L * esz;
+    if ((rc = grow((unsigned char **)&d->d_stage, d->stage_cap, need, d->bytes))) return rc;
+    if (need) CK(cudaMemcpyAsync(d->d_stage, a->scores, need, cudaMemcpyHostToDevice, st));
+    scores = d->d_stage;
+  }
+  if ((rc = ensure_batch(d, n))) return rc;
+  const int stream_mode = a->mode == AB_MODE_STREAM;
+  const int hyp_stride = stream_mode ? 2 * (int)std::min<int64_t>(maxT, 1 << 20) + 2 : 1;
+  const long long words_stride = stream_mode ? 2ll * d->path_cap + 1024 : 1;
+  if ((rc = grow(&d->d_hyps, d->hyps_cap, (size_t)n * hyp_stride, d->bytes)) ||
+      (rc = grow(&d->d_words, d->words_cap, (size_t)n * words_stride, d->bytes)))
+    return rc;
+  DecodeParams P;
+  fill_params(d, P);
+  P.scores = scores;
+  P.mode = a->mode;
+  P.beam = cf.beam;
+  P.max_active = cf.max_active;
+  P.max_eps = cf.max_epsilon_expansion;
+  P.partial_every = cf.partial_every;
+  P.endpoint_silence_frames = cf.endpoint_silence_frames;
+  P.silence_ilabel = cf.silence_ilabel;
+  P.hyps = d->d_hyps;
+  P.hyp_stride = hyp_stride;
+  P.n_hyps = d->d_nhyps;
+  P.errors = d->d_errors;
+  P.frames_done = d->d_done;
+  P.words = d->d_words;
+  P.words_stride = words_stride;
+  P.words_used = d->d_wused;
+  P.slots = d->d_slots;
+  P.frames = d->d_frames;
+  P.score_off = d->d_soff;
+  const size_t smem = dyn_smem(g->L, s64);
+  // active set: channels with frames left (all, on the first launch)
+  std::vector<int> act(n);
+  for (int i = 0; i < n; ++i) act[i] = i;
+  std::vector<int> remaining = frames;
+  std::vector<long long> cur_off = soff;
+  std::vector<int> hn, he, hd;
+  std::vector<long long> hw, hoffs;
+  std::vector<DevHyp> ph;
+  std::vector<int> pw;
+  float total_ms = 0.f;
+  while (!act.empty()) {
+    const int m = (int)act.size();
+    std::vector<int> ls(m), lf(m);
+    std::vector<long long> lo(m);
+    for (int j = 0; j < m; ++j) {
+      ls[j] = slots[act[j]];
+      lf[j] = remaining[act[j]];
+      lo[j] = cur_off[act[j]];
+    }
+    CK(cudaMemcpyAsync(d->d_slots, ls.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->d_frames, lf.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d->d_soff, lo.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d->d_wused, 0, m * sizeof(long long), st));
+    P.n = m;
+    const int block = pick_block(m);
+    CK(cudaEventRecord(d->ev0, st));
+    cudaError_t le;
+    if (g->w32) le = s64 ? launch_decode_b<float, double>(block, P, m, smem, st)
+                         : launch_decode_b<float, float>(block, P, m, smem, st);
+    else le = s64 ? launch_decode_b<double, double>(block, P, m, smem, st)
+                  : launch_decode_b<double, float>(block, P, m, smem, st);
+    if (le != cudaSuccess) return fail(AB_ERR_CUDA, "decode launch: %s", cudaGetErrorString(le));
+    d->last_launches += 1;
+    CK(cudaEventRecord(d->ev1, st));
+    // pack + read back
+    hn.resize(m);
+    he.resize(m);
+    hd.resize(m);
+    hw.resize(m);
+    CK(cudaMemcpyAsync(hn.data(), d->d_nhyps, m * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hw.data(), d->d_wused, m * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, d->ev0, d->ev1);
+    total_ms += ms;
+    long long th = 0, tw = 0;
+    for (int j = 0; j < m; ++j) {
+      th += hn[j];
+      tw += hw[j];
+    }
+    if ((rc = grow(&d->d_packh, d->packh_cap, (size_t)std::max<long long>(th, 1), d->bytes)) ||
+        (rc = grow(&d->d_packw, d->packw_cap, (size_t)std::max<long long>(tw, 1), d->bytes)))
+      return rc;
+    pack_kernel<<<m, 128, 0, st>>>(m, d->d_nhyps, d->d_wused, d->d_hyps, hyp_stride, d->d_words,
+                                   words_stride, d->d_packh, d->d_packw, d->d_packoff);
+    CK(cudaGetLastError());
+    d->last_launches += 1;
+    ph.resize(std::max<long long>(th, 1));
+    pw.resize(std::max<long long>(tw, 1));
+    hoffs.resize(2 * m);
+    if (th) CK(cudaMemcpyAsync(ph.data(), d->d_packh, th * sizeof(DevHyp), cudaMemcpyDeviceToHost, st));
+    if (tw) CK(cudaMemcpyAsync(pw.data(), d->d_packw, tw * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hoffs.data(), d->d_packoff, 2 * m * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(he.data(), d->d_errors, m * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hd.data(), d->d_done, m * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> next;
+    for (int j = 0; j < m; ++j) {
+      const int i = act[j];
+      auto &H = d->res_hyps[i];
+      auto &Wv = d->res_words[i];
+      const long long hb = hoffs[2 * j], wb = hoffs[2 * j + 1];
+      for (int q = 0; q < hn[j]; ++q) {
+        const DevHyp &x = ph[hb + q];
+        ab_hyp y;
+        y.cost = x.cost;
+        y.frame = x.frame;
+        y.kind = x.kind;
+        y.fallback = x.fallback;
+        y.hits = x.hits;
+        y.shared = x.shared;
+        y.n_words = x.n_words;
+        y.pad_ = 0;
+        y.words_off = (int64_t)Wv.size() + (x.words_off - wb);
+        H.push_back(y);
+      }
+      Wv.insert(Wv.end(), pw.begin() + wb, pw.begin() + wb + hw[j]);
+      d->res_nhyps[i] += hn[j];
+      if (he[j]) {
+        d->res_err[i] = he[j];
+        continue;
+      }
+      remaining[i] -= hd[j];
+      cur_off[i] += (long long)hd[j] * g->L;
+      if (remaining[i] > 0) next.push_back(i);
+    }
+    act.swap(next);
+  }
+  d->last_ms = total_ms;
+  return AB_OK;
+}
+
+extern "C" int ab_read_results(ab_decoder *d, int32_t *n_hyps, int32_t *errors, ab_hyp *hyps,
+                               int32_t hyp_stride, int32_t *words, int64_t words_cap,
+                               int64_t *words_used) {
+  if (!d) return fail(AB_ERR_INVALID, "null decoder");
+  const int n = (int)d->res_nhyps.size();
+  int64_t wpos = 0;
+  for (int i = 0; i < n; ++i) {
+    if (n_hyps) n_hyps[i] = d->res_nhyps[i];
+    if (errors) errors[i] = d->res_err[i];
+    wpos += (int64_t)d->res_words[i].size();
+  }
+  if (words_used) *words_used = wpos;
+  if (!hyps && !words) return AB_OK;
+  if (words && wpos > words_cap) return fail(AB_ERR_CAPACITY, "words buffer too small (%lld)", (long long)wpos);
+  int64_t wbase = 0;
+  for (int i = 0; i < n; ++i) {
+    const auto &H = d->res_hyps[i];
+    if (hyps) {
+      if ((int)H.size() > hyp_stride) return fail(AB_ERR_CAPACITY, "hyp_stride too small");
+      for (size_t q = 0; q < H.size(); ++q) {
+        ab_hyp y = H[q];
+        y.words_off += wbase;
+        hyps[(size_t)i * hyp_stride + q] = y;
+      }
+    }
+    if (words && !d->res_words[i].empty())
+      memcpy(words + wbase, d->res_words[i].data(), d->res_words[i].size() * sizeof(int32_t));
+    wbase += (int64_t)d->res_words[i].size();
+  }
+  return AB_OK;
+}
+
+static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *words,
+                   int32_t words_cap) {
+  int rc;
+  if ((rc = check_slot(d, ch))) return rc;
+  ab_graph *g = d->g;
+  CK(cudaSetDevice(g->device));
+  if ((rc = ensure_batch(d, 1))) return rc;
+  const long long words_stride = std::max<long long>(d->path_cap, 1);
+  if ((rc = grow(&d->d_hyps, d->hyps_cap, 1, d->bytes)) ||
+      (rc = grow(&d->d_words, d->words_cap, (size_t)words_stride, d->bytes)))
+    return rc;
+  cudaStream_t st = g->stream;
+  DecodeParams P;
+  fill_params(d, P);
+  P.n = 1;
+  P.slots = d->d_slots;
+  P.hyps = d->d_hyps;
+  P.hyp_stride = 1;
+  P.n_hyps = d->d_nhyps;
+  P.errors = d->d_errors;
+  P.frames_done = d->d_done;
+  P.words = d->d_words;
+  P.words_stride = words_stride;
+  P.words_used = d->d_wused;
+  CK(cudaMemcpyAsync(d->d_slots, &ch, sizeof(int), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d->d_wused, 0, sizeof(long long), st));
+  const size_t smem = CTX_SMEM_MAX * sizeof(u32);
+  cudaError_t le = g->w32 ? launch_hyp<256, float, float>(P, which, smem, st)
+                          : launch_hyp<256, double, float>(P, which, smem, st);
+  if (le != cudaSuccess) return fail(AB_ERR_CUDA, "hypothesis launch: %s", cudaGetErrorString(le));
+  int err = 0, nh = 0;
+  long long nw = 0;
+  DevHyp h;
+  CK(cudaMemcpyAsync(&err, d->d_errors, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nh, d->d_nhyps, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nw, d->d_wused, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h, d->d_hyps, sizeof(DevHyp), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err == AB_ERR_DEAD) return fail(AB_ERR_DEAD, "decode failure, no active tokens");
+  if (err == AB_ERR_STATUS) return fail(AB_ERR_STATUS, "cannot finalize in this status");
+  if (err) return fail(err, "device error %d", err);
+  if (nw > words_cap) return fail(AB_ERR_CAPACITY, "words buffer too small");
+  if (nw) CK(cudaMemcpy(words, d->d_words, nw * sizeof(int), cudaMemcpyDeviceToHost));
+  hyp->cost = h.cost;
+  hyp->frame = h.frame;
+  hyp->kind = h.kind;
+  hyp->fallback = h.fallback;
+  hyp->hits = h.hits;
+  hyp->shared = h.shared;
+  hyp->n_words = h.n_words;
+  hyp->pad_ = 0;
+  hyp->words_off = 0;
+  return AB_OK;
+}
+
+extern "C" int ab_partial(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words,
+                          int32_t words_cap) {
+  return one_hyp(d, ch, AB_PARTIAL, hyp, words, words_cap);
+}
+
+extern "C" int ab_finalize(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words,
+                           int32_t words_cap) {
+  return one_hyp(d, ch, AB_FINAL, hyp, words, words_cap);
+}
+
+extern "C" int ab_last_kernel_ms(ab_decoder *d, float *ms) {
+  if (!d) return fail(AB_ERR_INVALID, "null decoder");
+  *ms = d->last_ms;
+  return AB_OK;
+}
+
+extern "C" int ab_last_launch_count(ab_decoder *d, int32_t *launches) {
+  if (!d) return fail(AB_ERR_INVALID, "null decoder");
+  *launches = d->last_launches;
+  return AB_OK;
+}

@@ -1,0 +1,195 @@
+"""Graph types consumed by the decode path.
+
+Only what the hot path needs is provided: the CSR layout whose global arc
+index space contexts refer to (``CsrFst``, reference fst.py:116-162), its
+builder from an adjacency list (``build_csr``, fst.py:165-191), the graph
+fingerprint (fst.py:194-201) and a minimal text reader so tests and tools can
+state small graphs the way the reference's tests do (fst.py:204-275).  Any
+object exposing the ``CsrFst`` attributes (including the reference's own
+``arcboost.fst.CsrFst``) is accepted by the decoder.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+from typing import Iterable
+
+import numpy as np
+
+EPSILON = 0
+
+
+class FstError(ValueError):
+    """Malformed graph input."""
+
+
+@dataclass(frozen=True)
+class Arc:
+    ilabel: int
+    olabel: int
+    next_state: int
+    weight: float
+
+
+@dataclass
+class Fst:
+    """Adjacency list; arc order inside a state fixes the global arc index."""
+
+    start: int
+    num_states: int
+    arcs: list
+    finals: dict
+
+    def __post_init__(self) -> None:
+        if len(self.arcs) != self.num_states:
+            raise FstError("arc table length != num_states")
+        if self.num_states and not 0 <= self.start < self.num_states:
+            raise FstError(f"start state {self.start} out of range for {self.num_states} states")
+        for s, out in enumerate(self.arcs):
+            for a in out:
+                if not 0 <= a.next_state < self.num_states:
+                    raise FstError(f"arc from state {s} to nonexistent state {a.next_state}")
+                if a.ilabel < 0 or a.olabel < 0:
+                    raise FstError(f"negative label on arc from state {s}")
+                if not math.isfinite(a.weight):
+                    raise FstError(f"non-finite weight on arc from state {s}")
+
+    @property
+    def num_arcs(self) -> int:
+        return sum(len(out) for out in self.arcs)
+
+    def fingerprint(self) -> str:
+        return graph_fingerprint(
+            self.start, self.num_states,
+            ((a.ilabel, a.olabel, a.next_state, a.weight) for out in self.arcs for a in out),
+            self.finals)
+
+
+def graph_fingerprint(start, num_states, arc_tuples, finals) -> str:
+    """Same digest as the reference (fst.py:194-201), so a registry compiled
+    against a graph by the reference validates against this package's CSR."""
+    h = hashlib.sha256()
+    h.update(f"{start} {num_states}\n".encode())
+    for il, ol, dst, w in arc_tuples:
+        h.update(f"{il} {ol} {dst} {w!r}\n".encode())
+    for s in sorted(finals):
+        h.update(f"f {s} {finals[s]!r}\n".encode())
+    return h.hexdigest()
+
+
+@dataclass
+class CsrFst:
+    """State-major CSR; the arc at global index g belongs to state s iff
+    row_offsets[s] <= g < row_offsets[s + 1] (reference fst.py:116-162)."""
+
+    start: int
+    row_offsets: np.ndarray
+    ilabels: np.ndarray
+    olabels: np.ndarray
+    next_states: np.ndarray
+    weights: np.ndarray
+    finals: dict
+    _fingerprint: str | None = field(default=None, repr=False)
+
+    @property
+    def num_states(self) -> int:
+        return len(self.row_offsets) - 1
+
+    @property
+    def num_arcs(self) -> int:
+        return int(self.row_offsets[-1])
+
+    @property
+    def num_emitting_labels(self) -> int:
+        return int(self.ilabels.max()) if len(self.ilabels) else 0
+
+    @property
+    def fingerprint(self) -> str:
+        # computed lazily: hashing 2e7 arcs in Python takes tens of seconds
+        if self._fingerprint is None:
+            self._fingerprint = graph_fingerprint(
+                self.start, self.num_states,
+                zip(self.ilabels.tolist(), self.olabels.tolist(), self.next_states.tolist(),
+                    self.weights.tolist()),
+                self.finals)
+        return self._fingerprint
+
+    @fingerprint.setter
+    def fingerprint(self, v: str) -> None:
+        self._fingerprint = v
+
+    def arc_range(self, state: int) -> tuple[int, int]:
+        return int(self.row_offsets[state]), int(self.row_offsets[state + 1])
+
+
+def csr_from_arrays(start, row_offsets, ilabels, olabels, next_states, weights, finals,
+                    fingerprint: str | None = None) -> CsrFst:
+    return CsrFst(
+        start=int(start),
+        row_offsets=np.ascontiguousarray(row_offsets, dtype=np.int64),
+        ilabels=np.ascontiguousarray(ilabels, dtype=np.int64),
+        olabels=np.ascontiguousarray(olabels, dtype=np.int64),
+        next_states=np.ascontiguousarray(next_states, dtype=np.int64),
+        weights=np.ascontiguousarray(weights, dtype=np.float64),
+        finals=dict(finals),
+        _fingerprint=fingerprint,
+    )
+
+
+def build_csr(fst: Fst) -> CsrFst:
+    """Lay the adjacency list out state-major, arc order preserved (fst.py:165-191)."""
+    counts = np.array([len(out) for out in fst.arcs], dtype=np.int64)
+    offs = np.zeros(fst.num_states + 1, dtype=np.int64)
+    np.cumsum(counts, out=offs[1:])
+    flat = [a for out in fst.arcs for a in out]
+    return CsrFst(
+        start=fst.start,
+        row_offsets=offs,
+        ilabels=np.array([a.ilabel for a in flat], dtype=np.int64),
+        olabels=np.array([a.olabel for a in flat], dtype=np.int64),
+        next_states=np.array([a.next_state for a in flat], dtype=np.int64),
+        weights=np.array([a.weight for a in flat], dtype=np.float64),
+        finals=dict(fst.finals),
+        _fingerprint=fst.fingerprint(),
+    )
+
+
+def parse_text_fst(text: str | Iterable[str]) -> Fst:
+    """OpenFst-style text: ``src dst ilabel olabel [weight]`` arc lines and
+    ``state [weight]`` final lines; the first line names the start state."""
+    lines = text.splitlines() if isinstance(text, str) else list(text)
+    start = None
+    arcs_in: list[tuple[int, Arc]] = []
+    finals: dict[int, float] = {}
+    top = -1
+    for n, raw in enumerate(lines, 1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        f = line.split()
+        try:
+            if len(f) in (4, 5):
+                s, d, il, ol = (int(x) for x in f[:4])
+                w = float(f[4]) if len(f) == 5 else 0.0
+                arcs_in.append((s, Arc(il, ol, d, w)))
+                top = max(top, s, d)
+            elif len(f) in (1, 2):
+                s = int(f[0])
+                if s in finals:
+                    raise ValueError(f"duplicate final line for state {s}")
+                finals[s] = float(f[1]) if len(f) == 2 else 0.0
+                top = max(top, s)
+            else:
+                raise ValueError(f"expected 1, 2, 4 or 5 fields, got {len(f)}")
+        except ValueError as exc:
+            raise FstError(f"line {n}: {exc}: {raw!r}") from None
+        if start is None:
+            start = int(f[0])
+    if start is None:
+        raise FstError("no start state: input contains no arc or final lines")
+    adj: list[list[Arc]] = [[] for _ in range(top + 1)]
+    for s, a in arcs_in:
+        adj[s].append(a)
+    return Fst(start=start, num_states=top + 1, arcs=adj, finals=finals)

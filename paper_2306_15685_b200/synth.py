@@ -1,0 +1,116 @@
+"""Synthetic inputs for the BASELINE configs.
+
+``benchmark_graph`` reproduces the reference's ``build_benchmark_graph``
+(arcboost/synth.py:294-322) draw for draw, but returns the CSR arrays directly
+(vectorised; the reference builds Python Arc objects, which does not scale to
+2e7 arcs).  tests/test_synth_golden.py pins the arrays against the reference.
+With ``f32_weights`` the weights are rounded once to float32 so the device can
+store 4-byte weights while accumulating bit-exactly in f64; the same rounded
+arrays are what the CPU oracle sees.
+"""
+
+from __future__ import annotations
+
+import random
+
+import numpy as np
+
+from .biasing import BiasingContext
+from .fst import CsrFst, csr_from_arrays
+
+
+def benchmark_graph(num_states: int, arcs_per_state: int, num_labels: int, *,
+                    eps_input_frac: float = 0.1, seed: int = 421,
+                    f32_weights: bool = False) -> CsrFst:
+    rng = np.random.default_rng(seed)
+    n = num_states * arcs_per_state
+    dsts = rng.integers(0, num_states, size=n)
+    ilabels = rng.integers(1, num_labels + 1, size=n)
+    eps_in = rng.random(n) < eps_input_frac
+    ilabels[eps_in] = 0
+    olabels = rng.integers(0, num_labels + 1, size=n)
+    weights = rng.uniform(0.0, 3.0, size=n)
+    ilabels[:num_labels] = np.arange(1, num_labels + 1)
+    if f32_weights:
+        weights = weights.astype(np.float32).astype(np.float64)
+    row_offsets = np.arange(0, n + 1, arcs_per_state, dtype=np.int64)
+    finals = (np.arange(num_states, dtype=np.int64), np.zeros(num_states))
+    csr = csr_from_arrays(0, row_offsets, ilabels, olabels, dsts, weights, {})
+    csr.finals = _AllFinal(num_states)
+    return csr
+
+
+class _AllFinal(dict):
+    """finals = {s: 0.0 for every state} without materialising 5e6 dict entries
+    until someone iterates it (the device upload uses the array form)."""
+
+    def __init__(self, n: int):
+        super().__init__()
+        self._n = n
+        self._filled = False
+
+    def _fill(self):
+        if not self._filled:
+            super().update({s: 0.0 for s in range(self._n)})
+            self._filled = True
+
+    def as_arrays(self):
+        return np.arange(self._n, dtype=np.int32), np.zeros(self._n, dtype=np.float64)
+
+    def __len__(self):
+        return self._n
+
+    def __contains__(self, s):
+        return 0 <= int(s) < self._n
+
+    def __getitem__(self, s):
+        if s in self:
+            return 0.0
+        raise KeyError(s)
+
+    def get(self, s, default=None):
+        return 0.0 if s in self else default
+
+    def __iter__(self):
+        return iter(range(self._n))
+
+    def keys(self):
+        return range(self._n)
+
+    def values(self):
+        return (0.0 for _ in range(self._n))
+
+    def items(self):
+        return ((s, 0.0) for s in range(self._n))
+
+    def copy(self):
+        self._fill()
+        return dict(self)
+
+
+def channel_scores(seed: int, channel: int, frames: int, width: int,
+                   dtype=np.float32) -> np.ndarray:
+    """Acoustic costs U[0, 6) of one channel from default_rng([seed, channel])
+    (random_scores' range, synth.py:69-75; [seed, i] streams, harness.py:374)."""
+    x = np.random.default_rng([seed, channel]).uniform(0.0, 6.0, (frames, width))
+    return x.astype(dtype) if dtype != np.float64 else x
+
+
+def unigram_context(csr, num_words: int, ctx_seed: int, *, num_labels: int,
+                    discount: float = -2.0, ctx_id: str | None = None) -> BiasingContext:
+    """Context of single-word entities: exactly the arcs whose olabel is one of
+    the chosen words (single-word completeness of Alg. 1)."""
+    words = random.Random(ctx_seed).sample(range(1, num_labels + 1), num_words)
+    idx = np.flatnonzero(np.isin(np.asarray(csr.olabels), np.asarray(words)))
+    return BiasingContext(id=ctx_id or f"ctx{ctx_seed}", arc_indices=idx.astype(np.int64),
+                          discount=discount)
+
+
+def dense_context(csr, fraction: float, ctx_seed: int, *, discount: float = -2.0,
+                  ctx_id: str | None = None) -> BiasingContext:
+    """Context boosting a uniform random ``fraction`` of all arcs (ATC-style)."""
+    rng = np.random.default_rng([ctx_seed, 77])
+    n = csr.num_arcs if hasattr(csr, "num_arcs") else int(csr.row_offsets[-1])
+    k = int(round(fraction * n))
+    idx = np.sort(rng.choice(n, size=k, replace=False)).astype(np.int64)
+    return BiasingContext(id=ctx_id or f"dense{ctx_seed}", arc_indices=idx, discount=discount)

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the package API / C ABI) against the
+reference's golden fixtures and the CPU oracle on identical inputs.
+
+Bar (BASELINE.json north_star): identical words and boosted-arc hits, costs
+within 1e-4 relative.  Costs accumulate in f64 in the reference's operation
+order, so the tests below require bit-identical costs (a stricter bar).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import case_inputs, expect_hyps, fx, load_json
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL = 1e-4  # north-star tolerance; asserted in addition to bit equality
+
+
+def _decode(csr, scores, ctx, cfg, ch_id="c"):
+    import paper_2306_15685_b200 as ab
+
+    reg = None
+    if ctx is not None:
+        reg = ab.ContextRegistry({ctx.id: ctx}, graph_fingerprint="")
+    ch = ab.init_channel(ch_id, reg, ctx.id if ctx is not None else None, cfg)
+    res = ab.decode_batch([(ch, ab.ScoreMatrix(scores))], csr, reg, cfg)[0]
+    return res, ch
+
+
+def _oracle(csr, scores, ctx, cfg):
+    from oracle.oracle import OracleChannel, OracleGraph, decode_stream
+
+    og = OracleGraph.from_csr(csr)
+    ch = OracleChannel(og)
+    hyps, rc = decode_stream(og, np.asarray(scores, dtype=np.float64), ctx, cfg, channel=ch)
+    return hyps, rc, ch.info()
+
+
+def _same(got, want, where=""):
+    assert len(got) == len(want), where
+    for a, b in zip(got, want):
+        assert a.words == b.words, where
+        assert a.kind == b.kind and a.frame == b.frame and a.fallback == b.fallback, where
+        assert a.cost == pytest.approx(b.cost, rel=COST_RTOL, abs=1e-9), where
+        assert a.cost == b.cost, where  # bit-exact f64
+        assert a.hits == b.hits, where
+
+
+def test_small_cases_match_reference(small_cases):
+    """400+ reference-generated instances: ties, epsilon cycles, negative
+    weights, max_active binding, epsilon caps, endpointing, dead channels."""
+    for c in small_cases:
+        csr, scores, ctx, cfg = case_inputs(c)
+        res, ch = _decode(csr, scores, ctx, cfg)
+        e = c["expect"]
+        if e["error"] is not None:
+            assert res.error is not None, c["name"]
+            assert ("no active tokens" in res.error) == ("no active tokens" in e["error"]), c["name"]
+            continue
+        assert res.error is None, (c["name"], res.error)
+        got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
+        assert got == expect_hyps(e), c["name"]
+        assert ch.utterance_index == e["utterance_index"], c["name"]
+        assert ch.eps_truncations == e["eps_truncations"], c["name"]
+        assert len(ch.store) == e["store_len"], c["name"]
+        hyps, rc, _ = _oracle(csr, scores, ctx, cfg)
+        assert [h.hits for h in res.hypotheses] == [h.hits for h in hyps], c["name"]
+
+
+@pytest.mark.parametrize("variant", ["f32", "f64"])
+def test_c1_full_reference_run(variant):
+    """C1: G_small, 1 channel x 500 frames, 20-word context, beam 13 - the exact
+    run the reference decoded (golden), f32-stored or f64-stored weights."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    g = load_json("c1_small.json")
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=(variant == "f32"))
+    ctx = ab.BiasingContext("ctx1", np.array(g["ctx_arcs"], dtype=np.int64), -2.0)
+    cfg = ab.DecoderConfig(**g["cfg"])
+    scores = np.random.default_rng([7, 0]).uniform(0.0, 6.0, (500, 2000))
+    if variant == "f32":
+        scores = scores.astype(np.float32)
+    res, ch = _decode(csr, scores, ctx, cfg)
+    assert res.error is None, res.error
+    e = g["runs"][variant]
+    got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
+    assert got == expect_hyps(e)
+    assert len(ch.store) == e["store_len"]
+    hyps, rc, _ = _oracle(csr, scores, ctx, cfg)
+    _same(res.hypotheses, hyps)
+    dg = ab.device_graph(csr)
+    assert dg.weights_f32 == (variant == "f32")
+
+
+def test_c2_subset_partials_every_frame():
+    """C2 shape: G_small, 64 channels, each with its own 20-word context,
+    partial hypotheses every frame (100 frames here; the bench runs 500)."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=1)
+    ctxs = {f"k{c}": synth.unigram_context(csr, 20, c, num_labels=2000, ctx_id=f"k{c}")
+            for c in range(64)}
+    reg = ab.ContextRegistry(ctxs, graph_fingerprint="")
+    mats = [synth.channel_scores(11, c, 100, 2000) for c in range(64)]
+    pairs = [(ab.init_channel(f"ch{c}", reg, f"k{c}", cfg), ab.ScoreMatrix(mats[c]))
+             for c in range(64)]
+    res = ab.decode_batch(pairs, csr, reg, cfg)
+    for c in range(0, 64, 9):
+        assert res[c].error is None
+        hyps, rc, _ = _oracle(csr, mats[c], ctxs[f"k{c}"], cfg)
+        assert rc == 0
+        _same(res[c].hypotheses, hyps, f"channel {c}")
+
+
+def test_per_frame_token_sets_match_oracle():
+    """advance_frame one frame at a time: the surviving token set (states,
+    costs, hits) equals the oracle's after every frame, with max_active binding."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+    from oracle.oracle import OracleChannel, OracleGraph
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 3, num_labels=2000)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=3000)
+    og = OracleGraph.from_csr(csr)
+    och = OracleChannel(og)
+    ch = ab.init_channel("t", None, None, cfg)
+    scores = synth.channel_scores(5, 0, 40, 2000)
+    for t in range(40):
+        ab.advance_frame(ch, scores[t], csr, ctx, cfg)
+        och.advance(scores[t].astype(np.float64), ctx, cfg)
+        st, co, hi = och.tokens()
+        toks = ch.active_tokens()
+        assert [x.state for x in toks] == st.tolist(), t
+        assert [x.cost for x in toks] == co.tolist(), t
+        assert [x.hits for x in toks] == hi.tolist(), t
+        info = och.info()
+        assert ch.trailing_silence == info["trailing_silence"]
+        assert ch.eps_truncations == info["eps_truncations"]
+        assert len(ch.store) == info["store_len"]
+        if t % 7 == 3:
+            p = ab.partial_hypothesis(ch)
+            q = och.partial()
+            assert p.words == q.words and p.cost == q.cost and p.hits == q.hits
+    f = ab.finalize(ch, csr)
+    q = och.finalize()
+    assert f.words == q.words and f.cost == q.cost and f.fallback == q.fallback
+
+
+@pytest.mark.parametrize("mode", ["list", "bitset"])
+def test_context_representations_agree(mode):
+    """Sparse contexts (shared-memory sorted list) and dense ones (HBM bitset)
+    give identical decodes; a 5%-dense context is checked against the oracle."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import _lib, synth
+    from paper_2306_15685_b200.device import BatchDecoder, DeviceGraph
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.dense_context(csr, 0.05, 9) if mode == "bitset" else \
+        synth.unigram_context(csr, 20, 9, num_labels=2000)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
+    scores = synth.channel_scores(3, 1, 60, 2000)
+    dg = DeviceGraph(csr)
+    h = dg.register_context(ctx.arc_indices, ctx.discount,
+                            _lib.AB_CTX_BITSET if mode == "bitset" else _lib.AB_CTX_LIST)
+    dec = BatchDecoder(dg, 1)
+    dec.init_channel(0, h)
+    dec.decode([0], [60], [0], np.ascontiguousarray(scores), 2000, cfg, _lib.AB_MODE_STREAM)
+    nh, er, hyps, stride, words = dec.results(1)
+    assert er[0] == 0
+    want, rc, _ = _oracle(csr, scores, ctx, cfg)
+    last = []
+    got = []
+    for q in range(nh[0]):
+        x = hyps[q]
+        w = last[:x.shared] + words[x.words_off:x.words_off + x.n_words - x.shared].tolist()
+        last = w if x.kind == 0 else []
+        got.append((w, x.cost, x.hits))
+    assert got == [(h.words, h.cost, h.hits) for h in want]
+
+
+def test_zero_discount_context_is_identity():
+    """SPEC zero-discount identity: a 0.0-discount context changes nothing."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 100, 4, num_labels=2000, discount=0.0)
+    cfg = ab.DecoderConfig(beam=13.0)
+    scores = synth.channel_scores(2, 0, 50, 2000)
+    a, _ = _decode(csr, scores, None, cfg)
+    b, _ = _decode(csr, scores, ctx, cfg)
+    assert [(h.words, h.cost) for h in a.hypotheses] == [(h.words, h.cost) for h in b.hypotheses]
+
+
+def test_context_switch_per_segment():
+    """C3 shape: 4 utterance segments per channel with a context switch at each
+    boundary (harness.py:208-242 waves)."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    pool = {f"p{i}": synth.unigram_context(csr, 20, 100 + i, num_labels=2000, ctx_id=f"p{i}")
+            for i in range(6)}
+    reg = ab.ContextRegistry(pool, graph_fingerprint="")
+    cfg = ab.DecoderConfig(beam=13.0, partial_every=10)
+    chans = [ab.init_channel(f"c{i}", reg, None, cfg) for i in range(4)]
+    for seg in range(4):
+        pairs = []
+        for i, ch in enumerate(chans):
+            ab.switch_context(ch, reg, f"p{(i + seg) % 6}")
+            pairs.append((ch, ab.ScoreMatrix(synth.channel_scores(40 + seg, i, 25, 2000))))
+        res = ab.decode_batch(pairs, csr, reg, cfg)
+        for i, r in enumerate(res):
+            assert r.error is None
+            want, rc, _ = _oracle(csr, pairs[i][1].costs, pool[f"p{(i + seg) % 6}"], cfg)
+            _same(r.hypotheses, want, f"seg {seg} ch {i}")
+        assert all(ch.utterance_index == seg + 1 for ch in chans)
+
+
+def test_g_large_subset():
+    """C3/C5 graph (5M states / 20M arcs, hashed token table): a channel subset
+    against the oracle."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(5_000_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 5, num_labels=2000)
+    reg = ab.ContextRegistry({ctx.id: ctx}, graph_fingerprint="")
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
+    mats = [synth.channel_scores(21, c, 30, 2000) for c in range(3)]
+    pairs = [(ab.init_channel(f"g{c}", reg, ctx.id if c != 1 else None, cfg), ab.ScoreMatrix(m))
+             for c, m in enumerate(mats)]
+    res = ab.decode_batch(pairs, csr, reg, cfg)
+    for c in range(3):
+        assert res[c].error is None, res[c].error
+        want, rc, _ = _oracle(csr, mats[c], ctx if c != 1 else None, cfg)
+        _same(res[c].hypotheses, want, f"channel {c}")
+
+
+def test_margin_suite_on_device():
+    """Reference margin suite: biasing flips all 50 entity decisions on the GPU."""
+    m = load_json("margin_suite.json")
+    base = {"graph": m["graph"], "cfg": m["cfg"]}
+    for u in m["utts"]:
+        for key, use_ctx in (("unbiased", False), ("biased", True)):
+            c = dict(base, scores=u["scores"], ctx=m["ctx"] if use_ctx else None)
+            csr, scores, ctx, cfg = case_inputs(c)
+            res, _ = _decode(csr, scores, ctx, cfg)
+            assert res.error is None
+            got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
+            assert got == expect_hyps(u[key]), (u["utt_id"], key)
+        assert res.hypotheses[-1].words == u["transcript"]
