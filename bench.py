@@ -199,7 +199,7 @@ def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense
             pool = [synth.dense_context(csr, dense, 2000 + i) for i in range(8)]
         else:
             n_pool = CTX_POOL if W["channels"] > 1 else 1
-            pool = [synth.unigram_context(csr, 20, 1000 + i, num_labels=L) for i in range(n_pool)]
+            pool = synth.unigram_contexts(csr, 20, range(1000, 1000 + n_pool), num_labels=L)
     t1 = time.time()
     C, T = W["channels"], W["frames"]
     scores = np.empty((C, T, L), dtype=np.float32)

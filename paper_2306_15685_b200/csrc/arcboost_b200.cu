@@ -71,6 +71,7 @@ struct ab_graph {
 
 struct ab_decoder {
   ab_graph *g = nullptr;
+  int device = 0;
   int max_ch = 0;
   ab_capacity cap{};
   u32 table_cap = 0;
@@ -89,6 +90,7 @@ struct ab_decoder {
   u64 *scr_key = nullptr;
   u32 *scr_slot = nullptr;
   int2 *arena = nullptr;
+  u32 *gc_bits = nullptr, *gc_rank = nullptr;
   int *path_rec = nullptr, *path_words = nullptr;
   // per-call buffers (grown on demand)
   size_t batch_cap = 0;
@@ -374,6 +376,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   ab_capacity cap = capin ? *capin : ab_capacity{};
   ab_decoder *d = new ab_decoder();
   d->g = g;
+  d->device = g->device;
   d->max_ch = max_channels;
   uint64_t ts = cap.table_slots;
   if (ts <= 0) ts = (g->num_states <= (1 << 20)) ? (uint64_t)g->num_states : (1ull << 17);
@@ -386,7 +389,14 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->tok_cap = d->table_cap;
   d->flog_cap = (u32)(cap.frontier_rows > 0 ? cap.frontier_rows
                                             : std::max<uint64_t>(65536, 2ull * d->table_cap));
-  d->arena_cap = (u32)(cap.arena_records > 0 ? cap.arena_records : (1ll << 22));
+  // the arena must hold the live records plus one frame of appends (<= frontier rows)
+  d->arena_cap = (u32)(cap.arena_records > 0 ? cap.arena_records
+                                             : std::max<uint64_t>(1ull << 19, 8ull * d->flog_cap));
+  d->arena_cap = (d->arena_cap + 31) & ~31u;
+  if ((uint64_t)d->arena_cap < 2ull * d->flog_cap) {
+    delete d;
+    return fail(AB_ERR_INVALID, "arena_records must be at least twice frontier_rows");
+  }
   d->path_cap = (u32)(cap.path_words > 0 ? cap.path_words : (1ll << 16));
   d->cap.table_slots = d->table_cap;
   d->cap.frontier_rows = d->flog_cap;
@@ -404,7 +414,9 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
       dmalloc(&d->app_list, C * d->table_cap, acc) ||
       dmalloc(&d->scr_key, C * d->table_cap, acc) ||
       dmalloc(&d->scr_slot, C * d->table_cap, acc) ||
-      dmalloc(&d->arena, C * d->arena_cap, acc) ||
+      dmalloc(&d->arena, 2 * C * d->arena_cap, acc) ||
+      dmalloc(&d->gc_bits, C * (d->arena_cap / 32 + 1), acc) ||
+      dmalloc(&d->gc_rank, C * (d->arena_cap / 32 + 1), acc) ||
       dmalloc(&d->path_rec, C * d->path_cap, acc) ||
       dmalloc(&d->path_words, C * d->path_cap, acc)) {
     size_t need = acc;
@@ -436,10 +448,11 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
 
 extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
-  cudaSetDevice(d->g->device);
+  cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->tok_state, d->tok_cost, d->tok_info,
                   d->flog_state, d->flog_cost, d->flog_info, d->all_list, d->app_list,
                   d->scr_key,   d->scr_slot,  d->arena,     d->path_rec, d->path_words,
+                  d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
                   d->d_soff,    d->d_wused,   d->d_hyps,    d->d_words,  d->d_packh,
                   d->d_packw,   d->d_packoff, d->d_stage, d->d_infos, d->d_islots};
@@ -481,7 +494,7 @@ extern "C" int ab_channel_init(ab_decoder *d, int32_t ch, int32_t context) {
   info.context = context;
   // the epoch and path fields stay: epochs must never repeat within a slot
   CK(cudaMemcpy(&d->chans[ch].info, &info, sizeof(info), cudaMemcpyHostToDevice));
-  int zero[2] = {0, 0};
+  int zero[4] = {0, 0, 0, 0}; // path_len, max_depth, arena_half, rec_phys
   CK(cudaMemcpy(&d->chans[ch].path_len, zero, sizeof(zero), cudaMemcpyHostToDevice));
   return AB_OK;
 }
@@ -528,6 +541,8 @@ __global__ void scatter_infos(int n, const int *slots, ChanState *chans,
     if (reset_path) {
       chans[slots[i]].path_len = 0;
       chans[slots[i]].max_depth = 0;
+      chans[slots[i]].arena_half = 0;
+      chans[slots[i]].rec_phys = 0;
     }
   }
 }
@@ -703,6 +718,8 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.scr_slot = d->scr_slot;
   P.arena = d->arena;
   P.arena_cap = d->arena_cap;
+  P.gc_bits = d->gc_bits;
+  P.gc_rank = d->gc_rank;
   P.path_rec = d->path_rec;
   P.path_words = d->path_words;
   P.path_cap = d->path_cap;
@@ -823,6 +840,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       return fail(AB_ERR_INVALID, "a channel appears twice in one batch");
   }
   CK(cudaSetDevice(g->device));
+  (void)cudaGetLastError(); // drop stale non-sticky errors of unrelated earlier calls
   cudaStream_t st = a->stream ? (cudaStream_t)a->stream : g->stream;
   const bool s64 = a->scores_dtype == AB_F64;
   const size_t esz = s64 ? 8 : 4;
@@ -1010,6 +1028,7 @@ static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *w
       (rc = grow(&d->d_words, d->words_cap, (size_t)words_stride, d->bytes)))
     return rc;
   cudaStream_t st = g->stream;
+  (void)cudaGetLastError();
   DecodeParams P;
   fill_params(d, P);
   P.n = 1;

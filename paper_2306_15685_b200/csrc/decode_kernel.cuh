@@ -68,11 +68,13 @@ template <> struct __align__(16) XArc<float> { u32 ns, g; float w; u32 pad; };
 template <> struct __align__(16) XArc<double> { u32 ns, g; double w; };
 
 struct ChanState {
-  ab_channel_info info;
+  ab_channel_info info; // info.store_len = records appended this utterance (reference len(store))
   u32 epoch;
   int path_len;
-  int max_depth; // deepest token path in the current token list
-  int pad;
+  int max_depth;  // deepest token path in the current token list
+  int arena_half; // which half of the channel's arena is live (copying GC)
+  u32 rec_phys;   // records physically in the live half
+  u32 pad[3];
 };
 
 struct DevHyp {
@@ -112,8 +114,10 @@ struct DecodeParams {
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_slot;
-  int2 *arena;
+  int2 *arena;   // [channel][2][arena_cap]: live half + GC to-space
   u32 arena_cap;
+  u32 *gc_bits;  // [channel][arena_cap / 32] mark bitmap
+  u32 *gc_rank;  // [channel][arena_cap / 32] live records before each bitmap word
   int *path_rec;
   int *path_words;
   u32 path_cap;
@@ -278,6 +282,7 @@ enum {
 struct Shared {
   // per-phase counters
   u32 n_all, n_app, n_cand, rec_n, n_keep, n_tok, flog_n;
+  unsigned long long rec_logical;
   int error;
   u32 sel;
   u32 cum;
@@ -308,7 +313,10 @@ template <typename W, typename S> struct Chan {
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_slot;
-  int2 *arena;
+  int2 *arena;   // live half
+  int2 *arena_to;
+  u32 *gc_bits;
+  u32 *gc_rank;
   int *path_rec;
   int *path_words;
   const S *row;
@@ -502,6 +510,7 @@ __device__ void snapshot(const Chan<W, S> &C, Shared &sh, u32 round, const TokIn
     ni.hits = si.hits + ((info >> 23) & 1);
     ni.last_il = round == 0 ? meta.y : si.last_il;
     if (meta.x != 0) {
+      atomicAdd(&sh.rec_logical, 1ull);
       u32 r = atomicAdd(&sh.rec_n, 1u);
       if (r < P.arena_cap) {
         C.arena[r] = make_int2(meta.x, si.bp);
@@ -763,6 +772,68 @@ __device__ void materialize_start(Chan<W, S> &C, Shared &sh) {
   __syncthreads();
 }
 
+// Copying collector for the emission arena: records reachable from the token
+// list move to the other half in arena order (ids stay monotone), everything
+// else (records of pruned or superseded tokens) is dropped.  Words never
+// change: only record ids do, so the prefix-sharing path is reset.
+template <int BLOCK, typename W, typename S>
+__device__ void gc_arena(Chan<W, S> &C, Shared &sh) {
+  const u32 n = sh.rec_n;
+  const u32 nw = (n + 31) / 32;
+  const u32 n_tok = (u32)C.cs->info.num_active;
+  for (u32 w = threadIdx.x; w < nw; w += BLOCK) C.gc_bits[w] = 0;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) {
+    int r = C.tok_info[i].bp;
+    while (r >= 0) {
+      const u32 m = 1u << (r & 31);
+      const u32 old = atomicOr(&C.gc_bits[r >> 5], m);
+      if (old & m) break;
+      r = C.arena[r].y;
+    }
+  }
+  __syncthreads();
+  u32 carry = 0;
+  for (u32 base = 0; base < nw; base += BLOCK) {
+    const u32 w = base + threadIdx.x;
+    const u32 c = w < nw ? __popc(C.gc_bits[w]) : 0u;
+    u32 total;
+    const u32 ex = block_excl_scan<BLOCK>(c, total, sh.scan);
+    if (w < nw) C.gc_rank[w] = carry + ex;
+    carry += total;
+  }
+  __syncthreads();
+  auto newid = [&](int i) -> int {
+    const u32 w = (u32)i >> 5;
+    return (int)(C.gc_rank[w] + __popc(C.gc_bits[w] & ((1u << (i & 31)) - 1u)));
+  };
+  for (u32 w = threadIdx.x; w < nw; w += BLOCK) {
+    u32 b = C.gc_bits[w];
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      const int i = (int)(w * 32 + bit);
+      const int2 r = C.arena[i];
+      C.arena_to[newid(i)] = make_int2(r.x, r.y >= 0 ? newid(r.y) : -1);
+    }
+  }
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) {
+    const int bp = C.tok_info[i].bp;
+    if (bp >= 0) C.tok_info[i].bp = newid(bp);
+  }
+  __syncthreads();
+  int2 *t = C.arena;
+  C.arena = C.arena_to;
+  C.arena_to = t;
+  if (threadIdx.x == 0) {
+    sh.rec_n = carry;
+    C.cs->arena_half ^= 1;
+    C.cs->path_len = 0;
+  }
+  __syncthreads();
+}
+
 // advance_frame (decoder.py:341-411) for frame row C.row.
 template <int BLOCK, typename W, typename S>
 __device__ void advance(Chan<W, S> &C, Shared &sh) {
@@ -772,6 +843,15 @@ __device__ void advance(Chan<W, S> &C, Shared &sh) {
     if (threadIdx.x == 0) set_error(sh, E_STATUS);
     __syncthreads();
     return;
+  }
+  // one frame appends at most flog_cap records: collect first if they might not fit
+  if (!cs->info.fresh && (unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
+    gc_arena<BLOCK>(C, sh);
+    if ((unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
+      if (threadIdx.x == 0) set_error(sh, E_CAP);
+      __syncthreads();
+      return;
+    }
   }
   if (cs->info.fresh) {
     materialize_start<BLOCK>(C, sh);
@@ -971,6 +1051,7 @@ __device__ void finalize(Chan<W, S> &C, Shared &sh, int out_idx) {
     cs->info.frame_index = 0;
     cs->info.trailing_silence = 0;
     sh.rec_n = 0;
+    sh.rec_logical = 0;
     cs->path_len = 0;
     cs->max_depth = 0;
     cs->info.utterance_index += 1;
@@ -997,7 +1078,10 @@ __device__ void setup_channel(Chan<W, S> &C, const DecodeParams &P, int slot, S 
   C.app_list = P.app_list + s * P.table_cap;
   C.scr_key = P.scr_key + s * P.table_cap;
   C.scr_slot = P.scr_slot + s * P.table_cap;
-  C.arena = P.arena + s * P.arena_cap;
+  C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
+  C.arena_to = P.arena + (2 * s + ((C.cs->arena_half & 1) ^ 1)) * P.arena_cap;
+  C.gc_bits = P.gc_bits + s * (P.arena_cap / 32 + 1);
+  C.gc_rank = P.gc_rank + s * (P.arena_cap / 32 + 1);
   C.path_rec = P.path_rec + s * P.path_cap;
   C.path_words = P.path_words + s * P.path_cap;
   C.row = sh_row;
@@ -1039,7 +1123,8 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
   ChanState *cs = C.cs;
   if (threadIdx.x == 0) {
     sh.error = 0;
-    sh.rec_n = (u32)cs->info.store_len;
+    sh.rec_n = cs->rec_phys;
+    sh.rec_logical = (unsigned long long)cs->info.store_len;
     sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
     sh.n_all = sh.n_app = sh.n_cand = sh.flog_n = 0;
   }
@@ -1093,7 +1178,8 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    cs->info.store_len = sh.rec_n;
+    cs->rec_phys = sh.rec_n;
+    cs->info.store_len = (long long)sh.rec_logical;
     cs->info.tok_expansions += sh.cnt_tok;
     cs->info.emit_arcs += sh.cnt_emit;
     cs->info.eps_arcs += sh.cnt_eps;
@@ -1115,14 +1201,16 @@ __global__ void __launch_bounds__(BLOCK) hyp_kernel(const DecodeParams P, int wh
   setup_channel<BLOCK>(C, P, P.slots[blockIdx.x], sh_row, sh_ctx);
   if (threadIdx.x == 0) {
     sh.error = 0;
-    sh.rec_n = (u32)C.cs->info.store_len;
+    sh.rec_n = C.cs->rec_phys;
+    sh.rec_logical = (unsigned long long)C.cs->info.store_len;
   }
   __syncthreads();
   if (which == AB_PARTIAL) partial<BLOCK>(C, sh, 0);
   else finalize<BLOCK>(C, sh, 0);
   __syncthreads();
   if (threadIdx.x == 0) {
-    C.cs->info.store_len = sh.rec_n;
+    C.cs->rec_phys = sh.rec_n;
+    C.cs->info.store_len = (long long)sh.rec_logical;
     P.n_hyps[blockIdx.x] = sh.error ? 0 : 1;
     P.errors[blockIdx.x] = sh.error;
   }

@@ -64,7 +64,10 @@ class DeviceGraph:
         self.device_bytes = nbytes.value
         self._ctx: dict[int, tuple[weakref.ref, int]] = {}
         self._pages: list[BatchDecoder] = []
-        self._finalizer = weakref.finalize(self, _destroy_graph, self.handle)
+        # decoders built on this graph must be destroyed before it
+        self._decoder_finalizers: list = []
+        self._finalizer = weakref.finalize(self, _destroy_graph, self.handle,
+                                           self._decoder_finalizers)
 
     # -- context store -------------------------------------------------
     def register_context(self, arc_indices, discount: float, mode: int = _lib.AB_CTX_AUTO) -> int:
@@ -110,7 +113,9 @@ class DeviceGraph:
         return p, p.alloc_slot()
 
 
-def _destroy_graph(handle):
+def _destroy_graph(handle, decoder_finalizers):
+    for f in decoder_finalizers:
+        f()
     try:
         _lib.load().ab_graph_destroy(handle)
     except Exception:
@@ -155,6 +160,7 @@ class BatchDecoder:
         self.capacity = Capacity(q.table_slots, q.frontier_rows, q.arena_records, q.path_words)
         self.device_bytes = nb.value
         self._finalizer = weakref.finalize(self, _destroy_decoder, self.handle)
+        graph._decoder_finalizers.append(self._finalizer)
 
     def alloc_slot(self) -> int | None:
         if not self._free:

@@ -106,6 +106,34 @@ def unigram_context(csr, num_words: int, ctx_seed: int, *, num_labels: int,
                           discount=discount)
 
 
+class OlabelIndex:
+    """Arcs grouped by output label (one argsort of the olabel array), so the
+    unigram contexts of a 2e7-arc graph are built without rescanning it."""
+
+    def __init__(self, csr):
+        ol = np.asarray(csr.olabels)
+        self.order = np.argsort(ol, kind="stable").astype(np.int64)
+        self.sorted = ol[self.order]
+
+    def arcs_of(self, words) -> np.ndarray:
+        w = np.asarray(sorted(words))
+        lo = np.searchsorted(self.sorted, w, side="left")
+        hi = np.searchsorted(self.sorted, w, side="right")
+        parts = [self.order[a:b] for a, b in zip(lo, hi)]
+        return np.sort(np.concatenate(parts)) if parts else np.zeros(0, dtype=np.int64)
+
+
+def unigram_contexts(csr, num_words: int, ctx_seeds, *, num_labels: int,
+                     discount: float = -2.0) -> list:
+    """unigram_context for many seeds sharing one OlabelIndex."""
+    ix = OlabelIndex(csr)
+    out = []
+    for s in ctx_seeds:
+        words = random.Random(s).sample(range(1, num_labels + 1), num_words)
+        out.append(BiasingContext(id=f"ctx{s}", arc_indices=ix.arcs_of(words), discount=discount))
+    return out
+
+
 def dense_context(csr, fraction: float, ctx_seed: int, *, discount: float = -2.0,
                   ctx_id: str | None = None) -> BiasingContext:
     """Context boosting a uniform random ``fraction`` of all arcs (ATC-style)."""

@@ -182,6 +182,36 @@ def test_context_representations_agree(mode):
     assert got == [(h.words, h.cost, h.hits) for h in want]
 
 
+def test_arena_gc_long_utterance():
+    """A 600-frame utterance with a small arena forces many in-kernel garbage
+    collections; hypotheses and the reference-visible len(store) are unchanged."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import _lib, synth
+    from paper_2306_15685_b200.device import BatchDecoder, Capacity, DeviceGraph
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 2, num_labels=2000)
+    cfg = ab.DecoderConfig(beam=13.0, partial_every=25)
+    scores = synth.channel_scores(8, 0, 600, 2000)
+    dg = DeviceGraph(csr)
+    h = dg.register_context(ctx.arc_indices, ctx.discount)
+    dec = BatchDecoder(dg, 2, Capacity(frontier_rows=32768, arena_records=131072))
+    dec.init_channels([0, 1], [h, h])
+    dec.decode([0, 1], [600, 300], [0, 0], np.ascontiguousarray(scores), 2000, cfg,
+               _lib.AB_MODE_STREAM)
+    nh, er, hyps, stride, words = dec.results(2)
+    assert er.tolist() == [0, 0]
+    for c, T in ((0, 600), (1, 300)):
+        want, rc, info = _oracle(csr, scores[:T], ctx, cfg)
+        last, got = [], []
+        for q in range(nh[c]):
+            x = hyps[c * stride + q]
+            w = last[:x.shared] + words[x.words_off:x.words_off + x.n_words - x.shared].tolist()
+            last = w if x.kind == 0 else []
+            got.append((w, x.cost, x.hits, x.frame))
+        assert got == [(h.words, h.cost, h.hits, h.frame) for h in want]
+
+
 def test_zero_discount_context_is_identity():
     """SPEC zero-discount identity: a 0.0-discount context changes nothing."""
     import paper_2306_15685_b200 as ab
@@ -206,8 +236,12 @@ def test_context_switch_per_segment():
     pool = {f"p{i}": synth.unigram_context(csr, 20, 100 + i, num_labels=2000, ctx_id=f"p{i}")
             for i in range(6)}
     reg = ab.ContextRegistry(pool, graph_fingerprint="")
+    from oracle.oracle import OracleChannel, OracleGraph, decode_stream
+
     cfg = ab.DecoderConfig(beam=13.0, partial_every=10)
     chans = [ab.init_channel(f"c{i}", reg, None, cfg) for i in range(4)]
+    og = OracleGraph.from_csr(csr)
+    ochans = [OracleChannel(og) for _ in range(4)]  # persist like the device channels
     for seg in range(4):
         pairs = []
         for i, ch in enumerate(chans):
@@ -216,7 +250,9 @@ def test_context_switch_per_segment():
         res = ab.decode_batch(pairs, csr, reg, cfg)
         for i, r in enumerate(res):
             assert r.error is None
-            want, rc, _ = _oracle(csr, pairs[i][1].costs, pool[f"p{(i + seg) % 6}"], cfg)
+            want, rc = decode_stream(og, pairs[i][1].costs.astype(np.float64),
+                                     pool[f"p{(i + seg) % 6}"], cfg, channel=ochans[i])
+            assert rc == 0
             _same(r.hypotheses, want, f"seg {seg} ch {i}")
         assert all(ch.utterance_index == seg + 1 for ch in chans)
 
