@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+make -C oracle > /dev/null 2>&1
+timeout 1200 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
