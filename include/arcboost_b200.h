@@ -42,8 +42,15 @@ enum {
   AB_MODE_ADVANCE = 0, /* advance_frame only, T frames (decoder.py:341-411) */
   AB_MODE_STREAM = 1   /* _decode_one: partial cadence, endpointing, final (decoder.py:474-501) */
 };
-/* context lookup representation (ab_context_register mode) */
-enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2 };
+/* context lookup representation (ab_context_register mode):
+   LIST    sorted arc ids, binary search (shared memory when k <= 2048)
+   BITSET  one bit per arc in HBM
+   LABELS  one bit per output label in shared memory; only valid (and only
+           chosen by AUTO) when the context is exactly the set of arcs whose
+           olabel lies in some label set, e.g. single-word entities */
+enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2, AB_CTX_LABELS = 3 };
+/* device limits */
+enum { AB_MAX_TABLE_SLOTS = 131072, AB_MAX_EPSILON_ROUNDS = 63 };
 
 typedef struct ab_graph ab_graph;
 typedef struct ab_decoder ab_decoder;
@@ -136,6 +143,8 @@ int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels, int32_t *wei
    must be strictly increasing and non-negative (indices >= num_arcs never match). */
 int ab_context_register(ab_graph *g, const int64_t *arc_indices, int64_t k, double discount,
                         int32_t mode, int32_t *handle);
+/* representation the context store chose for a handle (AB_CTX_LIST/BITSET/LABELS) */
+int ab_context_mode(const ab_graph *g, int32_t handle, int32_t *mode);
 int ab_context_release(ab_graph *g, int32_t handle);
 
 int ab_decoder_create(ab_graph *g, const ab_capacity *cap, int32_t max_channels,

@@ -28,7 +28,8 @@ AB_IDLE, AB_DECODING, AB_ENDPOINTED, AB_FINISHED = 0, 1, 2, 3
 AB_PARTIAL, AB_FINAL = 0, 1
 AB_F32, AB_F64 = 0, 1
 AB_MODE_ADVANCE, AB_MODE_STREAM = 0, 1
-AB_CTX_AUTO, AB_CTX_LIST, AB_CTX_BITSET = 0, 1, 2
+AB_CTX_AUTO, AB_CTX_LIST, AB_CTX_BITSET, AB_CTX_LABELS = 0, 1, 2, 3
+AB_MAX_TABLE_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 63
 
 
 class ab_config(C.Structure):
@@ -115,6 +116,7 @@ SIGNATURES = {
     "ab_graph_query": (_I32, [_P, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I64)]),
     "ab_context_register": (_I32, [_P, _P, _I64, C.c_double, _I32, C.POINTER(_I32)]),
     "ab_context_release": (_I32, [_P, _I32]),
+    "ab_context_mode": (_I32, [_P, _I32, C.POINTER(_I32)]),
     "ab_decoder_create": (_I32, [_P, C.POINTER(ab_capacity), _I32, C.POINTER(_P)]),
     "ab_decoder_destroy": (None, [_P]),
     "ab_decoder_query": (_I32, [_P, C.POINTER(ab_capacity), C.POINTER(_I64)]),

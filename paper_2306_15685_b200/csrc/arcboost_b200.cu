@@ -46,7 +46,9 @@ struct HostCtx {
   bool live = false;
   double discount = 0.0;
   u32 k = 0;
-  int mode = AB_CTX_LIST;
+  int mode = CTX_SLIST; // device CTX_* code
+  int abi_mode = AB_CTX_LIST;
+  u32 words = 0;
   u32 *d_list = nullptr;
   u32 *d_bits = nullptr;
 };
@@ -58,6 +60,9 @@ struct ab_graph {
   int64_t num_arcs = 0;
   int L = 0;
   bool w32 = true;
+  bool fmt16 = true; // f32 weights and 16-bit labels: 16-byte arc records
+  std::vector<int32_t> olabels; // host copy for context classification
+  std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
   u32 *e_off = nullptr, *x_off = nullptr;
   void *e_arcs = nullptr, *x_arcs = nullptr;
   int2 *arc_meta = nullptr;
@@ -84,11 +89,11 @@ struct ab_decoder {
   double *tok_cost = nullptr;
   TokInfo *tok_info = nullptr;
   u32 *flog_state = nullptr;
-  double *flog_cost = nullptr;
+  u64 *flog_ck = nullptr;
   TokInfo *flog_info = nullptr;
-  u32 *all_list = nullptr, *app_list = nullptr;
+  u32 *app_list = nullptr;
   u64 *scr_key = nullptr;
-  u32 *scr_slot = nullptr;
+  u32 *scr_row = nullptr;
   int2 *arena = nullptr;
   u32 *gc_bits = nullptr, *gc_rank = nullptr;
   int *path_rec = nullptr, *path_words = nullptr;
@@ -152,6 +157,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     if (row_offsets[s + 1] < row_offsets[s])
       return fail(AB_ERR_INVALID, "row_offsets not monotone at state %d", s);
   int L = 0;
+  int max_ol = 0;
   bool w32 = true;
   std::vector<u32> e_cnt(num_states + 1, 0), x_cnt(num_states + 1, 0);
   for (int s = 0; s < num_states; ++s) {
@@ -165,6 +171,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
         return fail(AB_ERR_INVALID, "non-finite weight on arc %lld", (long long)a);
       if ((double)(float)weights[a] != weights[a]) w32 = false;
       L = std::max(L, ilabels[a]);
+      max_ol = std::max(max_ol, olabels[a]);
       if (ilabels[a] != 0) e_cnt[s + 1]++;
       else x_cnt[s + 1]++;
     }
@@ -190,34 +197,42 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   g->num_arcs = num_arcs;
   g->L = L;
   g->w32 = w32;
+  g->fmt16 = w32 && L <= 0xFFFF && max_ol <= 0xFFFF;
+  g->olabels.assign(olabels, olabels + num_arcs);
+  if (max_ol < (1 << 24)) {
+    g->ol_count.assign((size_t)max_ol + 1, 0);
+    for (int64_t a = 0; a < num_arcs; ++a) g->ol_count[olabels[a]]++;
+  }
   cudaError_t ce = cudaSetDevice(device);
   if (ce != cudaSuccess) {
     delete g;
     return fail(AB_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
   }
   // build the split arc arrays (arc order inside each state preserved)
-  size_t esz = w32 ? sizeof(EArc<float>) : sizeof(EArc<double>);
-  size_t xsz = w32 ? sizeof(XArc<float>) : sizeof(XArc<double>);
+  const bool f16 = g->fmt16;
+  size_t esz = f16 ? sizeof(EArc16) : sizeof(EArc24);
+  size_t xsz = f16 ? sizeof(XArc16) : sizeof(XArc24);
   std::vector<unsigned char> eh(std::max<size_t>(n_e, 1) * esz, 0), xh(std::max<size_t>(n_x, 1) * xsz, 0);
   for (int s = 0; s < num_states; ++s) {
     u32 pe = e_cnt[s], px = x_cnt[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
       meta[a] = make_int2(olabels[a], ilabels[a]);
       if (ilabels[a] != 0) {
-        if (w32) {
-          EArc<float> r{(u32)next_states[a], (u32)ilabels[a], (u32)a, (float)weights[a]};
+        if (f16) {
+          EArc16 r{(u32)next_states[a], (u32)a, (float)weights[a],
+                   (u32)ilabels[a] | ((u32)olabels[a] << 16)};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         } else {
-          EArc<double> r{(u32)next_states[a], (u32)ilabels[a], (u32)a, 0u, weights[a]};
+          EArc24 r{(u32)next_states[a], (u32)a, (u32)ilabels[a], (u32)olabels[a], weights[a]};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         }
         pe++;
       } else {
-        if (w32) {
-          XArc<float> r{(u32)next_states[a], (u32)a, (float)weights[a], 0u};
+        if (f16) {
+          XArc16 r{(u32)next_states[a], (u32)a, (float)weights[a], (u32)olabels[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         } else {
-          XArc<double> r{(u32)next_states[a], (u32)a, weights[a]};
+          XArc24 r{(u32)next_states[a], (u32)a, (u32)olabels[a], 0u, weights[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         }
         px++;
@@ -271,7 +286,7 @@ extern "C" int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels,
                               int32_t *weights_f32, int64_t *device_bytes) {
   if (!g) return fail(AB_ERR_INVALID, "null graph");
   if (num_emitting_labels) *num_emitting_labels = g->L;
-  if (weights_f32) *weights_f32 = g->w32 ? 1 : 0;
+  if (weights_f32) *weights_f32 = g->fmt16 ? 1 : 0;
   if (device_bytes) *device_bytes = (int64_t)g->bytes;
   return AB_OK;
 }
@@ -285,6 +300,8 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].discount = c.discount;
     h[i].k = c.live ? c.k : 0;
     h[i].mode = c.mode;
+    h[i].words = c.words;
+    h[i].pad = 0;
     h[i].list = c.d_list;
     h[i].bits = c.d_bits;
   }
@@ -318,9 +335,31 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   c.live = true;
   c.discount = discount;
   c.k = (u32)list.size();
-  if (mode == AB_CTX_AUTO) mode = c.k <= (u32)CTX_SMEM_MAX ? AB_CTX_LIST : AB_CTX_BITSET;
-  if (mode != AB_CTX_LIST && mode != AB_CTX_BITSET) return fail(AB_ERR_INVALID, "bad context mode %d", mode);
-  c.mode = mode;
+  // label-closed? (the context is exactly {g : olabel[g] in W} for W = its olabels)
+  bool closed = false;
+  std::vector<u32> lbits;
+  if (!g->ol_count.empty() && !list.empty()) {
+    std::vector<int32_t> labs;
+    labs.reserve(list.size());
+    for (u32 a : list) labs.push_back(g->olabels[a]);
+    std::sort(labs.begin(), labs.end());
+    labs.erase(std::unique(labs.begin(), labs.end()), labs.end());
+    uint64_t cover = 0;
+    for (int32_t l : labs) cover += g->ol_count[l];
+    if (cover == list.size() && labs.back() < 32 * CTX_SMEM_WORDS) {
+      closed = true;
+      lbits.assign((size_t)labs.back() / 32 + 1, 0u);
+      for (int32_t l : labs) lbits[l >> 5] |= 1u << (l & 31);
+    }
+  }
+  if (mode == AB_CTX_AUTO)
+    mode = closed ? AB_CTX_LABELS : (c.k <= (u32)CTX_SMEM_WORDS ? AB_CTX_LIST : AB_CTX_BITSET);
+  if (mode == AB_CTX_LABELS && !closed)
+    return fail(AB_ERR_INVALID, "context is not label-closed: AB_CTX_LABELS would change it");
+  if (mode != AB_CTX_LIST && mode != AB_CTX_BITSET && mode != AB_CTX_LABELS)
+    return fail(AB_ERR_INVALID, "bad context mode %d", mode);
+  c.abi_mode = mode;
+  c.mode = mode == AB_CTX_LABELS ? CTX_LABELS : mode == AB_CTX_BITSET ? CTX_BITSET : CTX_SLIST;
   CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
   if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
   if (mode == AB_CTX_BITSET) {
@@ -329,6 +368,10 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
     for (u32 a : list) bits[a >> 5] |= 1u << (a & 31);
     CK(cudaMalloc(&c.d_bits, words * sizeof(u32)));
     CK(cudaMemcpy(c.d_bits, bits.data(), words * sizeof(u32), cudaMemcpyHostToDevice));
+  } else if (mode == AB_CTX_LABELS) {
+    c.words = (u32)lbits.size();
+    CK(cudaMalloc(&c.d_bits, lbits.size() * sizeof(u32)));
+    CK(cudaMemcpy(c.d_bits, lbits.data(), lbits.size() * sizeof(u32), cudaMemcpyHostToDevice));
   }
   int h = -1;
   for (size_t i = 0; i < g->ctxs.size(); ++i)
@@ -345,6 +388,13 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   int rc = sync_ctx_table(g);
   if (rc) return rc;
   *handle = h;
+  return AB_OK;
+}
+
+extern "C" int ab_context_mode(const ab_graph *g, int32_t handle, int32_t *mode) {
+  if (!g || handle < 0 || handle >= (int)g->ctxs.size() || !g->ctxs[handle].live)
+    return fail(AB_ERR_UNKNOWN_CTX, "unknown context handle %d", handle);
+  *mode = g->ctxs[handle].abi_mode;
   return AB_OK;
 }
 
@@ -379,11 +429,11 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->device = g->device;
   d->max_ch = max_channels;
   uint64_t ts = cap.table_slots;
-  if (ts <= 0) ts = (g->num_states <= (1 << 20)) ? (uint64_t)g->num_states : (1ull << 17);
+  if (ts <= 0) ts = std::min<uint64_t>((uint64_t)g->num_states, MAX_TABLE_SLOTS);
   d->table_cap = next_pow2(ts);
-  if (d->table_cap > (1u << 23)) {
+  if (d->table_cap > MAX_TABLE_SLOTS) {
     delete d;
-    return fail(AB_ERR_INVALID, "table_slots too large (max 2^23)");
+    return fail(AB_ERR_INVALID, "table_slots too large (max %u)", MAX_TABLE_SLOTS);
   }
   d->hashed = d->table_cap < (u32)g->num_states ? 1 : 0;
   d->tok_cap = d->table_cap;
@@ -408,12 +458,11 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
       dmalloc(&d->tok_state, C * d->tok_cap, acc) || dmalloc(&d->tok_cost, C * d->tok_cap, acc) ||
       dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
-      dmalloc(&d->flog_cost, C * d->flog_cap, acc) ||
+      dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_info, C * d->flog_cap, acc) ||
-      dmalloc(&d->all_list, C * d->table_cap, acc) ||
       dmalloc(&d->app_list, C * d->table_cap, acc) ||
-      dmalloc(&d->scr_key, C * d->table_cap, acc) ||
-      dmalloc(&d->scr_slot, C * d->table_cap, acc) ||
+      dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
+      dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
       dmalloc(&d->arena, 2 * C * d->arena_cap, acc) ||
       dmalloc(&d->gc_bits, C * (d->arena_cap / 32 + 1), acc) ||
       dmalloc(&d->gc_rank, C * (d->arena_cap / 32 + 1), acc) ||
@@ -450,8 +499,8 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->tok_state, d->tok_cost, d->tok_info,
-                  d->flog_state, d->flog_cost, d->flog_info, d->all_list, d->app_list,
-                  d->scr_key,   d->scr_slot,  d->arena,     d->path_rec, d->path_words,
+                  d->flog_state, d->flog_ck,  d->flog_info, d->app_list,
+                  d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
                   d->d_soff,    d->d_wused,   d->d_hyps,    d->d_words,  d->d_packh,
@@ -709,13 +758,12 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.tok_info = d->tok_info;
   P.tok_cap = d->tok_cap;
   P.flog_state = d->flog_state;
-  P.flog_cost = d->flog_cost;
+  P.flog_ck = d->flog_ck;
   P.flog_info = d->flog_info;
   P.flog_cap = d->flog_cap;
-  P.all_list = d->all_list;
   P.app_list = d->app_list;
   P.scr_key = d->scr_key;
-  P.scr_slot = d->scr_slot;
+  P.scr_row = d->scr_row;
   P.arena = d->arena;
   P.arena_cap = d->arena_cap;
   P.gc_bits = d->gc_bits;
@@ -736,25 +784,25 @@ static int pick_block(int n) {
   return 512;
 }
 
-template <int BLOCK, typename W, typename S>
+template <int BLOCK, typename F, typename S>
 static cudaError_t launch_decode(const DecodeParams &P, int grid, size_t smem, cudaStream_t st) {
-  decode_kernel<BLOCK, W, S><<<grid, BLOCK, smem, st>>>(P);
+  decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
   return cudaGetLastError();
 }
 
-template <typename W, typename S>
+template <typename F, typename S>
 static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, size_t smem,
                                    cudaStream_t st) {
   switch (block) {
-  case 128: return launch_decode<128, W, S>(P, grid, smem, st);
-  case 256: return launch_decode<256, W, S>(P, grid, smem, st);
-  default: return launch_decode<512, W, S>(P, grid, smem, st);
+  case 128: return launch_decode<128, F, S>(P, grid, smem, st);
+  case 256: return launch_decode<256, F, S>(P, grid, smem, st);
+  default: return launch_decode<512, F, S>(P, grid, smem, st);
   }
 }
 
-template <int BLOCK, typename W, typename S>
+template <int BLOCK, typename F, typename S>
 static cudaError_t launch_hyp(const DecodeParams &P, int which, size_t smem, cudaStream_t st) {
-  hyp_kernel<BLOCK, W, S><<<1, BLOCK, smem, st>>>(P, which);
+  hyp_kernel<BLOCK, F, S><<<1, BLOCK, smem, st>>>(P, which);
   return cudaGetLastError();
 }
 
@@ -797,7 +845,7 @@ __global__ void pack_kernel(int n, const int *n_hyps, const long long *wused, co
 static size_t dyn_smem(int L, bool s64) {
   size_t row = (size_t)L * (s64 ? 8 : 4);
   if (row > (size_t)SCORE_SMEM_MAX_BYTES) row = 0;
-  return CTX_SMEM_MAX * sizeof(u32) + row;
+  return CTX_SMEM_WORDS * sizeof(u32) + row;
 }
 
 extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
@@ -821,8 +869,8 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   if (!(cf.beam > 0)) return fail(AB_ERR_INVALID, "beam must be positive");
   if (cf.max_active < 1) return fail(AB_ERR_INVALID, "max_active must be >= 1");
   if (cf.partial_every < 1) return fail(AB_ERR_INVALID, "partial_every must be >= 1");
-  if (cf.max_epsilon_expansion < 0 || cf.max_epsilon_expansion > 255)
-    return fail(AB_ERR_INVALID, "max_epsilon_expansion must be in [0, 255]");
+  if (cf.max_epsilon_expansion < 0 || cf.max_epsilon_expansion > MAX_EPS_ROUNDS)
+    return fail(AB_ERR_INVALID, "max_epsilon_expansion must be in [0, %d]", MAX_EPS_ROUNDS);
   std::vector<int> slots(a->channels, a->channels + n), frames(a->frames, a->frames + n);
   std::vector<long long> soff(a->score_offsets, a->score_offsets + n);
   int64_t maxT = 0, rows = 0;
@@ -909,10 +957,10 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     const int block = pick_block(m);
     CK(cudaEventRecord(d->ev0, st));
     cudaError_t le;
-    if (g->w32) le = s64 ? launch_decode_b<float, double>(block, P, m, smem, st)
-                         : launch_decode_b<float, float>(block, P, m, smem, st);
-    else le = s64 ? launch_decode_b<double, double>(block, P, m, smem, st)
-                  : launch_decode_b<double, float>(block, P, m, smem, st);
+    if (g->fmt16) le = s64 ? launch_decode_b<Fmt16, double>(block, P, m, smem, st)
+                           : launch_decode_b<Fmt16, float>(block, P, m, smem, st);
+    else le = s64 ? launch_decode_b<Fmt24, double>(block, P, m, smem, st)
+                  : launch_decode_b<Fmt24, float>(block, P, m, smem, st);
     if (le != cudaSuccess) return fail(AB_ERR_CUDA, "decode launch: %s", cudaGetErrorString(le));
     d->last_launches += 1;
     CK(cudaEventRecord(d->ev1, st));
@@ -1043,9 +1091,9 @@ static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *w
   P.words_used = d->d_wused;
   CK(cudaMemcpyAsync(d->d_slots, &ch, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d->d_wused, 0, sizeof(long long), st));
-  const size_t smem = CTX_SMEM_MAX * sizeof(u32);
-  cudaError_t le = g->w32 ? launch_hyp<256, float, float>(P, which, smem, st)
-                          : launch_hyp<256, double, float>(P, which, smem, st);
+  const size_t smem = CTX_SMEM_WORDS * sizeof(u32);
+  cudaError_t le = g->fmt16 ? launch_hyp<256, Fmt16, float>(P, which, smem, st)
+                            : launch_hyp<256, Fmt24, float>(P, which, smem, st);
   if (le != cudaSuccess) return fail(AB_ERR_CUDA, "hypothesis launch: %s", cudaGetErrorString(le));
   int err = 0, nh = 0;
   long long nw = 0;

@@ -4,7 +4,7 @@
 // of it: score-row staging, emitting expansion with the fused boost lookup,
 // bounded epsilon closure, beam + max_active pruning, partial / final
 // traceback.  Channels are independent, so a launch of n
-// CTAs decodes n channels with no inter-CTA synchronisation; with >= ~600
+// CTAs decodes n channels with no inter-CTA synchronisation; with ~1000
 // channels every SM holds several resident channels whose dependent memory
 // chains overlap.
 //
@@ -15,6 +15,12 @@
 //   best token / partial / final by (cost, state)                     337-338, 414-460
 // Costs accumulate in f64 in the reference's association order:
 //   emitting (c + w_eff) + score[il-1], epsilon c + w_eff, final c + final[s].
+//
+// Per-frame data flow (all per channel):
+//   token list --expand(emitting CSR)--> token table (128-bit CAS minimum)
+//   applied slots --snapshot--> frontier log rows (state, cost key, provenance)
+//   frontier rows --expand(epsilon CSR)--> table ... (Jacobi rounds)
+//   live frontier rows --prune (beam, exact top-k radix select)--> token list
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -26,11 +32,23 @@ namespace ab {
 typedef unsigned long long u64;
 typedef uint32_t u32;
 
-constexpr u64 KEY_PENDING = 1ull << 63;
 constexpr u64 KEY_EPOCH_MASK = 0x7FFFFFFF00000000ull;
-constexpr u32 SRC_MASK = 0x7FFFFFu;
-constexpr int CTX_SMEM_MAX = 1024;          // sparse contexts live in shared memory
+// value.info = round(6) | boosted(1) | epoch tag(8) | src(17)
+constexpr int ROUND_SHIFT = 26;
+constexpr int BOOST_SHIFT = 25;
+constexpr int TAG_SHIFT = 17;
+constexpr u32 SRC_BITS = 17;
+constexpr u32 SRC_MASK = (1u << SRC_BITS) - 1;
+constexpr u32 MAX_TABLE_SLOTS = 1u << SRC_BITS;
+constexpr int MAX_EPS_ROUNDS = 63;
+constexpr u32 ROW_DEAD = 0x80000000u;       // frontier-log row superseded later in the frame
+constexpr u32 APP_IMPROVED = 0x80000000u;   // applied-list flag: slot existed this frame
+constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
+constexpr int EXP_UNROLL = 2;  // independent candidates in flight per thread (expansion)
+constexpr int UNROLL = 2;      // independent rows in flight per thread (snapshot)
+
+enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
 
 // Token provenance carried with every token (decoder.py:58-62 + last_il 138).
 struct __align__(16) TokInfo {
@@ -40,12 +58,13 @@ struct __align__(16) TokInfo {
   int last_il; // ilabel of the last emitting arc (decoder.py:393, 404)
 };
 
-// Token-table slot (32 B = one sector).  key: state | epoch<<32 | PENDING.
-// value (16 B, CAS-128 target): ordered cost key, global arc id, info =
-// round(8) | boosted(1) | src(23).
+// Token-table slot (32 B = one sector).  key = state | epoch << 32 (hashed
+// tables only).  value (16 B, the CAS-128 target) = ordered cost key, global
+// arc id, info.  A value whose epoch tag differs from the channel's current
+// tag is empty; the table is wiped when the 8-bit tag wraps (every 255 epochs).
 struct __align__(32) Entry {
   u64 key;
-  u32 flog; // frontier-log row of the latest application
+  u32 flog; // frontier-log row of the latest application in this frame
   u32 pad;
   u64 ck;
   u32 g;
@@ -54,18 +73,66 @@ struct __align__(32) Entry {
 
 struct CtxDesc {
   double discount;
-  u32 k;
-  int mode; // AB_CTX_LIST / AB_CTX_BITSET
-  const u32 *list;
-  const u32 *bits;
+  u32 k;     // arcs in the context
+  int mode;  // CTX_*
+  u32 words; // CTX_LABELS: bitmap words
+  u32 pad;
+  const u32 *list; // sorted arc ids
+  const u32 *bits; // CTX_BITSET: arc bitmap, CTX_LABELS: olabel bitmap
 };
 
-template <typename W> struct EArc;
-template <> struct __align__(16) EArc<float> { u32 ns, il, g; float w; };
-template <> struct __align__(8) EArc<double> { u32 ns, il, g, pad; double w; };
-template <typename W> struct XArc;
-template <> struct __align__(16) XArc<float> { u32 ns, g; float w; u32 pad; };
-template <> struct __align__(16) XArc<double> { u32 ns, g; double w; };
+// Arc record formats.  Fmt16: f32 weight, 16-bit labels (one 16 B load).
+// Fmt24: f64 weight and 32-bit labels.  Records of a state are contiguous
+// and in source order (their g increase).
+struct __align__(16) EArc16 { u32 ns, g; float w; u32 lab; };
+struct __align__(16) XArc16 { u32 ns, g; float w; u32 ol; };
+struct __align__(8) EArc24 { u32 ns, g, il, ol; double w; };
+struct __align__(8) XArc24 { u32 ns, g, ol, pad; double w; };
+
+struct Fmt16 {
+  typedef EArc16 E;
+  typedef XArc16 X;
+  static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
+                                              u32 &il, u32 &ol) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(base) + a);
+    ns = r.x;
+    g = r.y;
+    w = (double)__uint_as_float(r.z);
+    il = r.w & 0xFFFFu;
+    ol = r.w >> 16;
+  }
+  static __device__ __forceinline__ void eps(const void *base, u32 a, u32 &ns, u32 &g, double &w,
+                                             u32 &ol) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(base) + a);
+    ns = r.x;
+    g = r.y;
+    w = (double)__uint_as_float(r.z);
+    ol = r.w;
+  }
+};
+struct Fmt24 {
+  typedef EArc24 E;
+  typedef XArc24 X;
+  static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
+                                              u32 &il, u32 &ol) {
+    const EArc24 *p = reinterpret_cast<const EArc24 *>(base) + a;
+    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(p));
+    ns = r.x;
+    g = r.y;
+    il = r.z;
+    ol = r.w;
+    w = __ldg(&p->w);
+  }
+  static __device__ __forceinline__ void eps(const void *base, u32 a, u32 &ns, u32 &g, double &w,
+                                             u32 &ol) {
+    const XArc24 *p = reinterpret_cast<const XArc24 *>(base) + a;
+    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(p));
+    ns = r.x;
+    g = r.y;
+    ol = r.z;
+    w = __ldg(&p->w);
+  }
+};
 
 struct ChanState {
   ab_channel_info info; // info.store_len = records appended this utterance (reference len(store))
@@ -107,13 +174,12 @@ struct DecodeParams {
   TokInfo *tok_info;
   u32 tok_cap;
   u32 *flog_state;
-  double *flog_cost;
+  u64 *flog_ck;
   TokInfo *flog_info;
   u32 flog_cap;
-  u32 *all_list;
   u32 *app_list;
   u64 *scr_key;
-  u32 *scr_slot;
+  u32 *scr_row;
   int2 *arena;   // [channel][2][arena_cap]: live half + GC to-space
   u32 arena_cap;
   u32 *gc_bits;  // [channel][arena_cap / 32] mark bitmap
@@ -154,10 +220,11 @@ __device__ __forceinline__ double key_cost(u64 k) {
   return __longlong_as_double((long long)b);
 }
 
-__device__ __forceinline__ u64 ld_cg_u64(const u64 *p) {
-  u64 v;
-  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
+__device__ __forceinline__ void ld_cg_head(const Entry *e, u64 &key, u32 &flog) {
+  u64 a, b;
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(&e->key));
+  key = a;
+  flog = (u32)b;
 }
 __device__ __forceinline__ void ld_cg_value(const Entry *e, u64 &ck, u32 &g, u32 &info) {
   u64 a, b;
@@ -165,10 +232,6 @@ __device__ __forceinline__ void ld_cg_value(const Entry *e, u64 &ck, u32 &g, u32
   ck = a;
   g = (u32)b;
   info = (u32)(b >> 32);
-}
-__device__ __forceinline__ void st_cg_value(Entry *e, u64 ck, u32 g, u32 info) {
-  u64 b = ((u64)info << 32) | g;
-  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(&e->ck), "l"(ck), "l"(b) : "memory");
 }
 // 128-bit compare-and-swap on the value half of an entry (ATOMG.E.CAS.128).
 __device__ __forceinline__ bool cas_value(Entry *e, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng,
@@ -251,23 +314,18 @@ __device__ __forceinline__ void block_argmin(u64 &key, u32 &state, int &idx, u64
   __syncthreads();
 }
 
-template <int BLOCK> __device__ __forceinline__ u64 block_min_u64(u64 v, u64 *sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int NW = BLOCK / 32;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    v = lane < NW ? sh[lane] : ~0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sh[0] = v;
+// warp-aggregated append to a shared counter: one smem atomic per warp.
+// Must be reached by every lane of the warp (pred may differ).
+__device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
+  const u32 m = __ballot_sync(0xffffffffu, pred);
+  const int lane = threadIdx.x & 31;
+  u32 base = 0;
+  if (m) {
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) base = atomicAdd(counter, (u32)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
   }
-  __syncthreads();
-  v = sh[0];
-  __syncthreads();
-  return v;
+  return base + __popc(m & ((1u << lane) - 1u));
 }
 
 // ------------------------------------------------------------ CTA state
@@ -281,8 +339,9 @@ enum {
 
 struct Shared {
   // per-phase counters
-  u32 n_all, n_app, n_cand, rec_n, n_keep, n_tok, flog_n;
+  u32 n_new, n_app, n_cand, rec_n, n_keep, n_tok, flog_n;
   unsigned long long rec_logical;
+  unsigned long long min_ck; // cheapest application of the current frame
   int error;
   u32 sel;
   u32 cum;
@@ -298,7 +357,7 @@ struct Shared {
   u32 hist[256];
 };
 
-template <typename W, typename S> struct Chan {
+template <typename F, typename S> struct Chan {
   const DecodeParams *P;
   int slot;
   ChanState *cs;
@@ -307,13 +366,12 @@ template <typename W, typename S> struct Chan {
   double *tok_cost;
   TokInfo *tok_info;
   u32 *flog_state;
-  double *flog_cost;
+  u64 *flog_ck;
   TokInfo *flog_info;
-  u32 *all_list;
   u32 *app_list;
   u64 *scr_key;
-  u32 *scr_slot;
-  int2 *arena;   // live half
+  u32 *scr_row;
+  int2 *arena; // live half
   int2 *arena_to;
   u32 *gc_bits;
   u32 *gc_rank;
@@ -322,157 +380,195 @@ template <typename W, typename S> struct Chan {
   const S *row;
   // context
   double discount;
-  int ctx_mode; // 0 none, 1 smem list, 2 global list, 3 bitset
+  int ctx_mode;
   const u32 *ctx_list;
   u32 ctx_k;
   const u32 *ctx_bits;
+  u32 ctx_words;
   u32 epoch;
+  u32 etag;
 };
 
-template <typename W, typename S>
-__device__ __forceinline__ bool is_boosted(const Chan<W, S> &C, u32 g) {
-  if (C.ctx_mode == 0) return false;
-  if (C.ctx_mode == 3) return (__ldg(&C.ctx_bits[g >> 5]) >> (g & 31)) & 1u;
-  // BiasingContext.boosted_mask: binary search in the sorted list (biasing.py:108-117)
-  const u32 *a = C.ctx_list;
-  u32 lo = 0, hi = C.ctx_k;
-  while (lo < hi) {
-    u32 mid = (lo + hi) >> 1;
-    u32 v = a[mid];
-    if (v == g) return true;
-    if (v < g) lo = mid + 1;
-    else hi = mid;
+// BiasingContext.boosted_mask (biasing.py:108-117) in the representation the
+// context store chose for this context.
+template <typename F, typename S>
+__device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 g, u32 ol) {
+  switch (C.ctx_mode) {
+  case CTX_NONE: return false;
+  case CTX_LABELS: return ol < C.ctx_words * 32u && ((C.ctx_bits[ol >> 5] >> (ol & 31)) & 1u);
+  case CTX_BITSET: return (__ldg(&C.ctx_bits[g >> 5]) >> (g & 31)) & 1u;
+  default: {
+    const u32 *a = C.ctx_list;
+    u32 lo = 0, hi = C.ctx_k;
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      u32 v = a[mid];
+      if (v == g) return true;
+      if (v < g) lo = mid + 1;
+      else hi = mid;
+    }
+    return false;
   }
-  return false;
+  }
 }
 
 __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.error, 0, code); }
 
-// Relaxation of one candidate into the token table (decoder.py:213-220 for the
-// emitting pass; 277-308 for epsilon rounds).  Claims the slot if the state is
-// new this epoch; otherwise CAS-128 minimum with the phase rule:
+__device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
+  return P.hashed ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
+}
+
+// Relaxation of one candidate into the token table (decoder.py:213-220 for
+// the emitting pass; 277-308 for epsilon rounds), starting from the entry
+// contents already loaded in (key, vck, vg, vinfo).  Hashed tables claim the
+// slot's key with a 64-bit CAS; the value is a CAS-128 minimum with the phase
+// rule:
+//   empty (stale tag)          -> take it: a new table entry
 //   value from an earlier round -> replace iff strictly cheaper (cost only)
 //   value from this round       -> replace iff (cost, arc) is smaller
-template <typename W, typename S>
-__device__ __forceinline__ void relax(const Chan<W, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
-                                      u32 info, u32 round) {
-  const DecodeParams &P = *C.P;
-  u32 slot = P.hashed ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
-  const u64 ep = (u64)C.epoch << 32;
-  u32 probes = 0;
-  while (true) {
-    Entry *e = &C.table[slot];
-    u64 k = ld_cg_u64(&e->key);
-    if ((k & KEY_EPOCH_MASK) != ep) {
-      u64 want = (u64)d | ep | KEY_PENDING;
-      u64 old = atomicCAS(&e->key, k, want);
-      if (old == k) {
-        st_cg_value(e, ck, g, info);
-        __threadfence();
-        atomicExch(&e->key, (u64)d | ep);
-        u32 ia = atomicAdd(&sh.n_all, 1u);
-        if (ia < P.table_cap) C.all_list[ia] = slot;
-        else set_error(sh, E_CAP);
-        u32 ip = atomicAdd(&sh.n_app, 1u);
-        if (ip < P.table_cap) C.app_list[ip] = slot;
-        return;
+template <typename F, typename S>
+__device__ __forceinline__ void relax(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
+                                      u32 info, u32 round, u32 slot, u64 key, u64 vck, u32 vg,
+                                      u32 vinfo) {
+  if (P.hashed) {
+    const u64 ep = (u64)C.epoch << 32;
+    u32 probes = 0;
+    while (true) {
+      Entry *e = &C.table[slot];
+      if ((key & KEY_EPOCH_MASK) != ep) {
+        const u64 want = (u64)d | ep;
+        const u64 old = atomicCAS(&e->key, key, want);
+        key = old == key ? want : old;
+        continue;
       }
-      continue; // lost the claim race: re-examine the slot
-    }
-    if ((u32)k != d) {
+      if ((u32)key == d) break;
       slot = (slot + 1) & P.table_mask;
       if (++probes > P.table_mask) {
         set_error(sh, E_CAP);
         return;
       }
-      continue;
+      u32 fl;
+      ld_cg_head(&C.table[slot], key, fl);
+      ld_cg_value(&C.table[slot], vck, vg, vinfo);
     }
-    while (k & KEY_PENDING) {
-      __nanosleep(20);
-      k = ld_cg_u64(&e->key);
-    }
-    __threadfence();
-    u64 cck;
-    u32 cg, cinfo;
-    ld_cg_value(e, cck, cg, cinfo);
-    while (true) {
-      u32 cround = cinfo >> 24;
-      bool better = (cround < round) ? (ck < cck) : (ck < cck || (ck == cck && g < cg));
-      if (!better) return;
-      if (cas_value(e, cck, cg, cinfo, ck, g, info)) {
-        if (cround < round) {
-          u32 ip = atomicAdd(&sh.n_app, 1u);
-          if (ip < P.table_cap) C.app_list[ip] = slot;
-        }
-        return;
+  }
+  Entry *e = &C.table[slot];
+  while (true) {
+    const bool valid = ((vinfo >> TAG_SHIFT) & 0xFFu) == C.etag;
+    const u32 cround = vinfo >> ROUND_SHIFT;
+    const bool better =
+        !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
+    if (!better) return;
+    if (cas_value(e, vck, vg, vinfo, ck, g, info)) {
+      if (!valid) {
+        if (atomicAdd(&sh.n_new, 1u) >= P.tok_cap) set_error(sh, E_CAP);
+        const u32 ip = atomicAdd(&sh.n_app, 1u);
+        if (ip < P.table_cap) C.app_list[ip] = slot;
+      } else if (cround < round) {
+        const u32 ip = atomicAdd(&sh.n_app, 1u);
+        if (ip < P.table_cap) C.app_list[ip] = slot | APP_IMPROVED;
       }
+      return;
     }
   }
 }
 
 // Load-balanced expansion of a token list over one CSR (emitting or epsilon):
-// tiles of BLOCK tokens, block scan of out-degrees, then each thread walks arc
-// positions and locates its token by binary search over the tile prefix.
-template <int BLOCK, bool EMIT, typename W, typename S>
-__device__ void expand(const Chan<W, S> &C, Shared &sh, const u32 *in_state,
+// tiles of TPT*BLOCK tokens, block scan of out-degrees, then each thread
+// takes UNROLL arc positions at a time, locates their tokens by binary search
+// over the tile prefix and keeps all their loads in flight together.
+template <int BLOCK, int TPT, bool EMIT, typename F, typename S>
+__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state, const u64 *in_ck,
                        const double *in_cost, u32 n_in, u32 round) {
-  const DecodeParams &P = *C.P;
-  __shared__ u32 t_a0[BLOCK];
-  __shared__ u32 t_pref[BLOCK];
-  __shared__ double t_cost[BLOCK];
+  constexpr int TILE = BLOCK * TPT;
+  __shared__ u32 t_a0[TILE];
+  __shared__ u32 t_pref[TILE];
+  __shared__ double t_cost[TILE];
   const int tid = threadIdx.x;
   const u32 *off = EMIT ? P.e_off : P.x_off;
+  const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
+  const u32 tag_bits = C.etag << TAG_SHIFT;
+  const u32 round_bits = round << ROUND_SHIFT;
   u32 arcs_seen = 0;
-  for (u32 base = 0; base < n_in; base += BLOCK) {
-    u32 i = base + tid;
-    u32 cnt = 0, a0 = 0;
-    double c = 0.0;
-    if (i < n_in) {
-      u32 s = in_state[i];
-      c = in_cost[i];
-      a0 = __ldg(&off[s]);
-      cnt = __ldg(&off[s + 1]) - a0;
+  for (u32 base = 0; base < n_in; base += TILE) {
+    u32 a0[TPT], cnt[TPT], s[TPT];
+    double c[TPT];
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const u32 i = base + tid * TPT + q;
+      s[q] = 0xFFFFFFFFu;
+      c[q] = 0.0;
+      if (i < n_in) {
+        s[q] = in_state[i];
+        c[q] = in_ck ? key_cost(in_ck[i]) : in_cost[i];
+      }
+    }
+    u32 sum = 0;
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      a0[q] = 0;
+      cnt[q] = 0;
+      if (s[q] != 0xFFFFFFFFu) {
+        a0[q] = __ldg(&off[s[q]]);
+        cnt[q] = __ldg(&off[s[q] + 1]) - a0[q];
+      }
+      sum += cnt[q];
     }
     u32 total;
-    u32 ex = block_excl_scan<BLOCK>(cnt, total, sh.scan);
-    t_a0[tid] = a0;
-    t_pref[tid] = ex;
-    t_cost[tid] = c;
+    u32 ex = block_excl_scan<BLOCK>(sum, total, sh.scan);
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      t_a0[tid * TPT + q] = a0[q];
+      t_pref[tid * TPT + q] = ex;
+      t_cost[tid * TPT + q] = c[q];
+      ex += cnt[q];
+    }
     __syncthreads();
     arcs_seen += total;
-    for (u32 k = tid; k < total; k += BLOCK) {
-      // largest j with t_pref[j] <= k (its count is > 0)
-      u32 lo = 0, hi = BLOCK - 1;
-      while (lo < hi) {
-        u32 mid = (lo + hi + 1) >> 1;
-        if (t_pref[mid] <= k) lo = mid;
-        else hi = mid - 1;
+    for (u32 k0 = tid; k0 < total; k0 += BLOCK * EXP_UNROLL) {
+      u32 d[EXP_UNROLL], g[EXP_UNROLL], info[EXP_UNROLL], slot[EXP_UNROLL], vg[EXP_UNROLL], vinfo[EXP_UNROLL];
+      u64 ck[EXP_UNROLL], key[EXP_UNROLL], vck[EXP_UNROLL];
+      bool on[EXP_UNROLL];
+#pragma unroll
+      for (int u = 0; u < EXP_UNROLL; ++u) {
+        const u32 k = k0 + u * BLOCK;
+        on[u] = k < total;
+        if (!on[u]) continue;
+        // largest j with t_pref[j] <= k (its count is > 0)
+        u32 lo = 0, hi = TILE - 1;
+        while (lo < hi) {
+          const u32 mid = (lo + hi + 1) >> 1;
+          if (t_pref[mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        const u32 a = t_a0[lo] + (k - t_pref[lo]);
+        const double cj = t_cost[lo];
+        u32 il = 0, ol;
+        double w;
+        if (EMIT) F::emit(arcs, a, d[u], g[u], w, il, ol);
+        else F::eps(arcs, a, d[u], g[u], w, ol);
+        // _effective_weights (decoder.py:234-240): boost fused into the cost add
+        const bool bst = is_boosted(C, g[u], ol);
+        const double we = bst ? w + C.discount : w;
+        double cand;
+        if (EMIT) cand = (cj + we) + (double)C.row[il - 1]; // decoder.py:378
+        else cand = cj + we;                                 // decoder.py:268
+        ck[u] = cost_key(cand);
+        info[u] = round_bits | (bst ? (1u << BOOST_SHIFT) : 0u) | tag_bits | ((base + lo) & SRC_MASK);
+        slot[u] = home_slot(P, d[u]);
       }
-      const u32 j = lo;
-      const u32 a = t_a0[j] + (k - t_pref[j]);
-      const double cj = t_cost[j];
-      u32 ns, g, il = 0;
-      double w;
-      if (EMIT) {
-        const EArc<W> r = reinterpret_cast<const EArc<W> *>(P.e_arcs)[a];
-        ns = r.ns;
-        il = r.il;
-        g = r.g;
-        w = (double)r.w;
-      } else {
-        const XArc<W> r = reinterpret_cast<const XArc<W> *>(P.x_arcs)[a];
-        ns = r.ns;
-        g = r.g;
-        w = (double)r.w;
+#pragma unroll
+      for (int u = 0; u < EXP_UNROLL; ++u) {
+        if (!on[u]) continue;
+        u32 fl;
+        key[u] = 0;
+        if (P.hashed) ld_cg_head(&C.table[slot[u]], key[u], fl);
+        ld_cg_value(&C.table[slot[u]], vck[u], vg[u], vinfo[u]);
       }
-      // _effective_weights (decoder.py:234-240): boost fused into the cost add
-      const bool bst = is_boosted(C, g);
-      const double we = bst ? w + C.discount : w;
-      double cand;
-      if (EMIT) cand = (cj + we) + (double)C.row[il - 1]; // decoder.py:378
-      else cand = cj + we;                                 // decoder.py:268
-      const u32 info = (round << 24) | (bst ? (1u << 23) : 0u) | ((base + j) & SRC_MASK);
-      relax(C, sh, ns, cost_key(cand), g, info, round);
+#pragma unroll
+      for (int u = 0; u < EXP_UNROLL; ++u)
+        if (on[u])
+          relax(P, C, sh, d[u], ck[u], g[u], info[u], round, slot[u], key[u], vck[u], vg[u], vinfo[u]);
     }
     __syncthreads();
   }
@@ -486,53 +582,84 @@ __device__ void expand(const Chan<W, S> &C, Shared &sh, const u32 *in_state,
 
 // Snapshot of the slots applied in one phase into the frontier log: resolves
 // the winner's provenance, appends emission records for olabel != 0
-// (decoder.py:385-389, 289-295) and points the slot at its log row.
-template <int BLOCK, typename W, typename S>
-__device__ void snapshot(const Chan<W, S> &C, Shared &sh, u32 round, const TokInfo *src_info,
+// (decoder.py:385-389, 289-295), points the slot at its row and retires the
+// row of an improved slot's previous application.
+template <int BLOCK, typename F, typename S>
+__device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 round, const TokInfo *src_info,
                          u32 n_app, u32 row_base) {
-  const DecodeParams &P = *C.P;
   if (row_base + n_app > P.flog_cap) {
     if (threadIdx.x == 0) set_error(sh, E_CAP);
     return;
   }
-  for (u32 i = threadIdx.x; i < n_app; i += BLOCK) {
-    const u32 slot = C.app_list[i];
-    Entry *e = &C.table[slot];
-    const u32 d = (u32)ld_cg_u64(&e->key);
-    u64 ck;
-    u32 g, info;
-    ld_cg_value(e, ck, g, info);
-    const TokInfo si = src_info[info & SRC_MASK];
-    const int2 meta = __ldg(&P.arc_meta[g]);
-    TokInfo ni;
-    ni.bp = si.bp;
-    ni.depth = si.depth;
-    ni.hits = si.hits + ((info >> 23) & 1);
-    ni.last_il = round == 0 ? meta.y : si.last_il;
-    if (meta.x != 0) {
-      atomicAdd(&sh.rec_logical, 1ull);
-      u32 r = atomicAdd(&sh.rec_n, 1u);
-      if (r < P.arena_cap) {
-        C.arena[r] = make_int2(meta.x, si.bp);
-        ni.bp = (int)r;
-        ni.depth = si.depth + 1;
-      } else {
-        set_error(sh, E_CAP);
-      }
+  u64 mck = ~0ull;
+  for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * UNROLL) {
+    u32 slot[UNROLL], d[UNROLL], g[UNROLL], info[UNROLL], oldrow[UNROLL];
+    u64 ck[UNROLL];
+    bool on[UNROLL], imp[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const u32 i = i0 + u * BLOCK;
+      on[u] = i < n_app;
+      slot[u] = 0;
+      imp[u] = false;
+      if (!on[u]) continue;
+      const u32 a = C.app_list[i];
+      slot[u] = a & ~APP_IMPROVED;
+      imp[u] = (a & APP_IMPROVED) != 0;
     }
-    const u32 row = row_base + i;
-    C.flog_state[row] = d;
-    C.flog_cost[row] = key_cost(ck);
-    C.flog_info[row] = ni;
-    e->flog = row;
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (!on[u]) continue;
+      const Entry *e = &C.table[slot[u]];
+      u64 key = slot[u];
+      oldrow[u] = 0;
+      if (P.hashed || imp[u]) ld_cg_head(e, key, oldrow[u]);
+      d[u] = P.hashed ? (u32)key : slot[u];
+      ld_cg_value(e, ck[u], g[u], info[u]);
+    }
+    TokInfo si[UNROLL];
+    int2 meta[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (!on[u]) continue;
+      si[u] = src_info[info[u] & SRC_MASK];
+      meta[u] = __ldg(&P.arc_meta[g[u]]);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (!on[u]) continue;
+      TokInfo ni;
+      ni.bp = si[u].bp;
+      ni.depth = si[u].depth;
+      ni.hits = si[u].hits + ((info[u] >> BOOST_SHIFT) & 1);
+      ni.last_il = round == 0 ? meta[u].y : si[u].last_il;
+      if (meta[u].x != 0) {
+        atomicAdd(&sh.rec_logical, 1ull);
+        const u32 r = atomicAdd(&sh.rec_n, 1u);
+        if (r < P.arena_cap) {
+          C.arena[r] = make_int2(meta[u].x, si[u].bp);
+          ni.bp = (int)r;
+          ni.depth = si[u].depth + 1;
+        } else {
+          set_error(sh, E_CAP);
+        }
+      }
+      const u32 row = row_base + i0 + u * BLOCK;
+      C.flog_state[row] = d[u];
+      C.flog_ck[row] = ck[u];
+      C.flog_info[row] = ni;
+      C.table[slot[u]].flog = row;
+      if (imp[u]) atomicOr(&C.flog_state[oldrow[u]], ROW_DEAD);
+      mck = min(mck, ck[u]);
+    }
   }
+  if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
 }
 
 // _epsilon_rounds (decoder.py:250-316) starting from frontier rows
 // [fbase, fbase + nf) of the frontier log.
-template <int BLOCK, typename W, typename S>
-__device__ void epsilon_rounds(const Chan<W, S> &C, Shared &sh, u32 fbase, u32 nf) {
-  const DecodeParams &P = *C.P;
+template <int BLOCK, int TPT, typename F, typename S>
+__device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 fbase, u32 nf) {
   int rounds = 0;
   while (true) {
     if (!(nf > 0 && rounds < P.max_eps)) {
@@ -545,13 +672,14 @@ __device__ void epsilon_rounds(const Chan<W, S> &C, Shared &sh, u32 fbase, u32 n
       sh.n_cand = 0;
     }
     __syncthreads();
-    expand<BLOCK, false>(C, sh, C.flog_state + fbase, C.flog_cost + fbase, nf, (u32)rounds);
+    expand<BLOCK, TPT, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
+                              (u32)rounds);
     __syncthreads();
     const u32 n_cand = sh.n_cand, n_app = sh.n_app;
     if (sh.error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
     const u32 row_base = sh.flog_n;
-    snapshot<BLOCK>(C, sh, (u32)rounds, C.flog_info + fbase, n_app, row_base);
+    snapshot<BLOCK>(P, C, sh, (u32)rounds, C.flog_info + fbase, n_app, row_base);
     __syncthreads();
     if (threadIdx.x == 0) sh.flog_n = row_base + n_app;
     __syncthreads();
@@ -588,16 +716,37 @@ __device__ u64 radix_select(Shared &sh, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &
       if (ok && (kk & above) == prefix) atomicAdd(&sh.hist[(kk >> lowbit) & ((1u << nb) - 1)], 1u);
     }
     __syncthreads();
-    if (tid == 0) {
-      u32 cum = 0, b = 0;
+    if (tid < 32) {
+      // warp scan over the buckets (8 per lane) to find the bucket of the need-th key
       const u32 nbk = 1u << nb;
-      for (; b < nbk; ++b) {
-        if (cum + sh.hist[b] >= need) break;
-        cum += sh.hist[b];
+      u32 loc[8];
+      u32 lsum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const u32 b = tid * 8 + q;
+        loc[q] = b < nbk ? sh.hist[b] : 0u;
+        lsum += loc[q];
       }
-      if (b >= nbk) b = nbk - 1; // unreachable when need <= matching keys
-      sh.sel = b;
-      sh.cum = cum;
+      u32 incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const u32 excl = incl - lsum;
+      if (excl < need && need <= incl) {
+        u32 cum = excl, b = tid * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (cum + loc[q] >= need) {
+            b = tid * 8 + q;
+            break;
+          }
+          cum += loc[q];
+        }
+        sh.sel = b;
+        sh.cum = cum;
+      }
     }
     __syncthreads();
     const u32 b = sh.sel;
@@ -617,21 +766,13 @@ __device__ u64 radix_select(Shared &sh, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &
   }
 }
 
-// _prune (decoder.py:319-334) + _best_token_pos (337-338) + silence bookkeeping
-// (400-407).  Survivors are written to the token list.
-template <int BLOCK, typename W, typename S>
-__device__ void prune(const Chan<W, S> &C, Shared &sh) {
-  const DecodeParams &P = *C.P;
+// _prune (decoder.py:319-334) + _best_token_pos (337-338) + silence
+// bookkeeping (400-407) over the live rows of the frame's frontier log.
+template <int BLOCK, typename F, typename S>
+__device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const int tid = threadIdx.x;
-  const u32 n_all = min(sh.n_all, P.table_cap);
-  u64 m = ~0ull;
-  for (u32 i = tid; i < n_all; i += BLOCK) {
-    u64 ck;
-    u32 g, info;
-    ld_cg_value(&C.table[C.all_list[i]], ck, g, info);
-    m = min(m, ck);
-  }
-  const u64 best_ck = block_min_u64<BLOCK>(m, sh.redk);
+  const u32 n_rows = sh.flog_n;
+  const u64 best_ck = sh.min_ck;
   const double thr = key_cost(best_ck) + P.beam;
   const u64 thr_ck = cost_key(thr);
   if (tid == 0) sh.n_keep = 0;
@@ -639,18 +780,20 @@ __device__ void prune(const Chan<W, S> &C, Shared &sh) {
   u64 bk = ~0ull;
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
-  for (u32 i = tid; i < n_all; i += BLOCK) {
-    const u32 slot = C.all_list[i];
-    Entry *e = &C.table[slot];
-    u64 ck;
-    u32 g, info;
-    ld_cg_value(e, ck, g, info);
-    if (ck <= thr_ck) {
-      const u32 st = (u32)ld_cg_u64(&e->key);
-      const u32 p = atomicAdd(&sh.n_keep, 1u);
+  for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
+    const u32 i = i0 + tid;
+    u32 st = ROW_DEAD;
+    u64 ck = ~0ull;
+    if (i < n_rows) {
+      st = C.flog_state[i];
+      ck = C.flog_ck[i];
+    }
+    const bool in = !(st & ROW_DEAD) && ck <= thr_ck;
+    const u32 p = warp_append(&sh.n_keep, in);
+    if (in) {
       C.scr_key[p] = ck;
-      C.scr_slot[p] = slot;
-      if (ck < bk || (ck == bk && st < bs)) bk = ck, bs = st, bi = (int)slot;
+      C.scr_row[p] = i;
+      if (ck < bk || (ck == bk && st < bs)) bk = ck, bs = st, bi = (int)i;
     }
   }
   __syncthreads();
@@ -670,7 +813,7 @@ __device__ void prune(const Chan<W, S> &C, Shared &sh) {
       // ties at the threshold cost: the smallest states survive
       auto sf = [&](u32 i, bool &ok) -> u64 {
         ok = C.scr_key[i] == tc;
-        return ok ? (u64)(u32)ld_cg_u64(&C.table[C.scr_slot[i]].key) : 0ull;
+        return ok ? (u64)C.flog_state[C.scr_row[i]] : 0ull;
       };
       bool exact2;
       ts = (u32)radix_select<BLOCK>(sh, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
@@ -682,22 +825,22 @@ __device__ void prune(const Chan<W, S> &C, Shared &sh) {
   }
   __syncthreads();
   int md = 0;
-  for (u32 i = tid; i < n_keep; i += BLOCK) {
-    const u64 ck = C.scr_key[i];
-    const u32 slot = C.scr_slot[i];
-    bool keep = ck < tc;
-    u32 st = 0;
-    if (!keep && ck == tc) {
-      st = (u32)ld_cg_u64(&C.table[slot].key);
-      keep = st <= ts;
+  for (u32 i0 = 0; i0 < n_keep; i0 += BLOCK) {
+    const u32 i = i0 + tid;
+    bool keep = false;
+    u64 ck = 0;
+    u32 row = 0;
+    if (i < n_keep) {
+      ck = C.scr_key[i];
+      row = C.scr_row[i];
+      keep = ck < tc;
+      if (!keep && ck == tc) keep = C.flog_state[row] <= ts;
     }
+    const u32 p = warp_append(&sh.n_tok, keep);
     if (keep) {
-      Entry *e = &C.table[slot];
-      if (!st) st = (u32)ld_cg_u64(&e->key);
-      const u32 p = atomicAdd(&sh.n_tok, 1u);
-      const TokInfo ti = C.flog_info[e->flog];
+      const TokInfo ti = C.flog_info[row];
       md = max(md, ti.depth);
-      C.tok_state[p] = st;
+      C.tok_state[p] = C.flog_state[row];
       C.tok_cost[p] = key_cost(ck);
       C.tok_info[p] = ti;
     }
@@ -707,7 +850,7 @@ __device__ void prune(const Chan<W, S> &C, Shared &sh) {
   if (tid == 0) {
     C.cs->max_depth = sh.max_depth;
     C.cs->info.num_active = (int)sh.n_tok;
-    const TokInfo bti = C.flog_info[C.table[bi].flog];
+    const TokInfo bti = C.flog_info[bi];
     if (P.silence_ilabel > 0 && bti.last_il == P.silence_ilabel)
       C.cs->info.trailing_silence += 1;
     else
@@ -716,58 +859,66 @@ __device__ void prune(const Chan<W, S> &C, Shared &sh) {
   __syncthreads();
 }
 
-// Writes the current token table = every slot claimed in this epoch
-// (used after the utterance-start closure, which is not pruned).
-template <int BLOCK, typename W, typename S>
-__device__ void table_to_tokens(const Chan<W, S> &C, Shared &sh) {
-  const u32 n_all = min(sh.n_all, C.P->table_cap);
-  if (threadIdx.x == 0) sh.max_depth = 0;
+// Token list := every live row of the epoch (after the utterance-start
+// closure, which is not pruned).
+template <int BLOCK, typename F, typename S>
+__device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+  const u32 n_rows = sh.flog_n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.n_tok = 0;
+    sh.max_depth = 0;
+  }
   __syncthreads();
   int md = 0;
-  for (u32 i = threadIdx.x; i < n_all; i += BLOCK) {
-    Entry *e = &C.table[C.all_list[i]];
-    u64 ck;
-    u32 g, info;
-    ld_cg_value(e, ck, g, info);
-    const TokInfo ti = C.flog_info[e->flog];
-    md = max(md, ti.depth);
-    C.tok_state[i] = (u32)ld_cg_u64(&e->key);
-    C.tok_cost[i] = key_cost(ck);
-    C.tok_info[i] = ti;
+  for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
+    const u32 i = i0 + threadIdx.x;
+    const u32 st = i < n_rows ? C.flog_state[i] : ROW_DEAD;
+    const bool live = !(st & ROW_DEAD);
+    const u32 p = warp_append(&sh.n_tok, live);
+    if (live) {
+      const TokInfo ti = C.flog_info[i];
+      md = max(md, ti.depth);
+      C.tok_state[p] = st;
+      C.tok_cost[p] = key_cost(C.flog_ck[i]);
+      C.tok_info[p] = ti;
+    }
   }
   atomicMax(&sh.max_depth, md);
   __syncthreads();
   if (threadIdx.x == 0) {
-    C.cs->info.num_active = (int)n_all;
+    C.cs->info.num_active = (int)sh.n_tok;
     C.cs->max_depth = sh.max_depth;
   }
   __syncthreads();
 }
 
-// Puts the utterance-start token into a fresh epoch (decoder.py:243-247).
-template <int BLOCK, typename W, typename S>
-__device__ void materialize_start(Chan<W, S> &C, Shared &sh) {
-  const DecodeParams &P = *C.P;
-  if (threadIdx.x == 0) {
-    C.cs->epoch += 1;
-    sh.n_all = 0;
-    sh.n_app = 0;
-    sh.flog_n = 1;
+// Moves the channel to a fresh table epoch; the table is wiped when the
+// 8-bit epoch tag would wrap, so a tag is never reused while stale values
+// carrying it can still be in the table.
+template <int BLOCK, typename F, typename S>
+__device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
+  u32 e = C.cs->epoch + 1;
+  if ((e & 0x7FFFFFFFu) == 0) e = 0x100; // 31-bit key epochs (wrap also wipes below)
+  if ((e & 0xFFu) == 0) {
+    for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) {
+      C.table[i].key = 0;
+      C.table[i].ck = 0;
+      C.table[i].g = 0;
+      C.table[i].info = 0;
+    }
+    e += 1;
   }
   __syncthreads();
-  C.epoch = C.cs->epoch;
   if (threadIdx.x == 0) {
-    relax(C, sh, (u32)P.start, cost_key(0.0), 0xFFFFFFFFu, 0u, 0u);
-    const u32 slot = C.all_list[0];
-    TokInfo t;
-    t.bp = -1;
-    t.depth = 0;
-    t.hits = 0;
-    t.last_il = 0;
-    C.flog_state[0] = (u32)P.start;
-    C.flog_cost[0] = 0.0;
-    C.flog_info[0] = t;
-    C.table[slot].flog = 0;
+    C.cs->epoch = e;
+    C.epoch = e;
+    C.etag = e & 0xFFu;
+    sh.n_new = 0;
+    sh.n_app = 0;
+    sh.n_cand = 0;
+    sh.flog_n = 0;
+    sh.min_ck = ~0ull;
   }
   __syncthreads();
 }
@@ -776,8 +927,8 @@ __device__ void materialize_start(Chan<W, S> &C, Shared &sh) {
 // list move to the other half in arena order (ids stay monotone), everything
 // else (records of pruned or superseded tokens) is dropped.  Words never
 // change: only record ids do, so the prefix-sharing path is reset.
-template <int BLOCK, typename W, typename S>
-__device__ void gc_arena(Chan<W, S> &C, Shared &sh) {
+template <int BLOCK, typename F, typename S>
+__device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const u32 n = sh.rec_n;
   const u32 nw = (n + 31) / 32;
   const u32 n_tok = (u32)C.cs->info.num_active;
@@ -823,10 +974,10 @@ __device__ void gc_arena(Chan<W, S> &C, Shared &sh) {
     if (bp >= 0) C.tok_info[i].bp = newid(bp);
   }
   __syncthreads();
-  int2 *t = C.arena;
-  C.arena = C.arena_to;
-  C.arena_to = t;
   if (threadIdx.x == 0) {
+    int2 *t = C.arena;
+    C.arena = C.arena_to;
+    C.arena_to = t;
     sh.rec_n = carry;
     C.cs->arena_half ^= 1;
     C.cs->path_len = 0;
@@ -834,10 +985,38 @@ __device__ void gc_arena(Chan<W, S> &C, Shared &sh) {
   __syncthreads();
 }
 
+// Puts the utterance-start token into a fresh epoch (decoder.py:243-247).
+template <int BLOCK, typename F, typename S>
+__device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
+  next_epoch<BLOCK>(P, C, sh);
+  if (threadIdx.x == 0) {
+    const u32 d = (u32)P.start;
+    const u32 slot = home_slot(P, d);
+    u64 key = 0, vck;
+    u32 fl, vg, vinfo;
+    if (P.hashed) ld_cg_head(&C.table[slot], key, fl);
+    ld_cg_value(&C.table[slot], vck, vg, vinfo);
+    relax(P, C, sh, d, cost_key(0.0), 0xFFFFFFFFu, C.etag << TAG_SHIFT, 0u, slot, key, vck, vg, vinfo);
+    // the start entry's slot is app_list[0]; its row 0 has no provenance
+    TokInfo t;
+    t.bp = -1;
+    t.depth = 0;
+    t.hits = 0;
+    t.last_il = 0;
+    const u32 s0 = C.app_list[0] & ~APP_IMPROVED;
+    C.flog_state[0] = d;
+    C.flog_ck[0] = cost_key(0.0);
+    C.flog_info[0] = t;
+    C.table[s0].flog = 0;
+    sh.flog_n = 1;
+    sh.min_ck = cost_key(0.0);
+  }
+  __syncthreads();
+}
+
 // advance_frame (decoder.py:341-411) for frame row C.row.
-template <int BLOCK, typename W, typename S>
-__device__ void advance(Chan<W, S> &C, Shared &sh) {
-  const DecodeParams &P = *C.P;
+template <int BLOCK, int TPT, typename F, typename S>
+__device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   ChanState *cs = C.cs;
   if (cs->info.status != AB_IDLE && cs->info.status != AB_DECODING) {
     if (threadIdx.x == 0) set_error(sh, E_STATUS);
@@ -846,7 +1025,7 @@ __device__ void advance(Chan<W, S> &C, Shared &sh) {
   }
   // one frame appends at most flog_cap records: collect first if they might not fit
   if (!cs->info.fresh && (unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
-    gc_arena<BLOCK>(C, sh);
+    gc_arena<BLOCK>(P, C, sh);
     if ((unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
       if (threadIdx.x == 0) set_error(sh, E_CAP);
       __syncthreads();
@@ -854,26 +1033,17 @@ __device__ void advance(Chan<W, S> &C, Shared &sh) {
     }
   }
   if (cs->info.fresh) {
-    materialize_start<BLOCK>(C, sh);
-    epsilon_rounds<BLOCK>(C, sh, 0u, 1u); // utterance-start closure, no prune
+    materialize_start<BLOCK>(P, C, sh);
+    epsilon_rounds<BLOCK, TPT>(P, C, sh, 0u, 1u); // utterance-start closure, no prune
     if (sh.error) return;
-    table_to_tokens<BLOCK>(C, sh);
+    rows_to_tokens<BLOCK>(P, C, sh);
     if (threadIdx.x == 0) cs->info.fresh = 0;
   }
   __syncthreads();
   const u32 n_tok = (u32)cs->info.num_active;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    cs->info.status = AB_DECODING;
-    cs->epoch += 1;
-    sh.n_all = 0;
-    sh.n_app = 0;
-    sh.n_cand = 0;
-    sh.flog_n = 0;
-  }
-  __syncthreads();
-  C.epoch = cs->epoch;
-  expand<BLOCK, true>(C, sh, C.tok_state, C.tok_cost, n_tok, 0u);
+  if (threadIdx.x == 0) cs->info.status = AB_DECODING;
+  next_epoch<BLOCK>(P, C, sh);
+  expand<BLOCK, TPT, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u);
   __syncthreads();
   if (sh.error) return;
   const u32 n_app = sh.n_app;
@@ -881,14 +1051,14 @@ __device__ void advance(Chan<W, S> &C, Shared &sh) {
     // no emitting arcs: every token dies (decoder.py:394-398)
     if (threadIdx.x == 0) cs->info.num_active = 0;
   } else {
-    snapshot<BLOCK>(C, sh, 0u, C.tok_info, n_app, 0u);
+    snapshot<BLOCK>(P, C, sh, 0u, C.tok_info, n_app, 0u);
     __syncthreads();
     if (threadIdx.x == 0) sh.flog_n = n_app;
     __syncthreads();
     if (sh.error) return;
-    epsilon_rounds<BLOCK>(C, sh, 0u, n_app);
+    epsilon_rounds<BLOCK, TPT>(P, C, sh, 0u, n_app);
     if (sh.error) return;
-    prune<BLOCK>(C, sh);
+    prune<BLOCK>(P, C, sh);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -900,10 +1070,9 @@ __device__ void advance(Chan<W, S> &C, Shared &sh) {
 
 // Traceback with prefix sharing against the channel's previous hypothesis
 // path (EmissionStore.backtrace, decoder.py:95-102), then hypothesis output.
-template <int BLOCK, typename W, typename S>
-__device__ void emit_hyp(Chan<W, S> &C, Shared &sh, int out_idx, int kind, int fallback,
+template <int BLOCK, typename F, typename S>
+__device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx, int kind, int fallback,
                          double cost, int bp, int depth, int hits) {
-  const DecodeParams &P = *C.P;
   ChanState *cs = C.cs;
   if (threadIdx.x == 0) {
     int shared_words = 0;
@@ -952,11 +1121,11 @@ __device__ void emit_hyp(Chan<W, S> &C, Shared &sh, int out_idx, int kind, int f
 }
 
 // partial_hypothesis (decoder.py:414-423).
-template <int BLOCK, typename W, typename S>
-__device__ void partial(Chan<W, S> &C, Shared &sh, int out_idx) {
+template <int BLOCK, typename F, typename S>
+__device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx) {
   ChanState *cs = C.cs;
   if (cs->info.fresh) {
-    emit_hyp<BLOCK>(C, sh, out_idx, AB_PARTIAL, 0, 0.0, -1, 0, 0);
+    emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, 0.0, -1, 0, 0);
     return;
   }
   const u32 n = (u32)cs->info.num_active;
@@ -975,14 +1144,13 @@ __device__ void partial(Chan<W, S> &C, Shared &sh, int out_idx) {
   }
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   const TokInfo t = C.tok_info[bi];
-  emit_hyp<BLOCK>(C, sh, out_idx, AB_PARTIAL, 0, C.tok_cost[bi], t.bp, t.depth, t.hits);
+  emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, C.tok_cost[bi], t.bp, t.depth, t.hits);
 }
 
 // finalize (decoder.py:426-460): best final token by (cost + final, state),
 // falling back to the best token; then the utterance is reset.
-template <int BLOCK, typename W, typename S>
-__device__ void finalize(Chan<W, S> &C, Shared &sh, int out_idx) {
-  const DecodeParams &P = *C.P;
+template <int BLOCK, typename F, typename S>
+__device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx) {
   ChanState *cs = C.cs;
   const int st = cs->info.status;
   if (st != AB_DECODING && st != AB_ENDPOINTED && !(st == AB_IDLE && cs->info.fresh)) {
@@ -1042,7 +1210,7 @@ __device__ void finalize(Chan<W, S> &C, Shared &sh, int out_idx) {
     cost = C.tok_cost[b];
   }
   const TokInfo t = C.tok_info[b];
-  emit_hyp<BLOCK>(C, sh, out_idx, AB_FINAL, fallback, cost, t.bp, t.depth, t.hits);
+  emit_hyp<BLOCK>(P, C, sh, out_idx, AB_FINAL, fallback, cost, t.bp, t.depth, t.hits);
   if (sh.error) return;
   if (threadIdx.x == 0) {
     // _reset_utterance (decoder.py:151-159)
@@ -1060,65 +1228,84 @@ __device__ void finalize(Chan<W, S> &C, Shared &sh, int out_idx) {
   __syncthreads();
 }
 
-template <int BLOCK, typename W, typename S>
-__device__ void setup_channel(Chan<W, S> &C, const DecodeParams &P, int slot, S *sh_row,
+// The channel's view (pool pointers, context, epoch) lives in shared memory:
+// it is uniform across the CTA, so keeping it out of registers frees them for
+// in-flight loads.
+template <int BLOCK, typename F, typename S>
+__device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int slot, S *sh_row,
                               u32 *sh_ctx) {
-  C.P = &P;
-  C.slot = slot;
-  C.cs = &P.chans[slot];
-  const size_t s = (size_t)slot;
-  C.table = P.table + s * P.table_cap;
-  C.tok_state = P.tok_state + s * P.tok_cap;
-  C.tok_cost = P.tok_cost + s * P.tok_cap;
-  C.tok_info = P.tok_info + s * P.tok_cap;
-  C.flog_state = P.flog_state + s * P.flog_cap;
-  C.flog_cost = P.flog_cost + s * P.flog_cap;
-  C.flog_info = P.flog_info + s * P.flog_cap;
-  C.all_list = P.all_list + s * P.table_cap;
-  C.app_list = P.app_list + s * P.table_cap;
-  C.scr_key = P.scr_key + s * P.table_cap;
-  C.scr_slot = P.scr_slot + s * P.table_cap;
-  C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
-  C.arena_to = P.arena + (2 * s + ((C.cs->arena_half & 1) ^ 1)) * P.arena_cap;
-  C.gc_bits = P.gc_bits + s * (P.arena_cap / 32 + 1);
-  C.gc_rank = P.gc_rank + s * (P.arena_cap / 32 + 1);
-  C.path_rec = P.path_rec + s * P.path_cap;
-  C.path_words = P.path_words + s * P.path_cap;
-  C.row = sh_row;
-  C.epoch = C.cs->epoch;
-  const int h = C.cs->info.context;
-  C.ctx_mode = 0;
-  C.discount = 0.0;
+  const int h = P.chans[slot].info.context;
+  if (threadIdx.x == 0) {
+    C.P = &P;
+    C.slot = slot;
+    C.cs = &P.chans[slot];
+    const size_t s = (size_t)slot;
+    C.table = P.table + s * P.table_cap;
+    C.tok_state = P.tok_state + s * P.tok_cap;
+    C.tok_cost = P.tok_cost + s * P.tok_cap;
+    C.tok_info = P.tok_info + s * P.tok_cap;
+    C.flog_state = P.flog_state + s * P.flog_cap;
+    C.flog_ck = P.flog_ck + s * P.flog_cap;
+    C.flog_info = P.flog_info + s * P.flog_cap;
+    C.app_list = P.app_list + s * P.table_cap;
+    C.scr_key = P.scr_key + s * P.flog_cap;
+    C.scr_row = P.scr_row + s * P.flog_cap;
+    C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
+    C.arena_to = P.arena + (2 * s + ((C.cs->arena_half & 1) ^ 1)) * P.arena_cap;
+    C.gc_bits = P.gc_bits + s * (P.arena_cap / 32 + 1);
+    C.gc_rank = P.gc_rank + s * (P.arena_cap / 32 + 1);
+    C.path_rec = P.path_rec + s * P.path_cap;
+    C.path_words = P.path_words + s * P.path_cap;
+    C.row = sh_row;
+    C.epoch = C.cs->epoch;
+    C.etag = C.epoch & 0xFFu;
+    C.ctx_mode = CTX_NONE;
+    C.discount = 0.0;
+    C.ctx_k = 0;
+    C.ctx_words = 0;
+    C.ctx_list = nullptr;
+    C.ctx_bits = nullptr;
+  }
+  __syncthreads();
   if (h >= 0 && h < P.num_ctxs) {
     const CtxDesc d = P.ctxs[h];
-    C.discount = d.discount;
-    C.ctx_k = d.k;
+    int mode = CTX_NONE;
     if (d.k == 0) {
-      C.ctx_mode = 0;
-    } else if (d.mode == AB_CTX_BITSET) {
-      C.ctx_mode = 3;
-      C.ctx_bits = d.bits;
-    } else if (d.k <= (u32)CTX_SMEM_MAX) {
+      mode = CTX_NONE;
+    } else if (d.mode == CTX_LABELS) {
+      for (u32 i = threadIdx.x; i < d.words; i += BLOCK) sh_ctx[i] = d.bits[i];
+      mode = CTX_LABELS;
+    } else if (d.mode == CTX_BITSET) {
+      mode = CTX_BITSET;
+    } else if (d.k <= (u32)CTX_SMEM_WORDS) {
       for (u32 i = threadIdx.x; i < d.k; i += BLOCK) sh_ctx[i] = d.list[i];
-      C.ctx_mode = 1;
-      C.ctx_list = sh_ctx;
+      mode = CTX_SLIST;
     } else {
-      C.ctx_mode = 2;
-      C.ctx_list = d.list;
+      mode = CTX_GLIST;
+    }
+    if (threadIdx.x == 0) {
+      C.discount = d.discount;
+      C.ctx_k = d.k;
+      C.ctx_mode = mode;
+      C.ctx_words = d.words;
+      C.ctx_bits = mode == CTX_LABELS ? sh_ctx : d.bits;
+      C.ctx_list = mode == CTX_SLIST ? sh_ctx : d.list;
     }
   }
   __syncthreads();
 }
 
-template <int BLOCK, typename W, typename S>
-__global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
+// 64 registers per thread: 8 CTAs of 128 threads (or 4 x 256, 2 x 512) per SM
+template <int BLOCK, typename F, typename S>
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) decode_kernel(const __grid_constant__ DecodeParams P) {
+  constexpr int TPT = BLOCK <= 128 ? 2 : 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
-  S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_MAX * sizeof(u32));
+  S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
   const int slot = P.slots[blockIdx.x];
-  Chan<W, S> C;
+  __shared__ Chan<F, S> C;
   setup_channel<BLOCK>(C, P, slot, sh_row, sh_ctx);
   ChanState *cs = C.cs;
   if (threadIdx.x == 0) {
@@ -1126,7 +1313,7 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
     sh.rec_n = cs->rec_phys;
     sh.rec_logical = (unsigned long long)cs->info.store_len;
     sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
-    sh.n_all = sh.n_app = sh.n_cand = sh.flog_n = 0;
+    sh.n_new = sh.n_app = sh.n_cand = sh.flog_n = 0;
   }
   __syncthreads();
   const int T = P.frames[blockIdx.x];
@@ -1143,28 +1330,30 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
       // a frame adds at most 1 + max_eps words to any path and emits at most two
       // hypotheses; pause (the host relaunches) if they might not fit
       const long long bound = (long long)(cs->info.fresh ? 0 : cs->max_depth) + 2 + P.max_eps;
-      if (P.words_used[blockIdx.x] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) break;
+      if (P.words_used[blockIdx.x] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
+        if (t == 0 && threadIdx.x == 0) set_error(sh, E_CAP); // no progress possible
+        break;
+      }
     }
     const S *grow = scores + (size_t)t * P.L;
     if (row_in_smem) {
       for (int i = threadIdx.x; i < P.L; i += BLOCK) sh_row[i] = grow[i];
-      C.row = sh_row;
-    } else {
+    } else if (threadIdx.x == 0) {
       C.row = grow;
     }
     __syncthreads();
-    advance<BLOCK>(C, sh);
+    advance<BLOCK, TPT>(P, C, sh);
     if (sh.error) break;
     if (P.mode == AB_MODE_STREAM) {
       if (cs->info.frame_index % P.partial_every == 0) {
-        partial<BLOCK>(C, sh, n_out++);
+        partial<BLOCK>(P, C, sh, n_out++);
         if (sh.error) break;
       }
       if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
         __syncthreads();
         if (threadIdx.x == 0) cs->info.status = AB_ENDPOINTED;
         __syncthreads();
-        finalize<BLOCK>(C, sh, n_out++);
+        finalize<BLOCK>(P, C, sh, n_out++);
         if (sh.error) break;
       }
     }
@@ -1172,7 +1361,7 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
   }
   const bool done = t == T;
   if (P.mode == AB_MODE_STREAM && !sh.error && done) {
-    if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(C, sh, n_out++);
+    if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(P, C, sh, n_out++);
     __syncthreads();
     if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
   }
@@ -1191,13 +1380,13 @@ __global__ void __launch_bounds__(BLOCK) decode_kernel(const DecodeParams P) {
 }
 
 // Standalone partial / finalize for one channel (the per-call Python API).
-template <int BLOCK, typename W, typename S>
-__global__ void __launch_bounds__(BLOCK) hyp_kernel(const DecodeParams P, int which) {
+template <int BLOCK, typename F, typename S>
+__global__ void __launch_bounds__(BLOCK) hyp_kernel(const __grid_constant__ DecodeParams P, int which) {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
-  S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_MAX * sizeof(u32));
-  Chan<W, S> C;
+  S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
+  __shared__ Chan<F, S> C;
   setup_channel<BLOCK>(C, P, P.slots[blockIdx.x], sh_row, sh_ctx);
   if (threadIdx.x == 0) {
     sh.error = 0;
@@ -1205,8 +1394,8 @@ __global__ void __launch_bounds__(BLOCK) hyp_kernel(const DecodeParams P, int wh
     sh.rec_logical = (unsigned long long)C.cs->info.store_len;
   }
   __syncthreads();
-  if (which == AB_PARTIAL) partial<BLOCK>(C, sh, 0);
-  else finalize<BLOCK>(C, sh, 0);
+  if (which == AB_PARTIAL) partial<BLOCK>(P, C, sh, 0);
+  else finalize<BLOCK>(P, C, sh, 0);
   __syncthreads();
   if (threadIdx.x == 0) {
     C.cs->rec_phys = sh.rec_n;

@@ -211,8 +211,9 @@ def _width_error(width, L) -> DecodeError:
 
 
 def _check_eps_cap(cfg) -> None:
-    if not 0 <= cfg.max_epsilon_expansion <= 255:
-        raise DecodeError("max_epsilon_expansion must be in [0, 255] on the device")
+    if not 0 <= cfg.max_epsilon_expansion <= _lib.AB_MAX_EPSILON_ROUNDS:
+        raise DecodeError(
+            f"max_epsilon_expansion must be in [0, {_lib.AB_MAX_EPSILON_ROUNDS}] on the device")
 
 
 # ------------------------------------------------------------------- public API

@@ -77,6 +77,11 @@ class DeviceGraph:
                                               int(mode), C.byref(h)))
         return h.value
 
+    def context_mode(self, handle: int) -> int:
+        m = C.c_int32()
+        check(_lib.load().ab_context_mode(self.handle, int(handle), C.byref(m)))
+        return m.value
+
     def release_context(self, handle: int) -> None:
         check(_lib.load().ab_context_release(self.handle, int(handle)))
 

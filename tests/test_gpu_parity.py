@@ -150,7 +150,7 @@ def test_per_frame_token_sets_match_oracle():
     assert f.words == q.words and f.cost == q.cost and f.fallback == q.fallback
 
 
-@pytest.mark.parametrize("mode", ["list", "bitset"])
+@pytest.mark.parametrize("mode", ["list", "bitset", "labels", "auto"])
 def test_context_representations_agree(mode):
     """Sparse contexts (shared-memory sorted list) and dense ones (HBM bitset)
     give identical decodes; a 5%-dense context is checked against the oracle."""
@@ -164,8 +164,11 @@ def test_context_representations_agree(mode):
     cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
     scores = synth.channel_scores(3, 1, 60, 2000)
     dg = DeviceGraph(csr)
-    h = dg.register_context(ctx.arc_indices, ctx.discount,
-                            _lib.AB_CTX_BITSET if mode == "bitset" else _lib.AB_CTX_LIST)
+    want_mode = {"list": _lib.AB_CTX_LIST, "bitset": _lib.AB_CTX_BITSET,
+                 "labels": _lib.AB_CTX_LABELS, "auto": _lib.AB_CTX_AUTO}[mode]
+    h = dg.register_context(ctx.arc_indices, ctx.discount, want_mode)
+    # a unigram context is label-closed: AUTO picks the shared-memory label bitmap
+    assert dg.context_mode(h) == (_lib.AB_CTX_LABELS if mode == "auto" else want_mode)
     dec = BatchDecoder(dg, 1)
     dec.init_channel(0, h)
     dec.decode([0], [60], [0], np.ascontiguousarray(scores), 2000, cfg, _lib.AB_MODE_STREAM)
@@ -210,6 +213,19 @@ def test_arena_gc_long_utterance():
             last = w if x.kind == 0 else []
             got.append((w, x.cost, x.hits, x.frame))
         assert got == [(h.words, h.cost, h.hits, h.frame) for h in want]
+
+
+def test_labels_mode_rejected_for_non_closed_context():
+    from paper_2306_15685_b200 import _lib, synth
+    from paper_2306_15685_b200.device import DeviceGraph
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 9, num_labels=2000)
+    dg = DeviceGraph(csr)
+    with pytest.raises(_lib.AbError):
+        dg.register_context(ctx.arc_indices[1:], -2.0, _lib.AB_CTX_LABELS)
+    h = dg.register_context(ctx.arc_indices[1:], -2.0)
+    assert dg.context_mode(h) == _lib.AB_CTX_LIST
 
 
 def test_zero_discount_context_is_identity():
