@@ -777,15 +777,30 @@ static int pick_block(int n) {
   const char *env = getenv("AB_BLOCK");
   if (env) {
     int b = atoi(env);
-    if (b == 128 || b == 256 || b == 512) return b;
+    if (b == 128 || b == 256) return b;
   }
-  if (n >= 512) return 128;
-  if (n >= 148) return 256;
-  return 512;
+  (void)n;
+  return 256;
 }
 
+// Persistent grid: at most one wave of resident CTAs, and the same number of
+// channels for every CTA (n = waves * grid, or within one of it).
 template <int BLOCK, typename F, typename S>
-static cudaError_t launch_decode(const DecodeParams &P, int grid, size_t smem, cudaStream_t st) {
+static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cudaStream_t st) {
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BLOCK, F, S>, BLOCK,
+                                                      smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+  }
+  int resident = std::max(1, per_sm * sms);
+  const char *env = getenv("AB_GRID");
+  if (env && atoi(env) > 0) resident = atoi(env);
+  const int waves = (n + resident - 1) / resident;
+  const int grid = (n + waves - 1) / waves;
   decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
   return cudaGetLastError();
 }
@@ -795,8 +810,7 @@ static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, s
                                    cudaStream_t st) {
   switch (block) {
   case 128: return launch_decode<128, F, S>(P, grid, smem, st);
-  case 256: return launch_decode<256, F, S>(P, grid, smem, st);
-  default: return launch_decode<512, F, S>(P, grid, smem, st);
+  default: return launch_decode<256, F, S>(P, grid, smem, st);
   }
 }
 
@@ -957,10 +971,17 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     const int block = pick_block(m);
     CK(cudaEventRecord(d->ev0, st));
     cudaError_t le;
-    if (g->fmt16) le = s64 ? launch_decode_b<Fmt16, double>(block, P, m, smem, st)
-                           : launch_decode_b<Fmt16, float>(block, P, m, smem, st);
-    else le = s64 ? launch_decode_b<Fmt24, double>(block, P, m, smem, st)
-                  : launch_decode_b<Fmt24, float>(block, P, m, smem, st);
+    if (d->hashed) {
+      if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<true>, double>(block, P, m, smem, st)
+                             : launch_decode_b<Fmt16<true>, float>(block, P, m, smem, st);
+      else le = s64 ? launch_decode_b<Fmt24<true>, double>(block, P, m, smem, st)
+                    : launch_decode_b<Fmt24<true>, float>(block, P, m, smem, st);
+    } else {
+      if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<false>, double>(block, P, m, smem, st)
+                             : launch_decode_b<Fmt16<false>, float>(block, P, m, smem, st);
+      else le = s64 ? launch_decode_b<Fmt24<false>, double>(block, P, m, smem, st)
+                    : launch_decode_b<Fmt24<false>, float>(block, P, m, smem, st);
+    }
     if (le != cudaSuccess) return fail(AB_ERR_CUDA, "decode launch: %s", cudaGetErrorString(le));
     d->last_launches += 1;
     CK(cudaEventRecord(d->ev1, st));
@@ -1092,8 +1113,10 @@ static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *w
   CK(cudaMemcpyAsync(d->d_slots, &ch, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d->d_wused, 0, sizeof(long long), st));
   const size_t smem = CTX_SMEM_WORDS * sizeof(u32);
-  cudaError_t le = g->fmt16 ? launch_hyp<256, Fmt16, float>(P, which, smem, st)
-                            : launch_hyp<256, Fmt24, float>(P, which, smem, st);
+  cudaError_t le = d->hashed ? (g->fmt16 ? launch_hyp<256, Fmt16<true>, float>(P, which, smem, st)
+                                         : launch_hyp<256, Fmt24<true>, float>(P, which, smem, st))
+                             : (g->fmt16 ? launch_hyp<256, Fmt16<false>, float>(P, which, smem, st)
+                                         : launch_hyp<256, Fmt24<false>, float>(P, which, smem, st));
   if (le != cudaSuccess) return fail(AB_ERR_CUDA, "hypothesis launch: %s", cudaGetErrorString(le));
   int err = 0, nh = 0;
   long long nw = 0;

@@ -45,7 +45,10 @@ constexpr u32 ROW_DEAD = 0x80000000u;       // frontier-log row superseded later
 constexpr u32 APP_IMPROVED = 0x80000000u;   // applied-list flag: slot existed this frame
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
-constexpr int EXP_UNROLL = 2;  // independent candidates in flight per thread (expansion)
+#ifndef AB_EXP_UNROLL
+#define AB_EXP_UNROLL 1
+#endif
+constexpr int EXP_UNROLL = AB_EXP_UNROLL; // independent candidates in flight per thread (expansion)
 constexpr int UNROLL = 2;      // independent rows in flight per thread (snapshot)
 
 enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
@@ -89,7 +92,8 @@ struct __align__(16) XArc16 { u32 ns, g; float w; u32 ol; };
 struct __align__(8) EArc24 { u32 ns, g, il, ol; double w; };
 struct __align__(8) XArc24 { u32 ns, g, ol, pad; double w; };
 
-struct Fmt16 {
+template <bool H> struct Fmt16 {
+  static constexpr bool hashed = H; // token table: hashed (true) or identity-mapped
   typedef EArc16 E;
   typedef XArc16 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -110,26 +114,29 @@ struct Fmt16 {
     ol = r.w;
   }
 };
-struct Fmt24 {
+template <bool H> struct Fmt24 {
+  static constexpr bool hashed = H;
   typedef EArc24 E;
   typedef XArc24 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
                                               u32 &il, u32 &ol) {
+    // 24-byte records are only 8-byte aligned: three 8-byte loads
     const EArc24 *p = reinterpret_cast<const EArc24 *>(base) + a;
-    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(p));
-    ns = r.x;
-    g = r.y;
-    il = r.z;
-    ol = r.w;
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2 *>(p));
+    const uint2 r1 = __ldg(reinterpret_cast<const uint2 *>(p) + 1);
+    ns = r0.x;
+    g = r0.y;
+    il = r1.x;
+    ol = r1.y;
     w = __ldg(&p->w);
   }
   static __device__ __forceinline__ void eps(const void *base, u32 a, u32 &ns, u32 &g, double &w,
                                              u32 &ol) {
     const XArc24 *p = reinterpret_cast<const XArc24 *>(base) + a;
-    const uint4 r = __ldg(reinterpret_cast<const uint4 *>(p));
-    ns = r.x;
-    g = r.y;
-    ol = r.z;
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2 *>(p));
+    ns = r0.x;
+    g = r0.y;
+    ol = __ldg(&p->ol);
     w = __ldg(&p->w);
   }
 };
@@ -252,6 +259,11 @@ __device__ __forceinline__ bool cas_value(Entry *e, u64 &ck, u32 &g, u32 &info, 
   return ok;
 }
 
+// L2 prefetch: memory-level parallelism that costs no registers
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int BLOCK> __device__ __forceinline__ u32 block_excl_scan(u32 v, u32 &total, u32 *sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NW = BLOCK / 32;
@@ -359,6 +371,7 @@ struct Shared {
 
 template <typename F, typename S> struct Chan {
   const DecodeParams *P;
+  int b; // batch index of the channel this CTA is decoding
   int slot;
   ChanState *cs;
   Entry *table;
@@ -414,8 +427,8 @@ __device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 g, u32 ol) {
 
 __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.error, 0, code); }
 
-__device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
-  return P.hashed ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
+template <bool H> __device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
+  return H ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
 }
 
 // Relaxation of one candidate into the token table (decoder.py:213-220 for
@@ -430,7 +443,7 @@ template <typename F, typename S>
 __device__ __forceinline__ void relax(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
                                       u32 info, u32 round, u32 slot, u64 key, u64 vck, u32 vg,
                                       u32 vinfo) {
-  if (P.hashed) {
+  if (F::hashed) {
     const u64 ep = (u64)C.epoch << 32;
     u32 probes = 0;
     while (true) {
@@ -474,12 +487,15 @@ __device__ __forceinline__ void relax(const DecodeParams &P, const Chan<F, S> &C
 }
 
 // Load-balanced expansion of a token list over one CSR (emitting or epsilon):
-// tiles of TPT*BLOCK tokens, block scan of out-degrees, then each thread
-// takes UNROLL arc positions at a time, locates their tokens by binary search
-// over the tile prefix and keeps all their loads in flight together.
+// tiles of TPT*BLOCK tokens, block scan of out-degrees, then each thread walks
+// arc positions k, k + BLOCK, ... and locates their tokens by binary search
+// over the tile prefix.  Software pipeline per thread: the arc record of the
+// next position and the table slot of the current candidate are prefetched to
+// L2 one iteration before they are used, and the candidate is relaxed one
+// iteration late.
 template <int BLOCK, int TPT, bool EMIT, typename F, typename S>
-__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state, const u64 *in_ck,
-                       const double *in_cost, u32 n_in, u32 round) {
+__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state,
+                       const u64 *in_ck, const double *in_cost, u32 n_in, u32 round) {
   constexpr int TILE = BLOCK * TPT;
   __shared__ u32 t_a0[TILE];
   __shared__ u32 t_pref[TILE];
@@ -487,15 +503,25 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   const int tid = threadIdx.x;
   const u32 *off = EMIT ? P.e_off : P.x_off;
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
+  constexpr u32 REC = EMIT ? (u32)sizeof(typename F::E) : (u32)sizeof(typename F::X);
   const u32 tag_bits = C.etag << TAG_SHIFT;
   const u32 round_bits = round << ROUND_SHIFT;
   u32 arcs_seen = 0;
+  auto locate = [&](u32 k) -> u32 { // largest j with t_pref[j] <= k (its count is > 0)
+    u32 lo = 0, hi = TILE - 1;
+    while (lo < hi) {
+      const u32 mid = (lo + hi + 1) >> 1;
+      if (t_pref[mid] <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
   for (u32 base = 0; base < n_in; base += TILE) {
     u32 a0[TPT], cnt[TPT], s[TPT];
     double c[TPT];
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
-      const u32 i = base + tid * TPT + q;
+      const u32 i = base + q * BLOCK + tid;
       s[q] = 0xFFFFFFFFu;
       c[q] = 0.0;
       if (i < n_in) {
@@ -512,63 +538,75 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         a0[q] = __ldg(&off[s[q]]);
         cnt[q] = __ldg(&off[s[q] + 1]) - a0[q];
       }
-      sum += cnt[q];
     }
-    u32 total;
-    u32 ex = block_excl_scan<BLOCK>(sum, total, sh.scan);
+    // tile order is (q, tid): token q * BLOCK + tid of the tile
+    u32 tot[TPT];
+    u32 ex[TPT];
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) ex[q] = block_excl_scan<BLOCK>(cnt[q], tot[q], sh.scan);
+    u32 qbase = 0;
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
-      t_a0[tid * TPT + q] = a0[q];
-      t_pref[tid * TPT + q] = ex;
-      t_cost[tid * TPT + q] = c[q];
-      ex += cnt[q];
+      const u32 j = q * BLOCK + tid;
+      t_a0[j] = a0[q];
+      t_pref[j] = qbase + ex[q];
+      t_cost[j] = c[q];
+      qbase += tot[q];
     }
+    const u32 total = qbase;
     __syncthreads();
     arcs_seen += total;
-    for (u32 k0 = tid; k0 < total; k0 += BLOCK * EXP_UNROLL) {
-      u32 d[EXP_UNROLL], g[EXP_UNROLL], info[EXP_UNROLL], slot[EXP_UNROLL], vg[EXP_UNROLL], vinfo[EXP_UNROLL];
-      u64 ck[EXP_UNROLL], key[EXP_UNROLL], vck[EXP_UNROLL];
-      bool on[EXP_UNROLL];
-#pragma unroll
-      for (int u = 0; u < EXP_UNROLL; ++u) {
-        const u32 k = k0 + u * BLOCK;
-        on[u] = k < total;
-        if (!on[u]) continue;
-        // largest j with t_pref[j] <= k (its count is > 0)
-        u32 lo = 0, hi = TILE - 1;
-        while (lo < hi) {
-          const u32 mid = (lo + hi + 1) >> 1;
-          if (t_pref[mid] <= k) lo = mid;
-          else hi = mid - 1;
-        }
-        const u32 a = t_a0[lo] + (k - t_pref[lo]);
-        const double cj = t_cost[lo];
+    // pipeline: prev = candidate waiting for its (prefetched) slot
+    bool have_prev = false;
+    u32 pd = 0, pg = 0, pinfo = 0;
+    u64 pck = 0;
+    u32 k = tid;
+    if (k < total) {
+      const u32 j = locate(k);
+      prefetch_l2(reinterpret_cast<const char *>(arcs) + (size_t)(t_a0[j] + (k - t_pref[j])) * REC);
+    }
+    while (true) {
+      const bool cur = k < total;
+      u32 d = 0, g = 0, info = 0;
+      u64 ck = 0;
+      if (cur) {
+        const u32 j = locate(k);
+        const u32 a = t_a0[j] + (k - t_pref[j]);
+        const double cj = t_cost[j];
         u32 il = 0, ol;
         double w;
-        if (EMIT) F::emit(arcs, a, d[u], g[u], w, il, ol);
-        else F::eps(arcs, a, d[u], g[u], w, ol);
+        if (EMIT) F::emit(arcs, a, d, g, w, il, ol);
+        else F::eps(arcs, a, d, g, w, ol);
         // _effective_weights (decoder.py:234-240): boost fused into the cost add
-        const bool bst = is_boosted(C, g[u], ol);
+        const bool bst = is_boosted(C, g, ol);
         const double we = bst ? w + C.discount : w;
         double cand;
         if (EMIT) cand = (cj + we) + (double)C.row[il - 1]; // decoder.py:378
         else cand = cj + we;                                 // decoder.py:268
-        ck[u] = cost_key(cand);
-        info[u] = round_bits | (bst ? (1u << BOOST_SHIFT) : 0u) | tag_bits | ((base + lo) & SRC_MASK);
-        slot[u] = home_slot(P, d[u]);
+        ck = cost_key(cand);
+        info = round_bits | (bst ? (1u << BOOST_SHIFT) : 0u) | tag_bits | ((base + j) & SRC_MASK);
+        prefetch_l2(&C.table[home_slot<F::hashed>(P, d)]);
+        const u32 k2 = k + BLOCK;
+        if (k2 < total) {
+          const u32 j2 = locate(k2);
+          prefetch_l2(reinterpret_cast<const char *>(arcs) + (size_t)(t_a0[j2] + (k2 - t_pref[j2])) * REC);
+        }
       }
-#pragma unroll
-      for (int u = 0; u < EXP_UNROLL; ++u) {
-        if (!on[u]) continue;
-        u32 fl;
-        key[u] = 0;
-        if (P.hashed) ld_cg_head(&C.table[slot[u]], key[u], fl);
-        ld_cg_value(&C.table[slot[u]], vck[u], vg[u], vinfo[u]);
+      if (have_prev) {
+        const u32 slot = home_slot<F::hashed>(P, pd);
+        u64 key = 0, vck;
+        u32 fl, vg, vinfo;
+        if (F::hashed) ld_cg_head(&C.table[slot], key, fl);
+        ld_cg_value(&C.table[slot], vck, vg, vinfo);
+        relax(P, C, sh, pd, pck, pg, pinfo, round, slot, key, vck, vg, vinfo);
       }
-#pragma unroll
-      for (int u = 0; u < EXP_UNROLL; ++u)
-        if (on[u])
-          relax(P, C, sh, d[u], ck[u], g[u], info[u], round, slot[u], key[u], vck[u], vg[u], vinfo[u]);
+      if (!cur) break;
+      pd = d;
+      pg = g;
+      pck = ck;
+      pinfo = info;
+      have_prev = true;
+      k += BLOCK;
     }
     __syncthreads();
   }
@@ -591,6 +629,10 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
     if (threadIdx.x == 0) set_error(sh, E_CAP);
     return;
   }
+  // pull every applied slot into L2 first (independent, register-free)
+#pragma unroll 4
+  for (u32 i = threadIdx.x; i < n_app; i += BLOCK)
+    prefetch_l2(&C.table[C.app_list[i] & ~APP_IMPROVED]);
   u64 mck = ~0ull;
   for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * UNROLL) {
     u32 slot[UNROLL], d[UNROLL], g[UNROLL], info[UNROLL], oldrow[UNROLL];
@@ -613,8 +655,8 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
       const Entry *e = &C.table[slot[u]];
       u64 key = slot[u];
       oldrow[u] = 0;
-      if (P.hashed || imp[u]) ld_cg_head(e, key, oldrow[u]);
-      d[u] = P.hashed ? (u32)key : slot[u];
+      if (F::hashed || imp[u]) ld_cg_head(e, key, oldrow[u]);
+      d[u] = F::hashed ? (u32)key : slot[u];
       ld_cg_value(e, ck[u], g[u], info[u]);
     }
     TokInfo si[UNROLL];
@@ -672,8 +714,8 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       sh.n_cand = 0;
     }
     __syncthreads();
-    expand<BLOCK, TPT, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
-                              (u32)rounds);
+    expand<BLOCK, 4, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
+                            (u32)rounds);
     __syncthreads();
     const u32 n_cand = sh.n_cand, n_app = sh.n_app;
     if (sh.error) return;
@@ -991,10 +1033,10 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
   next_epoch<BLOCK>(P, C, sh);
   if (threadIdx.x == 0) {
     const u32 d = (u32)P.start;
-    const u32 slot = home_slot(P, d);
+    const u32 slot = home_slot<F::hashed>(P, d);
     u64 key = 0, vck;
     u32 fl, vg, vinfo;
-    if (P.hashed) ld_cg_head(&C.table[slot], key, fl);
+    if (F::hashed) ld_cg_head(&C.table[slot], key, fl);
     ld_cg_value(&C.table[slot], vck, vg, vinfo);
     relax(P, C, sh, d, cost_key(0.0), 0xFFFFFFFFu, C.etag << TAG_SHIFT, 0u, slot, key, vck, vg, vinfo);
     // the start entry's slot is app_list[0]; its row 0 has no provenance
@@ -1092,11 +1134,11 @@ __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
       shared_words = d;
       cs->path_len = depth;
       const long long need = depth - shared_words;
-      const long long off = P.words_used[blockIdx.x];
+      const long long off = P.words_used[C.b];
       if (off + need > P.words_stride || out_idx >= P.hyp_stride) set_error(sh, E_CAP);
-      else P.words_used[blockIdx.x] = off + need;
+      else P.words_used[C.b] = off + need;
       sh.shared_words = shared_words;
-      sh.words_off = (long long)blockIdx.x * P.words_stride + off;
+      sh.words_off = (long long)C.b * P.words_stride + off;
     }
   }
   __syncthreads();
@@ -1115,7 +1157,7 @@ __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
     h.n_words = depth;
     h.pad = 0;
     h.words_off = off;
-    P.hyps[(size_t)blockIdx.x * P.hyp_stride + out_idx] = h;
+    P.hyps[(size_t)C.b * P.hyp_stride + out_idx] = h;
   }
   __syncthreads();
 }
@@ -1232,11 +1274,14 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
 // it is uniform across the CTA, so keeping it out of registers frees them for
 // in-flight loads.
 template <int BLOCK, typename F, typename S>
-__device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int slot, S *sh_row,
+__device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh_row,
                               u32 *sh_ctx) {
+  const int slot = P.slots[b];
   const int h = P.chans[slot].info.context;
+  __syncthreads(); // the previous channel of this CTA is done with C
   if (threadIdx.x == 0) {
     C.P = &P;
+    C.b = b;
     C.slot = slot;
     C.cs = &P.chans[slot];
     const size_t s = (size_t)slot;
@@ -1295,87 +1340,91 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int slot, S 
   __syncthreads();
 }
 
-// 64 registers per thread: 8 CTAs of 128 threads (or 4 x 256, 2 x 512) per SM
+// 64 registers per thread: 8 CTAs of 128 threads (or 4 x 256, 2 x 512) per SM.
+// Persistent over channels: CTA i decodes batch entries i, i + grid, ... one
+// after the other (the host sizes the grid so every CTA gets the same count).
 template <int BLOCK, typename F, typename S>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) decode_kernel(const __grid_constant__ DecodeParams P) {
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+    decode_kernel(const __grid_constant__ DecodeParams P) {
   constexpr int TPT = BLOCK <= 128 ? 2 : 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
+  __shared__ Chan<F, S> C;
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
-  const int slot = P.slots[blockIdx.x];
-  __shared__ Chan<F, S> C;
-  setup_channel<BLOCK>(C, P, slot, sh_row, sh_ctx);
-  ChanState *cs = C.cs;
-  if (threadIdx.x == 0) {
-    sh.error = 0;
-    sh.rec_n = cs->rec_phys;
-    sh.rec_logical = (unsigned long long)cs->info.store_len;
-    sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
-    sh.n_new = sh.n_app = sh.n_cand = sh.flog_n = 0;
-  }
-  __syncthreads();
-  const int T = P.frames[blockIdx.x];
-  const S *scores = reinterpret_cast<const S *>(P.scores) + P.score_off[blockIdx.x];
-  int n_out = 0;
-  if (P.mode == AB_MODE_STREAM && cs->info.status == AB_FINISHED) {
-    __syncthreads();
-    if (threadIdx.x == 0) cs->info.status = AB_IDLE; // decoder.py:488-489
-  }
-  __syncthreads();
-  int t = 0;
-  for (; t < T; ++t) {
-    if (P.mode == AB_MODE_STREAM) {
-      // a frame adds at most 1 + max_eps words to any path and emits at most two
-      // hypotheses; pause (the host relaunches) if they might not fit
-      const long long bound = (long long)(cs->info.fresh ? 0 : cs->max_depth) + 2 + P.max_eps;
-      if (P.words_used[blockIdx.x] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
-        if (t == 0 && threadIdx.x == 0) set_error(sh, E_CAP); // no progress possible
-        break;
-      }
-    }
-    const S *grow = scores + (size_t)t * P.L;
-    if (row_in_smem) {
-      for (int i = threadIdx.x; i < P.L; i += BLOCK) sh_row[i] = grow[i];
-    } else if (threadIdx.x == 0) {
-      C.row = grow;
+  for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
+    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx);
+    ChanState *cs = C.cs;
+    if (threadIdx.x == 0) {
+      sh.error = 0;
+      sh.rec_n = cs->rec_phys;
+      sh.rec_logical = (unsigned long long)cs->info.store_len;
+      sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
+      sh.n_new = sh.n_app = sh.n_cand = sh.flog_n = 0;
     }
     __syncthreads();
-    advance<BLOCK, TPT>(P, C, sh);
-    if (sh.error) break;
-    if (P.mode == AB_MODE_STREAM) {
-      if (cs->info.frame_index % P.partial_every == 0) {
-        partial<BLOCK>(P, C, sh, n_out++);
-        if (sh.error) break;
-      }
-      if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
-        __syncthreads();
-        if (threadIdx.x == 0) cs->info.status = AB_ENDPOINTED;
-        __syncthreads();
-        finalize<BLOCK>(P, C, sh, n_out++);
-        if (sh.error) break;
-      }
+    const int T = P.frames[b];
+    const S *scores = reinterpret_cast<const S *>(P.scores) + P.score_off[b];
+    int n_out = 0;
+    if (P.mode == AB_MODE_STREAM && cs->info.status == AB_FINISHED) {
+      __syncthreads();
+      if (threadIdx.x == 0) cs->info.status = AB_IDLE; // decoder.py:488-489
     }
     __syncthreads();
-  }
-  const bool done = t == T;
-  if (P.mode == AB_MODE_STREAM && !sh.error && done) {
-    if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(P, C, sh, n_out++);
+    int t = 0;
+    for (; t < T; ++t) {
+      if (P.mode == AB_MODE_STREAM) {
+        // a frame adds at most 1 + max_eps words to any path and emits at most two
+        // hypotheses; pause (the host relaunches) if they might not fit
+        const long long bound = (long long)(cs->info.fresh ? 0 : cs->max_depth) + 2 + P.max_eps;
+        if (P.words_used[b] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
+          if (t == 0 && threadIdx.x == 0) set_error(sh, E_CAP); // no progress possible
+          break;
+        }
+      }
+      const S *grow = scores + (size_t)t * P.L;
+      if (row_in_smem) {
+        for (int i = threadIdx.x; i < P.L; i += BLOCK) sh_row[i] = grow[i];
+      } else if (threadIdx.x == 0) {
+        C.row = grow;
+      }
+      __syncthreads();
+      advance<BLOCK, TPT>(P, C, sh);
+      if (sh.error) break;
+      if (P.mode == AB_MODE_STREAM) {
+        if (cs->info.frame_index % P.partial_every == 0) {
+          partial<BLOCK>(P, C, sh, n_out++);
+          if (sh.error) break;
+        }
+        if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
+          __syncthreads();
+          if (threadIdx.x == 0) cs->info.status = AB_ENDPOINTED;
+          __syncthreads();
+          finalize<BLOCK>(P, C, sh, n_out++);
+          if (sh.error) break;
+        }
+      }
+      __syncthreads();
+    }
+    const bool done = t == T;
+    if (P.mode == AB_MODE_STREAM && !sh.error && done) {
+      if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(P, C, sh, n_out++);
+      __syncthreads();
+      if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
+    }
     __syncthreads();
-    if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    cs->rec_phys = sh.rec_n;
-    cs->info.store_len = (long long)sh.rec_logical;
-    cs->info.tok_expansions += sh.cnt_tok;
-    cs->info.emit_arcs += sh.cnt_emit;
-    cs->info.eps_arcs += sh.cnt_eps;
-    cs->info.error = sh.error;
-    P.n_hyps[blockIdx.x] = n_out;
-    P.errors[blockIdx.x] = sh.error;
-    P.frames_done[blockIdx.x] = t;
+    if (threadIdx.x == 0) {
+      cs->rec_phys = sh.rec_n;
+      cs->info.store_len = (long long)sh.rec_logical;
+      cs->info.tok_expansions += sh.cnt_tok;
+      cs->info.emit_arcs += sh.cnt_emit;
+      cs->info.eps_arcs += sh.cnt_eps;
+      cs->info.error = sh.error;
+      P.n_hyps[b] = n_out;
+      P.errors[b] = sh.error;
+      P.frames_done[b] = t;
+    }
   }
 }
 
@@ -1387,7 +1436,7 @@ __global__ void __launch_bounds__(BLOCK) hyp_kernel(const __grid_constant__ Deco
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   __shared__ Chan<F, S> C;
-  setup_channel<BLOCK>(C, P, P.slots[blockIdx.x], sh_row, sh_ctx);
+  setup_channel<BLOCK>(C, P, (int)blockIdx.x, sh_row, sh_ctx);
   if (threadIdx.x == 0) {
     sh.error = 0;
     sh.rec_n = C.cs->rec_phys;
@@ -1400,8 +1449,8 @@ __global__ void __launch_bounds__(BLOCK) hyp_kernel(const __grid_constant__ Deco
   if (threadIdx.x == 0) {
     C.cs->rec_phys = sh.rec_n;
     C.cs->info.store_len = (long long)sh.rec_logical;
-    P.n_hyps[blockIdx.x] = sh.error ? 0 : 1;
-    P.errors[blockIdx.x] = sh.error;
+    P.n_hyps[C.b] = sh.error ? 0 : 1;
+    P.errors[C.b] = sh.error;
   }
 }
 
