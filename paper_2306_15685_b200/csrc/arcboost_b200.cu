@@ -149,6 +149,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   if (num_states < 1) return fail(AB_ERR_INVALID, "graph must have at least one state");
   if (num_arcs < 0 || num_arcs >= (int64_t)0xFFFFFFFFll)
     return fail(AB_ERR_INVALID, "num_arcs %lld out of range", (long long)num_arcs);
+  if (num_states > (int32_t)ROW_STATE)
+    return fail(AB_ERR_INVALID, "too many states (max %u)", ROW_STATE);
   if (start < 0 || start >= num_states)
     return fail(AB_ERR_INVALID, "start state %d out of range for %d states", start, num_states);
   if (row_offsets[0] != 0 || row_offsets[num_states] != num_arcs)
@@ -216,7 +218,9 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   for (int s = 0; s < num_states; ++s) {
     u32 pe = e_cnt[s], px = x_cnt[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
-      meta[a] = make_int2(olabels[a], ilabels[a]);
+      const int dst = next_states[a];
+      const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
+      meta[a] = make_int2(olabels[a], ilabels[a] | (dst_eps ? (int)META_DEST_EPS : 0));
       if (ilabels[a] != 0) {
         if (f16) {
           EArc16 r{(u32)next_states[a], (u32)a, (float)weights[a],

@@ -42,6 +42,9 @@ constexpr u32 SRC_MASK = (1u << SRC_BITS) - 1;
 constexpr u32 MAX_TABLE_SLOTS = 1u << SRC_BITS;
 constexpr int MAX_EPS_ROUNDS = 63;
 constexpr u32 ROW_DEAD = 0x80000000u;       // frontier-log row superseded later in the frame
+constexpr u32 ROW_EPS = 0x40000000u;        // row's state has epsilon out-arcs
+constexpr u32 ROW_STATE = 0x3FFFFFFFu;
+constexpr u32 META_DEST_EPS = 0x80000000u;  // arc_meta.y flag: the arc's destination has epsilon arcs
 constexpr u32 APP_IMPROVED = 0x80000000u;   // applied-list flag: slot existed this frame
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
@@ -164,7 +167,7 @@ struct DecodeParams {
   const void *e_arcs;
   const u32 *x_off;
   const void *x_arcs;
-  const int2 *arc_meta; // [num_arcs] {olabel, ilabel} by global arc id
+  const int2 *arc_meta; // [num_arcs] {olabel, ilabel | META_DEST_EPS} by global arc id
   const double *final_cost; // NaN = not final
   int start;
   int num_states;
@@ -534,9 +537,10 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     for (int q = 0; q < TPT; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (s[q] != 0xFFFFFFFFu) {
-        a0[q] = __ldg(&off[s[q]]);
-        cnt[q] = __ldg(&off[s[q] + 1]) - a0[q];
+      if (s[q] != 0xFFFFFFFFu && (EMIT || (s[q] & ROW_EPS))) {
+        const u32 st = EMIT ? s[q] : (s[q] & ROW_STATE);
+        a0[q] = __ldg(&off[st]);
+        cnt[q] = __ldg(&off[st + 1]) - a0[q];
       }
     }
     // tile order is (q, tid): token q * BLOCK + tid of the tile
@@ -629,10 +633,6 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
     if (threadIdx.x == 0) set_error(sh, E_CAP);
     return;
   }
-  // pull every applied slot into L2 first (independent, register-free)
-#pragma unroll 4
-  for (u32 i = threadIdx.x; i < n_app; i += BLOCK)
-    prefetch_l2(&C.table[C.app_list[i] & ~APP_IMPROVED]);
   u64 mck = ~0ull;
   for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * UNROLL) {
     u32 slot[UNROLL], d[UNROLL], g[UNROLL], info[UNROLL], oldrow[UNROLL];
@@ -674,7 +674,7 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
       ni.bp = si[u].bp;
       ni.depth = si[u].depth;
       ni.hits = si[u].hits + ((info[u] >> BOOST_SHIFT) & 1);
-      ni.last_il = round == 0 ? meta[u].y : si[u].last_il;
+      ni.last_il = round == 0 ? (int)((u32)meta[u].y & ~META_DEST_EPS) : si[u].last_il;
       if (meta[u].x != 0) {
         atomicAdd(&sh.rec_logical, 1ull);
         const u32 r = atomicAdd(&sh.rec_n, 1u);
@@ -687,7 +687,7 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
         }
       }
       const u32 row = row_base + i0 + u * BLOCK;
-      C.flog_state[row] = d[u];
+      C.flog_state[row] = d[u] | (((u32)meta[u].y & META_DEST_EPS) ? ROW_EPS : 0u);
       C.flog_ck[row] = ck[u];
       C.flog_info[row] = ni;
       C.table[slot[u]].flog = row;
@@ -831,6 +831,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       ck = C.flog_ck[i];
     }
     const bool in = !(st & ROW_DEAD) && ck <= thr_ck;
+    st &= ROW_STATE;
     const u32 p = warp_append(&sh.n_keep, in);
     if (in) {
       C.scr_key[p] = ck;
@@ -855,7 +856,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       // ties at the threshold cost: the smallest states survive
       auto sf = [&](u32 i, bool &ok) -> u64 {
         ok = C.scr_key[i] == tc;
-        return ok ? (u64)C.flog_state[C.scr_row[i]] : 0ull;
+        return ok ? (u64)(C.flog_state[C.scr_row[i]] & ROW_STATE) : 0ull;
       };
       bool exact2;
       ts = (u32)radix_select<BLOCK>(sh, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
@@ -876,13 +877,13 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       ck = C.scr_key[i];
       row = C.scr_row[i];
       keep = ck < tc;
-      if (!keep && ck == tc) keep = C.flog_state[row] <= ts;
+      if (!keep && ck == tc) keep = (C.flog_state[row] & ROW_STATE) <= ts;
     }
     const u32 p = warp_append(&sh.n_tok, keep);
     if (keep) {
       const TokInfo ti = C.flog_info[row];
       md = max(md, ti.depth);
-      C.tok_state[p] = C.flog_state[row];
+      C.tok_state[p] = C.flog_state[row] & ROW_STATE;
       C.tok_cost[p] = key_cost(ck);
       C.tok_info[p] = ti;
     }
@@ -921,7 +922,7 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
     if (live) {
       const TokInfo ti = C.flog_info[i];
       md = max(md, ti.depth);
-      C.tok_state[p] = st;
+      C.tok_state[p] = st & ROW_STATE;
       C.tok_cost[p] = key_cost(C.flog_ck[i]);
       C.tok_info[p] = ti;
     }
@@ -1046,7 +1047,7 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     t.hits = 0;
     t.last_il = 0;
     const u32 s0 = C.app_list[0] & ~APP_IMPROVED;
-    C.flog_state[0] = d;
+    C.flog_state[0] = d | ROW_EPS; // the closure reads the start state's epsilon range
     C.flog_ck[0] = cost_key(0.0);
     C.flog_info[0] = t;
     C.table[s0].flog = 0;
