@@ -781,7 +781,7 @@ static int pick_block(int n) {
   const char *env = getenv("AB_BLOCK");
   if (env) {
     int b = atoi(env);
-    if (b == 128 || b == 256) return b;
+    if (b == 128 || b == 256 || b == 512) return b;
   }
   (void)n;
   return 256;
@@ -803,6 +803,7 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   int resident = std::max(1, per_sm * sms);
   const char *env = getenv("AB_GRID");
   if (env && atoi(env) > 0) resident = atoi(env);
+  if (const char *l2 = getenv("AB_L2FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
   const int waves = (n + resident - 1) / resident;
   const int grid = (n + waves - 1) / waves;
   decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
@@ -814,6 +815,7 @@ static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, s
                                    cudaStream_t st) {
   switch (block) {
   case 128: return launch_decode<128, F, S>(P, grid, smem, st);
+  case 512: return launch_decode<512, F, S>(P, grid, smem, st);
   default: return launch_decode<256, F, S>(P, grid, smem, st);
   }
 }
@@ -1054,6 +1056,19 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     act.swap(next);
   }
   d->last_ms = total_ms;
+#ifdef AB_PROFILE
+  {
+    unsigned long long pr[PF_N];
+    cudaMemcpyFromSymbol(pr, g_prof, sizeof(pr));
+    static const char *names[PF_N] = {"start", "row", "emit_x", "emit_s", "eps_x", "eps_s",
+                                      "prune_scan", "prune_sel", "prune_out", "hyp", "gc", "rounds"};
+    fprintf(stderr, "AB_PROFILE");
+    for (int q = 0; q < 12; ++q) fprintf(stderr, " %s=%llu", names[q], pr[q]);
+    fprintf(stderr, "\n");
+    unsigned long long z[PF_N] = {};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+#endif
   return AB_OK;
 }
 

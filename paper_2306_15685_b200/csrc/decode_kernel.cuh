@@ -343,6 +343,30 @@ __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
   return base + __popc(m & ((1u << lane) - 1u));
 }
 
+// ------------------------------------------------------------ phase profile
+// Built with -DAB_PROFILE only (scripts/, never the shipped library): thread 0
+// accumulates SM clock cycles per phase; the kernel adds them to g_prof.
+enum { PF_START = 0, PF_ROW, PF_EMIT_X, PF_EMIT_S, PF_EPS_X, PF_EPS_S, PF_PRUNE_SCAN, PF_PRUNE_SEL,
+       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_N = 16 };
+#ifdef AB_PROFILE
+__device__ unsigned long long g_prof[PF_N];
+#define PROF_MARK(sh, id)                                                                          \
+  do {                                                                                             \
+    if (threadIdx.x == 0) {                                                                        \
+      const long long t_ = clock64();                                                              \
+      (sh).prof[id] += (unsigned long long)(t_ - (sh).prof_t);                                     \
+      (sh).prof_t = t_;                                                                            \
+    }                                                                                              \
+  } while (0)
+#define PROF_COUNT(sh, id, v)                                                                      \
+  do {                                                                                             \
+    if (threadIdx.x == 0) (sh).prof[id] += (v);                                                    \
+  } while (0)
+#else
+#define PROF_MARK(sh, id) do { } while (0)
+#define PROF_COUNT(sh, id, v) do { } while (0)
+#endif
+
 // ------------------------------------------------------------ CTA state
 
 enum {
@@ -370,6 +394,10 @@ struct Shared {
   u32 reds[32];
   int redi[32];
   u32 hist[256];
+#ifdef AB_PROFILE
+  unsigned long long prof[PF_N];
+  long long prof_t;
+#endif
 };
 
 template <typename F, typename S> struct Chan {
@@ -717,12 +745,15 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     expand<BLOCK, 4, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
                             (u32)rounds);
     __syncthreads();
+    PROF_MARK(sh, PF_EPS_X);
+    PROF_COUNT(sh, PF_ROUNDS, 1);
     const u32 n_cand = sh.n_cand, n_app = sh.n_app;
     if (sh.error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
     const u32 row_base = sh.flog_n;
     snapshot<BLOCK>(P, C, sh, (u32)rounds, C.flog_info + fbase, n_app, row_base);
     __syncthreads();
+    PROF_MARK(sh, PF_EPS_S);
     if (threadIdx.x == 0) sh.flog_n = row_base + n_app;
     __syncthreads();
     if (sh.error) return;
@@ -840,6 +871,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     }
   }
   __syncthreads();
+  PROF_MARK(sh, PF_PRUNE_SCAN);
   const u32 n_keep = sh.n_keep;
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   u64 tc = ~0ull;
@@ -867,6 +899,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     sh.max_depth = 0;
   }
   __syncthreads();
+  PROF_MARK(sh, PF_PRUNE_SEL);
   int md = 0;
   for (u32 i0 = 0; i0 < n_keep; i0 += BLOCK) {
     const u32 i = i0 + tid;
@@ -900,6 +933,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       C.cs->info.trailing_silence = 0;
   }
   __syncthreads();
+  PROF_MARK(sh, PF_PRUNE_OUT);
 }
 
 // Token list := every live row of the epoch (after the utterance-start
@@ -1069,6 +1103,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   // one frame appends at most flog_cap records: collect first if they might not fit
   if (!cs->info.fresh && (unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
     gc_arena<BLOCK>(P, C, sh);
+    PROF_MARK(sh, PF_GC);
     if ((unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
       if (threadIdx.x == 0) set_error(sh, E_CAP);
       __syncthreads();
@@ -1083,11 +1118,13 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     if (threadIdx.x == 0) cs->info.fresh = 0;
   }
   __syncthreads();
+  PROF_MARK(sh, PF_START);
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   next_epoch<BLOCK>(P, C, sh);
   expand<BLOCK, TPT, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u);
   __syncthreads();
+  PROF_MARK(sh, PF_EMIT_X);
   if (sh.error) return;
   const u32 n_app = sh.n_app;
   if (n_app == 0) {
@@ -1096,6 +1133,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   } else {
     snapshot<BLOCK>(P, C, sh, 0u, C.tok_info, n_app, 0u);
     __syncthreads();
+    PROF_MARK(sh, PF_EMIT_S);
     if (threadIdx.x == 0) sh.flog_n = n_app;
     __syncthreads();
     if (sh.error) return;
@@ -1363,6 +1401,10 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
       sh.rec_logical = (unsigned long long)cs->info.store_len;
       sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
       sh.n_new = sh.n_app = sh.n_cand = sh.flog_n = 0;
+#ifdef AB_PROFILE
+      for (int q = 0; q < PF_N; ++q) sh.prof[q] = 0;
+      sh.prof_t = clock64();
+#endif
     }
     __syncthreads();
     const int T = P.frames[b];
@@ -1391,6 +1433,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         C.row = grow;
       }
       __syncthreads();
+      PROF_MARK(sh, PF_ROW);
       advance<BLOCK, TPT>(P, C, sh);
       if (sh.error) break;
       if (P.mode == AB_MODE_STREAM) {
@@ -1407,6 +1450,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
         }
       }
       __syncthreads();
+      PROF_MARK(sh, PF_HYP);
     }
     const bool done = t == T;
     if (P.mode == AB_MODE_STREAM && !sh.error && done) {
@@ -1425,6 +1469,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
       P.n_hyps[b] = n_out;
       P.errors[b] = sh.error;
       P.frames_done[b] = t;
+#ifdef AB_PROFILE
+      for (int q = 0; q < PF_N; ++q) atomicAdd(&g_prof[q], sh.prof[q]);
+#endif
     }
   }
 }
