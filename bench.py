@@ -263,9 +263,10 @@ def run_b200(args, W, world, rank, local):
     t0 = time.time()
     dg = DeviceGraph(csr, device=local)
     handles = [dg.register_context(c.arc_indices, c.discount) for c in pool]
+    # emission arena: ~16 frames of appends (~45k records per channel-frame on
+    # G_large); the in-kernel copying GC reclaims records of pruned paths
     big = W["states"] > 1_000_000
-    records_per_frame = 45_000 if big else 12_000
-    cap = Capacity(arena_records=int(records_per_frame * (Tseg + 2) * 1.15))
+    cap = Capacity(arena_records=(1 << 20) if big else (1 << 19))
     dec = BatchDecoder(dg, C, cap)
     prep["upload_s"] = time.time() - t0
     scores_dev = torch.from_numpy(scores_np).to(dev)

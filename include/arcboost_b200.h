@@ -49,8 +49,8 @@ enum {
            chosen by AUTO) when the context is exactly the set of arcs whose
            olabel lies in some label set, e.g. single-word entities */
 enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2, AB_CTX_LABELS = 3 };
-/* device limits */
-enum { AB_MAX_TABLE_SLOTS = 131072, AB_MAX_EPSILON_ROUNDS = 63 };
+/* device limits: distinct tokens per channel-frame, hashed-table slots, epsilon rounds */
+enum { AB_MAX_TOKENS = 131072, AB_MAX_HASH_SLOTS = 4194304, AB_MAX_EPSILON_ROUNDS = 63 };
 
 typedef struct ab_graph ab_graph;
 typedef struct ab_decoder ab_decoder;
@@ -68,7 +68,10 @@ typedef struct ab_config {
 
 /* Device capacities per channel; 0 selects a default derived from the graph. */
 typedef struct ab_capacity {
-  int64_t table_slots;   /* token-table slots (power of two) */
+  int64_t table_slots;   /* token table: >= num_states (or 0 when the budget allows: 20 B per
+                            state and channel, AB_DIRECT_TABLE_GB or 60% of free HBM) selects
+                            a direct table (slot = state); fewer slots a hashed table
+                            (rounded up to a power of two, <= AB_MAX_HASH_SLOTS) */
   int64_t frontier_rows; /* epsilon-frontier log rows per frame */
   int64_t arena_records; /* emission records per utterance */
   int64_t path_words;    /* longest hypothesis path */

@@ -29,7 +29,7 @@ AB_PARTIAL, AB_FINAL = 0, 1
 AB_F32, AB_F64 = 0, 1
 AB_MODE_ADVANCE, AB_MODE_STREAM = 0, 1
 AB_CTX_AUTO, AB_CTX_LIST, AB_CTX_BITSET, AB_CTX_LABELS = 0, 1, 2, 3
-AB_MAX_TABLE_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 63
+AB_MAX_TOKENS, AB_MAX_HASH_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 4194304, 63
 
 
 class ab_config(C.Structure):

@@ -65,7 +65,8 @@ struct ab_graph {
   std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
   u32 *e_off = nullptr, *x_off = nullptr;
   void *e_arcs = nullptr, *x_arcs = nullptr;
-  int2 *arc_meta = nullptr;
+  int2 *arc_meta = nullptr;  // labels that do not fit the packed form
+  u32 *arc_meta32 = nullptr; // olabel:16 | ilabel:15 | META_DEST_EPS
   double *final_cost = nullptr;
   size_t bytes = 0;
   std::vector<HostCtx> ctxs;
@@ -84,7 +85,9 @@ struct ab_decoder {
   u32 tok_cap = 0, flog_cap = 0, arena_cap = 0, path_cap = 0;
   size_t bytes = 0;
   ChanState *chans = nullptr;
-  Entry *table = nullptr;
+  Entry *table = nullptr;  // hashed
+  u64 *vals = nullptr;     // direct
+  u32 *app_old = nullptr;  // direct
   u32 *tok_state = nullptr;
   double *tok_cost = nullptr;
   TokInfo *tok_info = nullptr;
@@ -245,9 +248,22 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   size_t acc = 0;
   unsigned char *de = nullptr, *dx = nullptr;
+  // packed 4-byte arc metadata when every label fits (halves the snapshot's random reads)
+  bool pack = true;
+  for (size_t a = 0; a < meta.size() && pack; ++a)
+    pack = meta[a].x >= 0 && meta[a].x < 65536 && (meta[a].y & ~(int)META_DEST_EPS) >= 0 &&
+           (meta[a].y & ~(int)META_DEST_EPS) < 32768;
+  std::vector<u32> meta32;
+  if (pack) {
+    meta32.resize(meta.size());
+    for (size_t a = 0; a < meta.size(); ++a)
+      meta32[a] = (u32)meta[a].x | ((u32)(meta[a].y & 0x7FFF) << 16) | ((u32)meta[a].y & META_DEST_EPS);
+    meta.clear();
+  }
   if (dmalloc(&g->e_off, num_states + 1, acc) || dmalloc(&g->x_off, num_states + 1, acc) ||
       dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
-      dmalloc(&g->arc_meta, meta.size(), acc) || dmalloc(&g->final_cost, num_states, acc)) {
+      (pack ? dmalloc(&g->arc_meta32, meta32.size(), acc) : dmalloc(&g->arc_meta, meta.size(), acc)) ||
+      dmalloc(&g->final_cost, num_states, acc)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "device allocation for the graph failed (%zu bytes)", acc);
   }
@@ -259,7 +275,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       cudaMemcpy(g->x_off, x_cnt.data(), (num_states + 1) * sizeof(u32), cudaMemcpyHostToDevice) ||
       cudaMemcpy(de, eh.data(), eh.size(), cudaMemcpyHostToDevice) ||
       cudaMemcpy(dx, xh.data(), xh.size(), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(g->arc_meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice) ||
+      (pack ? cudaMemcpy(g->arc_meta32, meta32.data(), meta32.size() * sizeof(u32), cudaMemcpyHostToDevice)
+            : cudaMemcpy(g->arc_meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice)) ||
       cudaMemcpy(g->final_cost, fin.data(), num_states * sizeof(double), cudaMemcpyHostToDevice)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "graph upload failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -281,6 +298,7 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   cudaFree(g->e_arcs);
   cudaFree(g->x_arcs);
   cudaFree(g->arc_meta);
+  cudaFree(g->arc_meta32);
   cudaFree(g->final_cost);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -432,17 +450,40 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->g = g;
   d->device = g->device;
   d->max_ch = max_channels;
-  uint64_t ts = cap.table_slots;
-  if (ts <= 0) ts = std::min<uint64_t>((uint64_t)g->num_states, MAX_TABLE_SLOTS);
-  d->table_cap = next_pow2(ts);
-  if (d->table_cap > MAX_TABLE_SLOTS) {
-    delete d;
-    return fail(AB_ERR_INVALID, "table_slots too large (max %u)", MAX_TABLE_SLOTS);
+  // Token table: direct (one value per graph state) when it fits the memory
+  // budget next to the other per-channel pools, else hashed.  table_slots > 0
+  // forces the choice: >= num_states gives a direct table, fewer slots a
+  // hashed one.
+  const uint64_t S = (uint64_t)g->num_states;
+  int64_t ts = cap.table_slots;
+  if (ts <= 0) {
+    const uint64_t tk = std::min<uint64_t>(S, MAX_TOKENS);
+    const uint64_t fl = cap.frontier_rows > 0 ? (uint64_t)cap.frontier_rows : std::max<uint64_t>(65536, 2 * tk);
+    const uint64_t ar = cap.arena_records > 0 ? (uint64_t)cap.arena_records : std::max<uint64_t>(1ull << 19, 8 * fl);
+    const double per_ch_other = (double)tk * (4 + 8 + 16 + 4) + (double)fl * (4 + 8 + 16 + 8 + 4) +
+                                (double)ar * (2 * 8 + 2 * 4.0 / 32);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    double budget = 0.85 * (double)free_b - (double)max_channels * per_ch_other;
+    if (const char *e = getenv("AB_DIRECT_TABLE_GB")) budget = atof(e) * 1e9;
+    const double direct = (double)max_channels * (double)S * (2 * sizeof(u64));
+    ts = (S <= MAX_TOKENS || direct <= budget) ? (int64_t)S
+                                              : (int64_t)std::min<uint64_t>(next_pow2(4 * MAX_TOKENS), next_pow2(S));
   }
-  d->hashed = d->table_cap < (u32)g->num_states ? 1 : 0;
-  d->tok_cap = d->table_cap;
+  if ((uint64_t)ts >= S) {
+    d->hashed = 0;
+    d->table_cap = (u32)S;
+  } else {
+    d->hashed = 1;
+    d->table_cap = next_pow2((uint64_t)ts);
+    if (d->table_cap > MAX_HASH_SLOTS) {
+      delete d;
+      return fail(AB_ERR_INVALID, "table_slots too large (max %u)", MAX_HASH_SLOTS);
+    }
+  }
+  d->tok_cap = std::min<u32>(d->table_cap, MAX_TOKENS);
   d->flog_cap = (u32)(cap.frontier_rows > 0 ? cap.frontier_rows
-                                            : std::max<uint64_t>(65536, 2ull * d->table_cap));
+                                            : std::max<uint64_t>(65536, 2ull * d->tok_cap));
   // the arena must hold the live records plus one frame of appends (<= frontier rows)
   d->arena_cap = (u32)(cap.arena_records > 0 ? cap.arena_records
                                              : std::max<uint64_t>(1ull << 19, 8ull * d->flog_cap));
@@ -458,13 +499,16 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->cap.path_words = d->path_cap;
   const size_t C = (size_t)max_channels;
   size_t &acc = d->bytes;
-  if (dmalloc(&d->chans, C, acc) || dmalloc(&d->table, C * d->table_cap, acc) ||
+  const size_t hslots = d->hashed ? C * d->table_cap : 0, dslots = d->hashed ? 0 : C * d->table_cap;
+  if (dmalloc(&d->chans, C, acc) || (hslots && dmalloc(&d->table, hslots, acc)) ||
+      (dslots && dmalloc(&d->vals, 2 * dslots, acc)) ||
+      (dslots && dmalloc(&d->app_old, C * d->tok_cap, acc)) ||
       dmalloc(&d->tok_state, C * d->tok_cap, acc) || dmalloc(&d->tok_cost, C * d->tok_cap, acc) ||
       dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_info, C * d->flog_cap, acc) ||
-      dmalloc(&d->app_list, C * d->table_cap, acc) ||
+      dmalloc(&d->app_list, C * d->tok_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
       dmalloc(&d->arena, 2 * C * d->arena_cap, acc) ||
@@ -477,7 +521,8 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
     return fail(AB_ERR_CUDA, "device allocation for %d channels failed (%zu bytes requested)",
                 max_channels, need);
   }
-  if (cudaMemset(d->table, 0, C * d->table_cap * sizeof(Entry)) != cudaSuccess ||
+  if ((hslots && cudaMemset(d->table, 0, hslots * sizeof(Entry)) != cudaSuccess) ||
+      (dslots && cudaMemset(d->vals, 0, dslots * 2 * sizeof(u64)) != cudaSuccess) ||
       cudaMemset(d->chans, 0, C * sizeof(ChanState)) != cudaSuccess ||
       cudaEventCreate(&d->ev0) != cudaSuccess || cudaEventCreate(&d->ev1) != cudaSuccess) {
     ab_decoder_destroy(d);
@@ -502,7 +547,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
 extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
-  void *ptrs[] = {d->chans,     d->table,     d->tok_state, d->tok_cost, d->tok_info,
+  void *ptrs[] = {d->chans,     d->table,     d->vals,      d->app_old, d->tok_state, d->tok_cost, d->tok_info,
                   d->flog_state, d->flog_ck,  d->flog_info, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
@@ -743,6 +788,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.x_off = g->x_off;
   P.x_arcs = g->x_arcs;
   P.arc_meta = g->arc_meta;
+  P.arc_meta32 = g->arc_meta32;
   P.final_cost = g->final_cost;
   P.start = g->start;
   P.num_states = g->num_states;
@@ -751,6 +797,8 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.num_ctxs = (int)g->ctxs.size();
   P.chans = d->chans;
   P.table = d->table;
+  P.vals = d->vals;
+  P.app_old = d->app_old;
   P.table_cap = d->table_cap;
   P.table_mask = d->table_cap - 1;
   int lg = 0;
@@ -777,11 +825,13 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.path_cap = d->path_cap;
 }
 
+static size_t dyn_smem_max() { return CTX_SMEM_WORDS * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
+
 static int pick_block(int n) {
   const char *env = getenv("AB_BLOCK");
   if (env) {
     int b = atoi(env);
-    if (b == 128 || b == 256 || b == 512) return b;
+    if (b == 256) return b;
   }
   (void)n;
   return 256;
@@ -795,6 +845,9 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   if (per_sm < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
+    // static tiles + dynamic (context, score row) exceed the 48 KB default
+    cudaFuncSetAttribute(decode_kernel<BLOCK, F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dyn_smem_max());
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BLOCK, F, S>, BLOCK,
                                                       smem) != cudaSuccess || per_sm < 1)
@@ -814,8 +867,6 @@ template <typename F, typename S>
 static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, size_t smem,
                                    cudaStream_t st) {
   switch (block) {
-  case 128: return launch_decode<128, F, S>(P, grid, smem, st);
-  case 512: return launch_decode<512, F, S>(P, grid, smem, st);
   default: return launch_decode<256, F, S>(P, grid, smem, st);
   }
 }
@@ -977,6 +1028,12 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     const int block = pick_block(m);
     CK(cudaEventRecord(d->ev0, st));
     cudaError_t le;
+#ifdef AB_BENCH_ONLY
+    // experiment builds (scripts/build_variants.sh): only the C3 bench path
+    if (!(g->fmt16 && !s64)) return fail(AB_ERR_INVALID, "AB_BENCH_ONLY build");
+    le = d->hashed ? launch_decode_b<Fmt16<true>, float>(block, P, m, smem, st)
+                   : launch_decode_b<Fmt16<false>, float>(block, P, m, smem, st);
+#else
     if (d->hashed) {
       if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<true>, double>(block, P, m, smem, st)
                              : launch_decode_b<Fmt16<true>, float>(block, P, m, smem, st);
@@ -988,6 +1045,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       else le = s64 ? launch_decode_b<Fmt24<false>, double>(block, P, m, smem, st)
                     : launch_decode_b<Fmt24<false>, float>(block, P, m, smem, st);
     }
+#endif
     if (le != cudaSuccess) return fail(AB_ERR_CUDA, "decode launch: %s", cudaGetErrorString(le));
     d->last_launches += 1;
     CK(cudaEventRecord(d->ev1, st));

@@ -39,7 +39,8 @@ constexpr int BOOST_SHIFT = 25;
 constexpr int TAG_SHIFT = 17;
 constexpr u32 SRC_BITS = 17;
 constexpr u32 SRC_MASK = (1u << SRC_BITS) - 1;
-constexpr u32 MAX_TABLE_SLOTS = 1u << SRC_BITS;
+constexpr u32 MAX_TOKENS = 1u << SRC_BITS;      // distinct tokens per channel-frame
+constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per channel
 constexpr int MAX_EPS_ROUNDS = 63;
 constexpr u32 ROW_DEAD = 0x80000000u;       // frontier-log row superseded later in the frame
 constexpr u32 ROW_EPS = 0x40000000u;        // row's state has epsilon out-arcs
@@ -48,11 +49,22 @@ constexpr u32 META_DEST_EPS = 0x80000000u;  // arc_meta.y flag: the arc's destin
 constexpr u32 APP_IMPROVED = 0x80000000u;   // applied-list flag: slot existed this frame
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
-#ifndef AB_EXP_UNROLL
-#define AB_EXP_UNROLL 1
+#ifndef AB_EXP_Q
+#define AB_EXP_Q 2
 #endif
-constexpr int EXP_UNROLL = AB_EXP_UNROLL; // independent candidates in flight per thread (expansion)
-constexpr int UNROLL = 2;      // independent rows in flight per thread (snapshot)
+#ifndef AB_EXP_U
+#define AB_EXP_U 1
+#endif
+#ifndef AB_SNAP
+#define AB_SNAP 1
+#endif
+constexpr int EXP_Q = AB_EXP_Q; // inputs per thread per expansion tile (CSR range loads in flight)
+constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
+constexpr int SNAP = AB_SNAP;   // applied slots per thread in flight (snapshot)
+#ifndef AB_PRUNE_Q
+#define AB_PRUNE_Q 2
+#endif
+constexpr int PRUNE_Q = AB_PRUNE_Q; // rows per thread in flight (prune)
 
 enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
 
@@ -64,10 +76,13 @@ struct __align__(16) TokInfo {
   int last_il; // ilabel of the last emitting arc (decoder.py:393, 404)
 };
 
-// Token-table slot (32 B = one sector).  key = state | epoch << 32 (hashed
-// tables only).  value (16 B, the CAS-128 target) = ordered cost key, global
-// arc id, info.  A value whose epoch tag differs from the channel's current
-// tag is empty; the table is wiped when the 8-bit tag wraps (every 255 epochs).
+// Token table.  Hashed (graphs too large for a direct table in the memory
+// budget): 32-B slots (one sector), key = state | epoch << 32, the frontier
+// row of the slot's latest application, and the value.  Direct: one 16-B
+// value per graph state (slot = state, no key, no probing) plus a u32 row
+// array.  The value (16 B, the CAS-128 target) = ordered cost key, global arc
+// id, info.  A value whose epoch tag differs from the channel's current tag is
+// empty; the table is wiped when the 8-bit tag wraps (every 255 epochs).
 struct __align__(32) Entry {
   u64 key;
   u32 flog; // frontier-log row of the latest application in this frame
@@ -168,6 +183,7 @@ struct DecodeParams {
   const u32 *x_off;
   const void *x_arcs;
   const int2 *arc_meta; // [num_arcs] {olabel, ilabel | META_DEST_EPS} by global arc id
+  const u32 *arc_meta32; // packed olabel:16 | ilabel:15 | META_DEST_EPS when labels fit (else null)
   const double *final_cost; // NaN = not final
   int start;
   int num_states;
@@ -176,7 +192,9 @@ struct DecodeParams {
   int num_ctxs;
   // per-channel pools (slot-major)
   ChanState *chans;
-  Entry *table;
+  Entry *table;   // hashed
+  u64 *vals;      // direct: [channel][table_cap][2]
+  u32 *app_old;   // direct: [channel][tok_cap] row superseded by an improving application
   u32 table_cap, table_mask, hash_shift;
   int hashed;
   u32 *tok_state;
@@ -236,15 +254,15 @@ __device__ __forceinline__ void ld_cg_head(const Entry *e, u64 &key, u32 &flog) 
   key = a;
   flog = (u32)b;
 }
-__device__ __forceinline__ void ld_cg_value(const Entry *e, u64 &ck, u32 &g, u32 &info) {
+__device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
   u64 a, b;
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(&e->ck));
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v));
   ck = a;
   g = (u32)b;
   info = (u32)(b >> 32);
 }
 // 128-bit compare-and-swap on the value half of an entry (ATOMG.E.CAS.128).
-__device__ __forceinline__ bool cas_value(Entry *e, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng,
+__device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng,
                                           u32 ninfo) {
   u64 e0 = ck, e1 = ((u64)info << 32) | g;
   u64 d0 = nck, d1 = ((u64)ninfo << 32) | ng;
@@ -253,13 +271,24 @@ __device__ __forceinline__ bool cas_value(Entry *e, u64 &ck, u32 &g, u32 &info, 
       "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
       " atom.global.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
       : "=l"(r0), "=l"(r1)
-      : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(&e->ck)
+      : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(v)
       : "memory");
   bool ok = (r0 == e0) && (r1 == e1);
   ck = r0;
   g = (u32)r1;
   info = (u32)(r1 >> 32);
   return ok;
+}
+
+// CAS-128 that only issues: the old value comes back in (r0, r1); the caller
+// compares, so several can be in flight per thread.
+__device__ __forceinline__ void cas128(u64 *addr, u64 e0, u64 e1, u64 d0, u64 d1, u64 &r0, u64 &r1) {
+  asm volatile(
+      "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
+      " atom.global.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
+      : "=l"(r0), "=l"(r1)
+      : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(addr)
+      : "memory");
 }
 
 // L2 prefetch: memory-level parallelism that costs no registers
@@ -406,6 +435,8 @@ template <typename F, typename S> struct Chan {
   int slot;
   ChanState *cs;
   Entry *table;
+  u64 *vals;
+  u32 *app_old;
   u32 *tok_state;
   double *tok_cost;
   TokInfo *tok_info;
@@ -431,6 +462,10 @@ template <typename F, typename S> struct Chan {
   u32 ctx_words;
   u32 epoch;
   u32 etag;
+  // expansion tile (shared memory)
+  u32 *t_a0;
+  u32 *t_pref;
+  double *t_cost;
 };
 
 // BiasingContext.boosted_mask (biasing.py:108-117) in the representation the
@@ -461,184 +496,291 @@ __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.
 template <bool H> __device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
   return H ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
 }
+// value / frontier-row word of a slot (direct tables: the value's arc field)
+template <typename F, typename S> __device__ __forceinline__ u64 *val_at(const Chan<F, S> &C, u32 slot) {
+  return F::hashed ? &C.table[slot].ck : C.vals + 2 * (size_t)slot;
+}
+template <typename F, typename S> __device__ __forceinline__ u32 *row_at(const Chan<F, S> &C, u32 slot) {
+  return F::hashed ? &C.table[slot].flog : reinterpret_cast<u32 *>(C.vals + 2 * (size_t)slot + 1);
+}
 
-// Relaxation of one candidate into the token table (decoder.py:213-220 for
-// the emitting pass; 277-308 for epsilon rounds), starting from the entry
-// contents already loaded in (key, vck, vg, vinfo).  Hashed tables claim the
-// slot's key with a 64-bit CAS; the value is a CAS-128 minimum with the phase
-// rule:
-//   empty (stale tag)          -> take it: a new table entry
+// Value half of a relaxation (decoder.py:213-220 emitting, 277-308 epsilon):
+// CAS-128 minimum with the phase rule
+//   empty (stale tag)           -> take it: a new table entry
 //   value from an earlier round -> replace iff strictly cheaper (cost only)
 //   value from this round       -> replace iff (cost, arc) is smaller
+// starting from the value already loaded in (vck, vg, vinfo).  Returns 0 (not
+// applied), 1 (new entry) or 2 (improved an entry of an earlier round).
+__device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 round, u32 etag, u64 vck, u32 vg,
+                                             u32 vinfo) {
+  const bool valid = ((vinfo >> TAG_SHIFT) & 0xFFu) == etag;
+  const u32 cround = vinfo >> ROUND_SHIFT;
+  return !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
+}
+__device__ __forceinline__ int applied_code(u32 round, u32 etag, u32 old_info) {
+  if (((old_info >> TAG_SHIFT) & 0xFFu) != etag) return 1;
+  return (old_info >> ROUND_SHIFT) < round ? 2 : 0;
+}
+__device__ __forceinline__ int relax_value(u64 *e, u64 ck, u32 g, u32 info, u32 round, u32 etag,
+                                          u64 vck, u32 vg, u32 vinfo, u32 &old_g) {
+  while (true) {
+    if (!value_better(ck, g, round, etag, vck, vg, vinfo)) return 0;
+    const u32 old_info = vinfo;
+    old_g = vg;
+    if (cas_value(e, vck, vg, vinfo, ck, g, info)) return applied_code(round, etag, old_info);
+  }
+}
+
+// Records one application in the applied-slot list.  Direct tables keep the
+// frontier row of a slot's latest application in the value's arc field
+// (snapshot writes it; values of earlier rounds are compared by cost only), so
+// an improvement carries the row it supersedes (`old_g`) in app_old.
 template <typename F, typename S>
-__device__ __forceinline__ void relax(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
-                                      u32 info, u32 round, u32 slot, u64 key, u64 vck, u32 vg,
-                                      u32 vinfo) {
-  if (F::hashed) {
-    const u64 ep = (u64)C.epoch << 32;
-    u32 probes = 0;
-    while (true) {
-      Entry *e = &C.table[slot];
-      if ((key & KEY_EPOCH_MASK) != ep) {
-        const u64 want = (u64)d | ep;
-        const u64 old = atomicCAS(&e->key, key, want);
-        key = old == key ? want : old;
-        continue;
+__device__ __forceinline__ void record_applied(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
+                                               u32 slot, int code, u32 old_g) {
+  if (code == 1 && atomicAdd(&sh.n_new, 1u) + 1u > P.tok_cap) set_error(sh, E_CAP);
+  const u32 ip = atomicAdd(&sh.n_app, 1u);
+  if (ip < P.tok_cap) {
+    C.app_list[ip] = slot | (code == 2 ? APP_IMPROVED : 0u);
+    if (!F::hashed && code == 2) C.app_old[ip] = old_g;
+  }
+}
+
+// Sequential relaxation with linear probing (hashed tables: the home slot
+// belongs to another state).  (key, vck, vg, vinfo) = contents of `slot`.
+template <typename F, typename S>
+__device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
+                            u32 info, u32 round, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
+  const u64 ep = (u64)C.epoch << 32;
+  u32 probes = 0;
+  while (true) {
+    Entry *e = &C.table[slot];
+    if ((key & KEY_EPOCH_MASK) != ep) {
+      const u64 want = (u64)d | ep;
+      const u64 old = atomicCAS(&e->key, key, want);
+      key = old == key ? want : old;
+      continue;
+    }
+    if ((u32)key == d) break;
+    slot = (slot + 1) & P.table_mask;
+    if (++probes > P.table_mask) {
+      set_error(sh, E_CAP);
+      return;
+    }
+    u32 fl;
+    ld_cg_head(&C.table[slot], key, fl);
+    ld_cg_value(val_at(C, slot), vck, vg, vinfo);
+  }
+  u32 old_g = 0;
+  const int r = relax_value(val_at(C, slot), ck, g, info, round, C.etag, vck, vg, vinfo, old_g);
+  if (r) record_applied(P, C, sh, slot, r, old_g);
+}
+
+// Relaxation of U independent candidates of one thread.  Every memory step
+// is issued for all U candidates before any result is consumed, so a thread
+// keeps U table round trips in flight: loads of the entries, key claims
+// (hashed tables), value CAS-128s.  Lost races and probe chains fall back to
+// the sequential path.
+template <int U, typename F, typename S>
+__device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
+                                            const bool (&on)[U], const u32 (&d)[U],
+                                            const u64 (&ck)[U], const u32 (&g)[U],
+                                            const u32 (&info)[U], u32 round) {
+  const u32 etag = C.etag;
+  const u64 ep = (u64)C.epoch << 32;
+  u32 slot[U];
+  u64 key[U], vck[U];
+  u32 vg[U], vinfo[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    slot[u] = home_slot<F::hashed>(P, d[u]);
+    key[u] = 0;
+    vck[u] = 0;
+    vg[u] = 0;
+    vinfo[u] = 0;
+    if (on[u]) {
+      if (F::hashed) {
+        u32 fl;
+        ld_cg_head(&C.table[slot[u]], key[u], fl);
       }
-      if ((u32)key == d) break;
-      slot = (slot + 1) & P.table_mask;
-      if (++probes > P.table_mask) {
-        set_error(sh, E_CAP);
-        return;
-      }
-      u32 fl;
-      ld_cg_head(&C.table[slot], key, fl);
-      ld_cg_value(&C.table[slot], vck, vg, vinfo);
+      ld_cg_value(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
     }
   }
-  Entry *e = &C.table[slot];
-  while (true) {
-    const bool valid = ((vinfo >> TAG_SHIFT) & 0xFFu) == C.etag;
-    const u32 cround = vinfo >> ROUND_SHIFT;
-    const bool better =
-        !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
-    if (!better) return;
-    if (cas_value(e, vck, vg, vinfo, ck, g, info)) {
-      if (!valid) {
-        if (atomicAdd(&sh.n_new, 1u) >= P.tok_cap) set_error(sh, E_CAP);
-        const u32 ip = atomicAdd(&sh.n_app, 1u);
-        if (ip < P.table_cap) C.app_list[ip] = slot;
-      } else if (cround < round) {
-        const u32 ip = atomicAdd(&sh.n_app, 1u);
-        if (ip < P.table_cap) C.app_list[ip] = slot | APP_IMPROVED;
+  bool fast[U];
+  if (F::hashed) {
+    u64 old[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (on[u] && (key[u] & KEY_EPOCH_MASK) != ep)
+        old[u] = atomicCAS(&C.table[slot[u]].key, key[u], (u64)d[u] | ep);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (on[u] && (key[u] & KEY_EPOCH_MASK) != ep) key[u] = old[u] == key[u] ? ((u64)d[u] | ep) : old[u];
+      fast[u] = on[u] && (key[u] & KEY_EPOCH_MASK) == ep && (u32)key[u] == d[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (on[u] && !fast[u]) relax_probe<F, S>(P, C, sh, d[u], ck[u], g[u], info[u], round, slot[u], key[u], vck[u], vg[u], vinfo[u]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) fast[u] = on[u];
+  }
+  bool want[U];
+  u64 r0[U], r1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    want[u] = fast[u] && value_better(ck[u], g[u], round, etag, vck[u], vg[u], vinfo[u]);
+    if (want[u])
+      cas128(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u],
+             ((u64)info[u] << 32) | g[u], r0[u], r1[u]);
+  }
+  int code[U];
+  u32 n_new = 0, n_app = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    code[u] = 0;
+    if (!want[u]) continue;
+    if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u])) {
+      code[u] = applied_code(round, etag, vinfo[u]);
+    } else {
+      code[u] = relax_value(val_at(C, slot[u]), ck[u], g[u], info[u], round, etag, r0[u], (u32)r1[u],
+                            (u32)(r1[u] >> 32), vg[u]);
+    }
+    n_app += code[u] != 0;
+    n_new += code[u] == 1;
+  }
+  if (n_new && atomicAdd(&sh.n_new, n_new) + n_new > P.tok_cap) set_error(sh, E_CAP);
+  if (n_app) {
+    u32 ip = atomicAdd(&sh.n_app, n_app);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!code[u]) continue;
+      if (ip < P.tok_cap) {
+        C.app_list[ip] = slot[u] | (code[u] == 2 ? APP_IMPROVED : 0u);
+        if (!F::hashed && code[u] == 2) C.app_old[ip] = vg[u];
       }
-      return;
+      ++ip;
     }
   }
 }
 
-// Load-balanced expansion of a token list over one CSR (emitting or epsilon):
-// tiles of TPT*BLOCK tokens, block scan of out-degrees, then each thread walks
-// arc positions k, k + BLOCK, ... and locates their tokens by binary search
-// over the tile prefix.  Software pipeline per thread: the arc record of the
-// next position and the table slot of the current candidate are prefetched to
-// L2 one iteration before they are used, and the candidate is relaxed one
-// iteration late.
-template <int BLOCK, int TPT, bool EMIT, typename F, typename S>
+// Expansion of an input list (token list or frontier rows) over one CSR
+// (emitting or epsilon), in tiles of BLOCK * Q inputs:
+//   1. each thread loads Q consecutive inputs and their CSR ranges (all loads
+//      independent), one block scan of the out-degrees;
+//   2. the tile's arcs are split into one contiguous range per thread; a
+//      thread walks its range U arcs at a time: U arc-record loads, U
+//      candidates (boost lookup fused into the cost add), one batched
+//      relaxation.
+template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state,
                        const u64 *in_ck, const double *in_cost, u32 n_in, u32 round) {
-  constexpr int TILE = BLOCK * TPT;
-  __shared__ u32 t_a0[TILE];
-  __shared__ u32 t_pref[TILE];
-  __shared__ double t_cost[TILE];
+  constexpr u32 TILE = BLOCK * Q;
+  u32 *t_a0 = C.t_a0;
+  u32 *t_pref = C.t_pref;
+  double *t_cost = C.t_cost;
   const int tid = threadIdx.x;
   const u32 *off = EMIT ? P.e_off : P.x_off;
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
-  constexpr u32 REC = EMIT ? (u32)sizeof(typename F::E) : (u32)sizeof(typename F::X);
-  const u32 tag_bits = C.etag << TAG_SHIFT;
-  const u32 round_bits = round << ROUND_SHIFT;
+  const u32 info_hi = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT);
   u32 arcs_seen = 0;
-  auto locate = [&](u32 k) -> u32 { // largest j with t_pref[j] <= k (its count is > 0)
-    u32 lo = 0, hi = TILE - 1;
-    while (lo < hi) {
-      const u32 mid = (lo + hi + 1) >> 1;
-      if (t_pref[mid] <= k) lo = mid;
-      else hi = mid - 1;
-    }
-    return lo;
-  };
   for (u32 base = 0; base < n_in; base += TILE) {
-    u32 a0[TPT], cnt[TPT], s[TPT];
-    double c[TPT];
+    const u32 i0 = base + (u32)tid * Q;
+    u32 st[Q], a0[Q], cnt[Q];
+    double c[Q];
 #pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      const u32 i = base + q * BLOCK + tid;
-      s[q] = 0xFFFFFFFFu;
-      c[q] = 0.0;
-      if (i < n_in) {
-        s[q] = in_state[i];
-        c[q] = in_ck ? key_cost(in_ck[i]) : in_cost[i];
-      }
-    }
-    u32 sum = 0;
+    for (int q = 0; q < Q; ++q) st[q] = i0 + q < n_in ? in_state[i0 + q] : 0xFFFFFFFFu;
 #pragma unroll
-    for (int q = 0; q < TPT; ++q) {
+    for (int q = 0; q < Q; ++q) c[q] = i0 + q < n_in ? (in_ck ? key_cost(in_ck[i0 + q]) : in_cost[i0 + q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (s[q] != 0xFFFFFFFFu && (EMIT || (s[q] & ROW_EPS))) {
-        const u32 st = EMIT ? s[q] : (s[q] & ROW_STATE);
-        a0[q] = __ldg(&off[st]);
-        cnt[q] = __ldg(&off[st + 1]) - a0[q];
+      if (st[q] != 0xFFFFFFFFu && (EMIT || (st[q] & ROW_EPS))) {
+        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
+        a0[q] = __ldg(&off[s]);
+        cnt[q] = __ldg(&off[s + 1]);
       }
     }
-    // tile order is (q, tid): token q * BLOCK + tid of the tile
-    u32 tot[TPT];
-    u32 ex[TPT];
+    u32 tsum = 0;
 #pragma unroll
-    for (int q = 0; q < TPT; ++q) ex[q] = block_excl_scan<BLOCK>(cnt[q], tot[q], sh.scan);
-    u32 qbase = 0;
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      const u32 j = q * BLOCK + tid;
-      t_a0[j] = a0[q];
-      t_pref[j] = qbase + ex[q];
-      t_cost[j] = c[q];
-      qbase += tot[q];
+    for (int q = 0; q < Q; ++q) {
+      cnt[q] -= a0[q];
+      tsum += cnt[q];
     }
-    const u32 total = qbase;
+    u32 total;
+    u32 run = block_excl_scan<BLOCK>(tsum, total, sh.scan);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const u32 j = (u32)tid * Q + q;
+      t_a0[j] = a0[q];
+      t_pref[j] = run;
+      t_cost[j] = c[q];
+      run += cnt[q];
+    }
+    if (tid == 0) t_pref[TILE] = total;
     __syncthreads();
     arcs_seen += total;
-    // pipeline: prev = candidate waiting for its (prefetched) slot
-    bool have_prev = false;
-    u32 pd = 0, pg = 0, pinfo = 0;
-    u64 pck = 0;
-    u32 k = tid;
-    if (k < total) {
-      const u32 j = locate(k);
-      prefetch_l2(reinterpret_cast<const char *>(arcs) + (size_t)(t_a0[j] + (k - t_pref[j])) * REC);
+    const u32 per = (total + BLOCK - 1) / BLOCK;
+    u32 k = min((u32)tid * per, total);
+    const u32 ke = min(k + per, total);
+    u32 j = 0;
+    if (k < ke) { // largest j with t_pref[j] <= k
+      u32 lo = 0, hi = TILE - 1;
+      while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (t_pref[mid] <= k) lo = mid;
+        else hi = mid - 1;
+      }
+      j = lo;
     }
-    while (true) {
-      const bool cur = k < total;
-      u32 d = 0, g = 0, info = 0;
-      u64 ck = 0;
-      if (cur) {
-        const u32 j = locate(k);
-        const u32 a = t_a0[j] + (k - t_pref[j]);
-        const double cj = t_cost[j];
-        u32 il = 0, ol;
-        double w;
-        if (EMIT) F::emit(arcs, a, d, g, w, il, ol);
-        else F::eps(arcs, a, d, g, w, ol);
-        // _effective_weights (decoder.py:234-240): boost fused into the cost add
-        const bool bst = is_boosted(C, g, ol);
-        const double we = bst ? w + C.discount : w;
-        double cand;
-        if (EMIT) cand = (cj + we) + (double)C.row[il - 1]; // decoder.py:378
-        else cand = cj + we;                                 // decoder.py:268
-        ck = cost_key(cand);
-        info = round_bits | (bst ? (1u << BOOST_SHIFT) : 0u) | tag_bits | ((base + j) & SRC_MASK);
-        prefetch_l2(&C.table[home_slot<F::hashed>(P, d)]);
-        const u32 k2 = k + BLOCK;
-        if (k2 < total) {
-          const u32 j2 = locate(k2);
-          prefetch_l2(reinterpret_cast<const char *>(arcs) + (size_t)(t_a0[j2] + (k2 - t_pref[j2])) * REC);
+    while (k < ke) {
+      bool on[U];
+      u32 a[U], src[U];
+      double cj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        on[u] = k + u < ke;
+        a[u] = 0;
+        src[u] = 0;
+        cj[u] = 0.0;
+        if (on[u]) {
+          while (t_pref[j + 1] <= k + u) ++j;
+          a[u] = t_a0[j] + (k + u - t_pref[j]);
+          src[u] = base + j;
+          cj[u] = t_cost[j];
         }
       }
-      if (have_prev) {
-        const u32 slot = home_slot<F::hashed>(P, pd);
-        u64 key = 0, vck;
-        u32 fl, vg, vinfo;
-        if (F::hashed) ld_cg_head(&C.table[slot], key, fl);
-        ld_cg_value(&C.table[slot], vck, vg, vinfo);
-        relax(P, C, sh, pd, pck, pg, pinfo, round, slot, key, vck, vg, vinfo);
+      u32 d[U], g[U], il[U], ol[U];
+      double w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        d[u] = g[u] = il[u] = ol[u] = 0;
+        w[u] = 0.0;
+        if (on[u]) {
+          if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
+          else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
+        }
       }
-      if (!cur) break;
-      pd = d;
-      pg = g;
-      pck = ck;
-      pinfo = info;
-      have_prev = true;
-      k += BLOCK;
+      u64 ck[U];
+      u32 info[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ck[u] = 0;
+        info[u] = 0;
+        if (on[u]) {
+          // _effective_weights (decoder.py:234-240): boost fused into the cost add
+          const bool bst = is_boosted(C, g[u], ol[u]);
+          const double we = bst ? w[u] + C.discount : w[u];
+          double cand;
+          if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
+          else cand = cj[u] + we;                                    // decoder.py:268
+          ck[u] = cost_key(cand);
+          info[u] = info_hi | (bst ? (1u << BOOST_SHIFT) : 0u) | (src[u] & SRC_MASK);
+        }
+      }
+      relax_batch<U>(P, C, sh, on, d, ck, g, info, round);
+      k += U;
     }
     __syncthreads();
   }
@@ -653,7 +795,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 // Snapshot of the slots applied in one phase into the frontier log: resolves
 // the winner's provenance, appends emission records for olabel != 0
 // (decoder.py:385-389, 289-295), points the slot at its row and retires the
-// row of an improved slot's previous application.
+// row of an improved slot's previous application.  SNAP rows in flight per
+// thread; every load step is issued for all of them first.
 template <int BLOCK, typename F, typename S>
 __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 round, const TokInfo *src_info,
                          u32 n_app, u32 row_base) {
@@ -662,12 +805,13 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
     return;
   }
   u64 mck = ~0ull;
-  for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * UNROLL) {
-    u32 slot[UNROLL], d[UNROLL], g[UNROLL], info[UNROLL], oldrow[UNROLL];
-    u64 ck[UNROLL];
-    bool on[UNROLL], imp[UNROLL];
+  u32 n_rec_logical = 0;
+  for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * SNAP) {
+    u32 slot[SNAP], d[SNAP], g[SNAP], info[SNAP], oldrow[SNAP] = {};
+    u64 ck[SNAP];
+    bool on[SNAP], imp[SNAP];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < SNAP; ++u) {
       const u32 i = i0 + u * BLOCK;
       on[u] = i < n_app;
       slot[u] = 0;
@@ -676,27 +820,44 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
       const u32 a = C.app_list[i];
       slot[u] = a & ~APP_IMPROVED;
       imp[u] = (a & APP_IMPROVED) != 0;
+      oldrow[u] = (!F::hashed && imp[u]) ? C.app_old[i] : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < SNAP; ++u) {
+      d[u] = 0;
+      ck[u] = 0;
+      g[u] = 0;
+      info[u] = 0;
       if (!on[u]) continue;
-      const Entry *e = &C.table[slot[u]];
-      u64 key = slot[u];
-      oldrow[u] = 0;
-      if (F::hashed || imp[u]) ld_cg_head(e, key, oldrow[u]);
-      d[u] = F::hashed ? (u32)key : slot[u];
-      ld_cg_value(e, ck[u], g[u], info[u]);
+      if (F::hashed) {
+        u64 key;
+        ld_cg_head(&C.table[slot[u]], key, oldrow[u]);
+        d[u] = (u32)key;
+      } else {
+        d[u] = slot[u];
+      }
+      ld_cg_value(val_at(C, slot[u]), ck[u], g[u], info[u]);
     }
-    TokInfo si[UNROLL];
-    int2 meta[UNROLL];
+    TokInfo si[SNAP];
+    int2 meta[SNAP];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < SNAP; ++u) {
       if (!on[u]) continue;
       si[u] = src_info[info[u] & SRC_MASK];
-      meta[u] = __ldg(&P.arc_meta[g[u]]);
+      if (P.arc_meta32) {
+        const u32 m = __ldg(&P.arc_meta32[g[u]]);
+        meta[u] = make_int2((int)(m & 0xFFFFu), (int)((m >> 16) & 0x7FFFu) | (int)(m & META_DEST_EPS));
+      } else {
+        meta[u] = __ldg(&P.arc_meta[g[u]]);
+      }
     }
+    u32 nrec = 0;
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < SNAP; ++u) nrec += (on[u] && meta[u].x != 0) ? 1u : 0u;
+    u32 r = nrec ? atomicAdd(&sh.rec_n, nrec) : 0u;
+    n_rec_logical += nrec;
+#pragma unroll
+    for (int u = 0; u < SNAP; ++u) {
       if (!on[u]) continue;
       TokInfo ni;
       ni.bp = si[u].bp;
@@ -704,8 +865,6 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
       ni.hits = si[u].hits + ((info[u] >> BOOST_SHIFT) & 1);
       ni.last_il = round == 0 ? (int)((u32)meta[u].y & ~META_DEST_EPS) : si[u].last_il;
       if (meta[u].x != 0) {
-        atomicAdd(&sh.rec_logical, 1ull);
-        const u32 r = atomicAdd(&sh.rec_n, 1u);
         if (r < P.arena_cap) {
           C.arena[r] = make_int2(meta[u].x, si[u].bp);
           ni.bp = (int)r;
@@ -713,16 +872,18 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
         } else {
           set_error(sh, E_CAP);
         }
+        ++r;
       }
       const u32 row = row_base + i0 + u * BLOCK;
       C.flog_state[row] = d[u] | (((u32)meta[u].y & META_DEST_EPS) ? ROW_EPS : 0u);
       C.flog_ck[row] = ck[u];
       C.flog_info[row] = ni;
-      C.table[slot[u]].flog = row;
+      *row_at(C, slot[u]) = row;
       if (imp[u]) atomicOr(&C.flog_state[oldrow[u]], ROW_DEAD);
       mck = min(mck, ck[u]);
     }
   }
+  if (n_rec_logical) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec_logical);
   if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
 }
 
@@ -742,8 +903,8 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       sh.n_cand = 0;
     }
     __syncthreads();
-    expand<BLOCK, 4, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
-                            (u32)rounds);
+    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
+                                       (u32)rounds);
     __syncthreads();
     PROF_MARK(sh, PF_EPS_X);
     PROF_COUNT(sh, PF_ROUNDS, 1);
@@ -763,14 +924,15 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
   __syncthreads();
 }
 
-// Radix select over 64-bit keys (MSD, 8-bit digits, starting below the
+// Radix select over 64-bit keys (MSD, DB-bit digits, starting below the
 // highest bit where the bounds [lo, hi] of all candidate keys differ).
 // Returns t with count(key < t) < need <= count(key <= t).  On return
 // `exact` tells whether ties at t still have to be resolved (then `need` is
 // the number of keys equal to t that survive); otherwise every key <= t
-// survives.
-template <int BLOCK, typename KeyFn>
-__device__ u64 radix_select(Shared &sh, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &need,
+// survives.  Each pass reads the keys QR per thread (loads first), into a
+// 2^DB-bucket shared histogram.
+template <int BLOCK, int QR, int DB, typename KeyFn>
+__device__ u64 radix_select(Shared &sh, u32 *hist, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &need,
                             bool &exact) {
   const int tid = threadIdx.x;
   exact = true;
@@ -778,53 +940,46 @@ __device__ u64 radix_select(Shared &sh, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &
   int pos = 63 - __clzll(lo ^ hi);
   u64 prefix = pos >= 63 ? 0ull : (lo & ~((1ull << (pos + 1)) - 1));
   while (true) {
-    const int lowbit = pos >= 7 ? pos - 7 : 0;
+    const int lowbit = pos >= DB - 1 ? pos - (DB - 1) : 0;
     const int nb = pos - lowbit + 1;
+    const u32 nbk = 1u << nb;
     const u64 above = pos >= 63 ? 0ull : ~((1ull << (pos + 1)) - 1);
-    for (int b = tid; b < 256; b += BLOCK) sh.hist[b] = 0;
+    for (u32 b = tid; b < nbk; b += BLOCK) hist[b] = 0;
     __syncthreads();
-    for (u32 i = tid; i < n; i += BLOCK) {
-      bool ok;
-      const u64 kk = keyf(i, ok);
-      if (ok && (kk & above) == prefix) atomicAdd(&sh.hist[(kk >> lowbit) & ((1u << nb) - 1)], 1u);
+    for (u32 base = 0; base < n; base += BLOCK * QR) {
+      u64 kk[QR];
+      bool ok[QR];
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        const u32 i = base + q * BLOCK + tid;
+        ok[q] = i < n;
+        kk[q] = ok[q] ? keyf(i, ok[q]) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < QR; ++q)
+        if (ok[q] && (kk[q] & above) == prefix) atomicAdd(&hist[(kk[q] >> lowbit) & (nbk - 1)], 1u);
     }
     __syncthreads();
-    if (tid < 32) {
-      // warp scan over the buckets (8 per lane) to find the bucket of the need-th key
-      const u32 nbk = 1u << nb;
-      u32 loc[8];
-      u32 lsum = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const u32 b = tid * 8 + q;
-        loc[q] = b < nbk ? sh.hist[b] : 0u;
-        lsum += loc[q];
+    // bucket holding the need-th key: contiguous bucket chunks per thread + block scan
+    const u32 per = (nbk + BLOCK - 1) / BLOCK;
+    const u32 b0 = min((u32)tid * per, nbk), b1 = min(b0 + per, nbk);
+    u32 lsum = 0;
+    for (u32 b = b0; b < b1; ++b) lsum += hist[b];
+    u32 total;
+    const u32 excl = block_excl_scan<BLOCK>(lsum, total, sh.scan);
+    if (excl < need && need <= excl + lsum) {
+      u32 cum = excl, b = b0;
+      for (; b < b1; ++b) {
+        if (cum + hist[b] >= need) break;
+        cum += hist[b];
       }
-      u32 incl = lsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      const u32 excl = incl - lsum;
-      if (excl < need && need <= incl) {
-        u32 cum = excl, b = tid * 8;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (cum + loc[q] >= need) {
-            b = tid * 8 + q;
-            break;
-          }
-          cum += loc[q];
-        }
-        sh.sel = b;
-        sh.cum = cum;
-      }
+      sh.sel = b;
+      sh.cum = cum;
     }
     __syncthreads();
     const u32 b = sh.sel;
     need -= sh.cum;
-    const u32 cnt = sh.hist[b];
+    const u32 cnt = hist[b];
     __syncthreads();
     prefix |= ((u64)b << lowbit);
     if (lowbit == 0) {
@@ -841,91 +996,121 @@ __device__ u64 radix_select(Shared &sh, u32 n, KeyFn keyf, u64 lo, u64 hi, u32 &
 
 // _prune (decoder.py:319-334) + _best_token_pos (337-338) + silence
 // bookkeeping (400-407) over the live rows of the frame's frontier log.
+//   scan:   rows QP per thread (loads first), live and within the beam ->
+//           compacted (cost key, row, state) by block scan;
+//   select: if more than max_active survive, exact top-k by (cost, state):
+//           radix select on the cost keys, then on states for ties;
+//   output: survivors -> token list (provenance gathered QP per thread).
 template <int BLOCK, typename F, typename S>
 __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+  constexpr int QP = PRUNE_Q;
+  constexpr u32 TILE = BLOCK * QP;
+  constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : 10; // histogram lives in the expansion tile
   const int tid = threadIdx.x;
   const u32 n_rows = sh.flog_n;
   const u64 best_ck = sh.min_ck;
   const double thr = key_cost(best_ck) + P.beam;
   const u64 thr_ck = cost_key(thr);
-  if (tid == 0) sh.n_keep = 0;
-  __syncthreads();
+  u32 *scr_state = C.app_list; // the applied-slot list is free until the next frame
   u64 bk = ~0ull;
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
-  for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
-    const u32 i = i0 + tid;
-    u32 st = ROW_DEAD;
-    u64 ck = ~0ull;
-    if (i < n_rows) {
-      st = C.flog_state[i];
-      ck = C.flog_ck[i];
+  u32 n_keep = 0;
+  for (u32 base = 0; base < n_rows; base += TILE) {
+    const u32 i0 = base + (u32)tid * QP;
+    u32 st[QP];
+    u64 ck[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DEAD;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
+    u32 cnt = 0;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) cnt += (!(st[q] & ROW_DEAD) && ck[q] <= thr_ck) ? 1u : 0u;
+    u32 total;
+    u32 p = n_keep + block_excl_scan<BLOCK>(cnt, total, sh.scan);
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      if ((st[q] & ROW_DEAD) || ck[q] > thr_ck) continue;
+      const u32 s = st[q] & ROW_STATE;
+      C.scr_key[p] = ck[q];
+      C.scr_row[p] = i0 + q;
+      scr_state[p] = s;
+      ++p;
+      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
     }
-    const bool in = !(st & ROW_DEAD) && ck <= thr_ck;
-    st &= ROW_STATE;
-    const u32 p = warp_append(&sh.n_keep, in);
-    if (in) {
-      C.scr_key[p] = ck;
-      C.scr_row[p] = i;
-      if (ck < bk || (ck == bk && st < bs)) bk = ck, bs = st, bi = (int)i;
-    }
+    n_keep += total;
   }
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_SCAN);
-  const u32 n_keep = sh.n_keep;
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   u64 tc = ~0ull;
   u32 ts = 0xFFFFFFFFu;
   if (n_keep > (u32)P.max_active) {
     u32 need = (u32)P.max_active;
+    u32 *hist = C.t_a0;
     auto kf = [&](u32 i, bool &ok) -> u64 {
       ok = true;
       return C.scr_key[i];
     };
     bool exact;
-    tc = radix_select<BLOCK>(sh, n_keep, kf, best_ck, thr_ck, need, exact);
+    tc = radix_select<BLOCK, 8, DB>(sh, hist, n_keep, kf, best_ck, thr_ck, need, exact);
     if (exact) {
       // ties at the threshold cost: the smallest states survive
       auto sf = [&](u32 i, bool &ok) -> u64 {
-        ok = C.scr_key[i] == tc;
-        return ok ? (u64)(C.flog_state[C.scr_row[i]] & ROW_STATE) : 0ull;
+        const u64 k = C.scr_key[i];
+        const u32 s = scr_state[i];
+        ok = k == tc;
+        return (u64)s;
       };
       bool exact2;
-      ts = (u32)radix_select<BLOCK>(sh, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
+      ts = (u32)radix_select<BLOCK, 8, DB>(sh, hist, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
     }
   }
-  if (tid == 0) {
-    sh.n_tok = 0;
-    sh.max_depth = 0;
-  }
+  if (tid == 0) sh.max_depth = 0;
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_SEL);
   int md = 0;
-  for (u32 i0 = 0; i0 < n_keep; i0 += BLOCK) {
-    const u32 i = i0 + tid;
-    bool keep = false;
-    u64 ck = 0;
-    u32 row = 0;
-    if (i < n_keep) {
-      ck = C.scr_key[i];
-      row = C.scr_row[i];
-      keep = ck < tc;
-      if (!keep && ck == tc) keep = (C.flog_state[row] & ROW_STATE) <= ts;
+  u32 n_tok = 0;
+  for (u32 base = 0; base < n_keep; base += TILE) {
+    const u32 i0 = base + (u32)tid * QP;
+    u64 ck[QP];
+    u32 row[QP], s[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_keep ? C.scr_key[i0 + q] : ~0ull;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) row[q] = i0 + q < n_keep ? C.scr_row[i0 + q] : 0u;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) s[q] = i0 + q < n_keep ? scr_state[i0 + q] : 0xFFFFFFFFu;
+    bool keep[QP];
+    u32 cnt = 0;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      keep[q] = i0 + q < n_keep && (ck[q] < tc || (ck[q] == tc && s[q] <= ts));
+      cnt += keep[q] ? 1u : 0u;
     }
-    const u32 p = warp_append(&sh.n_tok, keep);
-    if (keep) {
-      const TokInfo ti = C.flog_info[row];
-      md = max(md, ti.depth);
-      C.tok_state[p] = C.flog_state[row] & ROW_STATE;
-      C.tok_cost[p] = key_cost(ck);
-      C.tok_info[p] = ti;
+    TokInfo ti[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q)
+      if (keep[q]) ti[q] = C.flog_info[row[q]];
+    u32 total;
+    u32 p = n_tok + block_excl_scan<BLOCK>(cnt, total, sh.scan);
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      if (!keep[q]) continue;
+      md = max(md, ti[q].depth);
+      C.tok_state[p] = s[q];
+      C.tok_cost[p] = key_cost(ck[q]);
+      C.tok_info[p] = ti[q];
+      ++p;
     }
+    n_tok += total;
   }
   atomicMax(&sh.max_depth, md);
   __syncthreads();
   if (tid == 0) {
     C.cs->max_depth = sh.max_depth;
-    C.cs->info.num_active = (int)sh.n_tok;
+    C.cs->info.num_active = (int)n_tok;
     const TokInfo bti = C.flog_info[bi];
     if (P.silence_ilabel > 0 && bti.last_il == P.silence_ilabel)
       C.cs->info.trailing_silence += 1;
@@ -978,11 +1163,16 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   u32 e = C.cs->epoch + 1;
   if ((e & 0x7FFFFFFFu) == 0) e = 0x100; // 31-bit key epochs (wrap also wipes below)
   if ((e & 0xFFu) == 0) {
-    for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) {
-      C.table[i].key = 0;
-      C.table[i].ck = 0;
-      C.table[i].g = 0;
-      C.table[i].info = 0;
+    if (F::hashed) {
+      for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) {
+        C.table[i].key = 0;
+        C.table[i].ck = 0;
+        C.table[i].g = 0;
+        C.table[i].info = 0;
+      }
+    } else {
+      uint4 *v = reinterpret_cast<uint4 *>(C.vals);
+      for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) v[i] = make_uint4(0, 0, 0, 0);
     }
     e += 1;
   }
@@ -1068,12 +1258,10 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
   next_epoch<BLOCK>(P, C, sh);
   if (threadIdx.x == 0) {
     const u32 d = (u32)P.start;
-    const u32 slot = home_slot<F::hashed>(P, d);
-    u64 key = 0, vck;
-    u32 fl, vg, vinfo;
-    if (F::hashed) ld_cg_head(&C.table[slot], key, fl);
-    ld_cg_value(&C.table[slot], vck, vg, vinfo);
-    relax(P, C, sh, d, cost_key(0.0), 0xFFFFFFFFu, C.etag << TAG_SHIFT, 0u, slot, key, vck, vg, vinfo);
+    const bool on1[1] = {true};
+    const u32 d1[1] = {d}, g1[1] = {0xFFFFFFFFu}, i1[1] = {C.etag << TAG_SHIFT};
+    const u64 c1[1] = {cost_key(0.0)};
+    relax_batch<1>(P, C, sh, on1, d1, c1, g1, i1, 0u);
     // the start entry's slot is app_list[0]; its row 0 has no provenance
     TokInfo t;
     t.bp = -1;
@@ -1084,7 +1272,7 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     C.flog_state[0] = d | ROW_EPS; // the closure reads the start state's epsilon range
     C.flog_ck[0] = cost_key(0.0);
     C.flog_info[0] = t;
-    C.table[s0].flog = 0;
+    *row_at(C, s0) = 0;
     sh.flog_n = 1;
     sh.min_ck = cost_key(0.0);
   }
@@ -1122,7 +1310,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   next_epoch<BLOCK>(P, C, sh);
-  expand<BLOCK, TPT, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u);
+  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u);
   __syncthreads();
   PROF_MARK(sh, PF_EMIT_X);
   if (sh.error) return;
@@ -1314,7 +1502,8 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
 // in-flight loads.
 template <int BLOCK, typename F, typename S>
 __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh_row,
-                              u32 *sh_ctx) {
+                              u32 *sh_ctx, u32 *t_a0 = nullptr, u32 *t_pref = nullptr,
+                              double *t_cost = nullptr) {
   const int slot = P.slots[b];
   const int h = P.chans[slot].info.context;
   __syncthreads(); // the previous channel of this CTA is done with C
@@ -1324,14 +1513,16 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.slot = slot;
     C.cs = &P.chans[slot];
     const size_t s = (size_t)slot;
-    C.table = P.table + s * P.table_cap;
+    C.table = P.table ? P.table + s * P.table_cap : nullptr;
+    C.vals = P.vals ? P.vals + 2 * s * P.table_cap : nullptr;
+    C.app_old = P.app_old ? P.app_old + s * P.tok_cap : nullptr;
     C.tok_state = P.tok_state + s * P.tok_cap;
     C.tok_cost = P.tok_cost + s * P.tok_cap;
     C.tok_info = P.tok_info + s * P.tok_cap;
     C.flog_state = P.flog_state + s * P.flog_cap;
     C.flog_ck = P.flog_ck + s * P.flog_cap;
     C.flog_info = P.flog_info + s * P.flog_cap;
-    C.app_list = P.app_list + s * P.table_cap;
+    C.app_list = P.app_list + s * P.tok_cap;
     C.scr_key = P.scr_key + s * P.flog_cap;
     C.scr_row = P.scr_row + s * P.flog_cap;
     C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
@@ -1349,6 +1540,9 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.ctx_words = 0;
     C.ctx_list = nullptr;
     C.ctx_bits = nullptr;
+    C.t_a0 = t_a0;
+    C.t_pref = t_pref;
+    C.t_cost = t_cost;
   }
   __syncthreads();
   if (h >= 0 && h < P.num_ctxs) {
@@ -1383,17 +1577,23 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
 // Persistent over channels: CTA i decodes batch entries i, i + grid, ... one
 // after the other (the host sizes the grid so every CTA gets the same count).
 template <int BLOCK, typename F, typename S>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK)
+#ifndef AB_MINB
+#define AB_MINB 4
+#endif
+__global__ void __launch_bounds__(BLOCK, AB_MINB)
     decode_kernel(const __grid_constant__ DecodeParams P) {
-  constexpr int TPT = BLOCK <= 128 ? 2 : 1;
+  constexpr int TPT = 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
   __shared__ Chan<F, S> C;
+  __shared__ double tile_cost[BLOCK * EXP_Q];
+  __shared__ u32 tile_a0[BLOCK * EXP_Q];
+  __shared__ u32 tile_pref[BLOCK * EXP_Q + 1];
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
   for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
-    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx);
+    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost);
     ChanState *cs = C.cs;
     if (threadIdx.x == 0) {
       sh.error = 0;
