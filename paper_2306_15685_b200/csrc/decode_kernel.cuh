@@ -1005,7 +1005,8 @@ template <int BLOCK, typename F, typename S>
 __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   constexpr int QP = PRUNE_Q;
   constexpr u32 TILE = BLOCK * QP;
-  constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : 10; // histogram lives in the expansion tile
+  // the digit histogram lives in the expansion tile (BLOCK * EXP_Q words)
+  constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : (BLOCK * EXP_Q >= 1024) ? 10 : (BLOCK * EXP_Q >= 512) ? 9 : 8;
   const int tid = threadIdx.x;
   const u32 n_rows = sh.flog_n;
   const u64 best_ck = sh.min_ck;
