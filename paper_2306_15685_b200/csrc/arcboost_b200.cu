@@ -93,7 +93,8 @@ struct ab_decoder {
   TokInfo *tok_info = nullptr;
   u32 *flog_state = nullptr;
   u64 *flog_ck = nullptr;
-  TokInfo *flog_info = nullptr;
+  uint2 *flog_aux = nullptr;
+  TokInfo *tok_info_alt = nullptr;
   u32 *app_list = nullptr;
   u64 *scr_key = nullptr;
   u32 *scr_row = nullptr;
@@ -150,7 +151,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
                                const double *final_costs, ab_graph **out) {
   *out = nullptr;
   if (num_states < 1) return fail(AB_ERR_INVALID, "graph must have at least one state");
-  if (num_arcs < 0 || num_arcs >= (int64_t)0xFFFFFFFFll)
+  if (num_arcs < 0 || num_arcs >= (int64_t)G_MASK) // arc ids carry a flag in bit 31
     return fail(AB_ERR_INVALID, "num_arcs %lld out of range", (long long)num_arcs);
   if (num_states > (int32_t)ROW_STATE)
     return fail(AB_ERR_INVALID, "too many states (max %u)", ROW_STATE);
@@ -225,21 +226,23 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
       meta[a] = make_int2(olabels[a], ilabels[a] | (dst_eps ? (int)META_DEST_EPS : 0));
       if (ilabels[a] != 0) {
+        const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
         if (f16) {
-          EArc16 r{(u32)next_states[a], (u32)a, (float)weights[a],
+          EArc16 r{(u32)next_states[a], ga, (float)weights[a],
                    (u32)ilabels[a] | ((u32)olabels[a] << 16)};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         } else {
-          EArc24 r{(u32)next_states[a], (u32)a, (u32)ilabels[a], (u32)olabels[a], weights[a]};
+          EArc24 r{(u32)next_states[a], ga, (u32)ilabels[a], (u32)olabels[a], weights[a]};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         }
         pe++;
       } else {
+        const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
         if (f16) {
-          XArc16 r{(u32)next_states[a], (u32)a, (float)weights[a], (u32)olabels[a]};
+          XArc16 r{(u32)next_states[a], ga, (float)weights[a], (u32)olabels[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         } else {
-          XArc24 r{(u32)next_states[a], (u32)a, (u32)olabels[a], 0u, weights[a]};
+          XArc24 r{(u32)next_states[a], ga, (u32)olabels[a], 0u, weights[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         }
         px++;
@@ -507,7 +510,8 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
       dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
-      dmalloc(&d->flog_info, C * d->flog_cap, acc) ||
+      dmalloc(&d->flog_aux, C * d->flog_cap, acc) ||
+      dmalloc(&d->tok_info_alt, C * d->tok_cap, acc) ||
       dmalloc(&d->app_list, C * d->tok_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
@@ -548,7 +552,7 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->vals,      d->app_old, d->tok_state, d->tok_cost, d->tok_info,
-                  d->flog_state, d->flog_ck,  d->flog_info, d->app_list,
+                  d->flog_state, d->flog_ck,  d->flog_aux, d->tok_info_alt, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
@@ -811,7 +815,8 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.tok_cap = d->tok_cap;
   P.flog_state = d->flog_state;
   P.flog_ck = d->flog_ck;
-  P.flog_info = d->flog_info;
+  P.flog_aux = d->flog_aux;
+  P.tok_info_alt = d->tok_info_alt;
   P.flog_cap = d->flog_cap;
   P.app_list = d->app_list;
   P.scr_key = d->scr_key;

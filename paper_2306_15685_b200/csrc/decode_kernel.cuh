@@ -33,10 +33,18 @@ typedef unsigned long long u64;
 typedef uint32_t u32;
 
 constexpr u64 KEY_EPOCH_MASK = 0x7FFFFFFF00000000ull;
-// value.info = round(6) | boosted(1) | epoch tag(8) | src(17)
+// value.info = round(6) | boosted(1) | olabel != 0 (1) | epoch tag(7) | src(17)
 constexpr int ROUND_SHIFT = 26;
 constexpr int BOOST_SHIFT = 25;
+constexpr int HASOL_SHIFT = 24;
 constexpr int TAG_SHIFT = 17;
+constexpr u32 TAG_MASK = 0x7Fu;
+// arc records carry the destination's "has epsilon arcs" flag in bit 31 of the
+// arc id; every candidate into one destination has the same flag, so the
+// (cost, arc id) order inside a slot is unchanged (graphs have < 2^31 arcs)
+constexpr u32 G_DEST_EPS = 0x80000000u;
+constexpr u32 G_MASK = 0x7FFFFFFFu;
+constexpr u32 G_START = 0xFFFFFFFFu; // frontier row of the utterance-start token
 constexpr u32 SRC_BITS = 17;
 constexpr u32 SRC_MASK = (1u << SRC_BITS) - 1;
 constexpr u32 MAX_TOKENS = 1u << SRC_BITS;      // distinct tokens per channel-frame
@@ -203,8 +211,9 @@ struct DecodeParams {
   u32 tok_cap;
   u32 *flog_state;
   u64 *flog_ck;
-  TokInfo *flog_info;
+  uint2 *flog_aux; // {winner info, arc id | G_DEST_EPS} per frontier row
   u32 flog_cap;
+  TokInfo *tok_info_alt;
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_row;
@@ -423,6 +432,8 @@ struct Shared {
   u32 reds[32];
   int redi[32];
   u32 hist[256];
+  u32 round_base[MAX_EPS_ROUNDS + 2]; // first frontier row of each round of the frame
+  int best_last_il;
 #ifdef AB_PROFILE
   unsigned long long prof[PF_N];
   long long prof_t;
@@ -442,7 +453,8 @@ template <typename F, typename S> struct Chan {
   TokInfo *tok_info;
   u32 *flog_state;
   u64 *flog_ck;
-  TokInfo *flog_info;
+  uint2 *flog_aux;
+  TokInfo *tok_info_alt;
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_row;
@@ -513,21 +525,33 @@ template <typename F, typename S> __device__ __forceinline__ u32 *row_at(const C
 // applied), 1 (new entry) or 2 (improved an entry of an earlier round).
 __device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 round, u32 etag, u64 vck, u32 vg,
                                              u32 vinfo) {
-  const bool valid = ((vinfo >> TAG_SHIFT) & 0xFFu) == etag;
+  const bool valid = ((vinfo >> TAG_SHIFT) & TAG_MASK) == etag;
   const u32 cround = vinfo >> ROUND_SHIFT;
   return !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
 }
 __device__ __forceinline__ int applied_code(u32 round, u32 etag, u32 old_info) {
-  if (((old_info >> TAG_SHIFT) & 0xFFu) != etag) return 1;
+  if (((old_info >> TAG_SHIFT) & TAG_MASK) != etag) return 1;
   return (old_info >> ROUND_SHIFT) < round ? 2 : 0;
 }
+// Emission records the reference appends (decoder.py:385-389, 289-295) are
+// counted exactly without reading labels at snapshot time: every successful
+// CAS adds its own "olabel != 0" bit and, when it displaces a winner of the
+// same round, subtracts that winner's bit; the sum telescopes to the final
+// winners of each round.
+__device__ __forceinline__ int rec_delta(int code, u32 info, u32 old_info) {
+  return (int)((info >> HASOL_SHIFT) & 1u) - (code == 0 ? (int)((old_info >> HASOL_SHIFT) & 1u) : 0);
+}
 __device__ __forceinline__ int relax_value(u64 *e, u64 ck, u32 g, u32 info, u32 round, u32 etag,
-                                          u64 vck, u32 vg, u32 vinfo, u32 &old_g) {
+                                          u64 vck, u32 vg, u32 vinfo, u32 &old_g, int &rec) {
   while (true) {
     if (!value_better(ck, g, round, etag, vck, vg, vinfo)) return 0;
     const u32 old_info = vinfo;
     old_g = vg;
-    if (cas_value(e, vck, vg, vinfo, ck, g, info)) return applied_code(round, etag, old_info);
+    if (cas_value(e, vck, vg, vinfo, ck, g, info)) {
+      const int code = applied_code(round, etag, old_info);
+      rec += rec_delta(code, info, old_info);
+      return code;
+    }
   }
 }
 
@@ -572,7 +596,9 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     ld_cg_value(val_at(C, slot), vck, vg, vinfo);
   }
   u32 old_g = 0;
-  const int r = relax_value(val_at(C, slot), ck, g, info, round, C.etag, vck, vg, vinfo, old_g);
+  int rec = 0;
+  const int r = relax_value(val_at(C, slot), ck, g, info, round, C.etag, vck, vg, vinfo, old_g, rec);
+  if (rec) atomicAdd(&sh.rec_logical, (unsigned long long)(long long)rec);
   if (r) record_applied(P, C, sh, slot, r, old_g);
 }
 
@@ -585,7 +611,7 @@ template <int U, typename F, typename S>
 __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
                                             const bool (&on)[U], const u32 (&d)[U],
                                             const u64 (&ck)[U], const u32 (&g)[U],
-                                            const u32 (&info)[U], u32 round) {
+                                            const u32 (&info)[U], u32 round, int &rec) {
   const u32 etag = C.etag;
   const u64 ep = (u64)C.epoch << 32;
   u32 slot[U];
@@ -642,9 +668,10 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     if (!want[u]) continue;
     if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u])) {
       code[u] = applied_code(round, etag, vinfo[u]);
+      rec += rec_delta(code[u], info[u], vinfo[u]);
     } else {
       code[u] = relax_value(val_at(C, slot[u]), ck[u], g[u], info[u], round, etag, r0[u], (u32)r1[u],
-                            (u32)(r1[u] >> 32), vg[u]);
+                            (u32)(r1[u] >> 32), vg[u], rec);
     }
     n_app += code[u] != 0;
     n_new += code[u] == 1;
@@ -684,6 +711,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
   const u32 info_hi = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT);
   u32 arcs_seen = 0;
+  int rec = 0;
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
     u32 st[Q], a0[Q], cnt[Q];
@@ -770,20 +798,22 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         info[u] = 0;
         if (on[u]) {
           // _effective_weights (decoder.py:234-240): boost fused into the cost add
-          const bool bst = is_boosted(C, g[u], ol[u]);
+          const bool bst = is_boosted(C, g[u] & G_MASK, ol[u]);
           const double we = bst ? w[u] + C.discount : w[u];
           double cand;
           if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
           else cand = cj[u] + we;                                    // decoder.py:268
           ck[u] = cost_key(cand);
-          info[u] = info_hi | (bst ? (1u << BOOST_SHIFT) : 0u) | (src[u] & SRC_MASK);
+          info[u] = info_hi | (bst ? (1u << BOOST_SHIFT) : 0u) | (ol[u] ? (1u << HASOL_SHIFT) : 0u) |
+                    (src[u] & SRC_MASK);
         }
       }
-      relax_batch<U>(P, C, sh, on, d, ck, g, info, round);
+      relax_batch<U>(P, C, sh, on, d, ck, g, info, round, rec);
       k += U;
     }
     __syncthreads();
   }
+  if (rec) atomicAdd(&sh.rec_logical, (unsigned long long)(long long)rec);
   if (tid == 0) {
     sh.n_cand += arcs_seen;
     sh.cnt_tok += n_in;
@@ -792,20 +822,21 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   }
 }
 
-// Snapshot of the slots applied in one phase into the frontier log: resolves
-// the winner's provenance, appends emission records for olabel != 0
-// (decoder.py:385-389, 289-295), points the slot at its row and retires the
-// row of an improved slot's previous application.  SNAP rows in flight per
-// thread; every load step is issued for all of them first.
+// Snapshot of the slots applied in one phase into the frontier log: one row
+// per application {state | flags, cost key, (info, arc id)} of the winner;
+// the slot is pointed at its row and the row of an improved slot's previous
+// application is retired.  Provenance (back-pointer, emission records, hits,
+// last ilabel) is not resolved here: prune resolves it for the survivors only
+// by walking the rows' source links (resolve_row).
 template <int BLOCK, typename F, typename S>
-__device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 round, const TokInfo *src_info,
-                         u32 n_app, u32 row_base) {
+__device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 round, u32 n_app,
+                         u32 row_base) {
   if (row_base + n_app > P.flog_cap) {
     if (threadIdx.x == 0) set_error(sh, E_CAP);
     return;
   }
+  if (threadIdx.x == 0) sh.round_base[round] = row_base;
   u64 mck = ~0ull;
-  u32 n_rec_logical = 0;
   for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * SNAP) {
     u32 slot[SNAP], d[SNAP], g[SNAP], info[SNAP], oldrow[SNAP] = {};
     u64 ck[SNAP];
@@ -838,53 +869,93 @@ __device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
       }
       ld_cg_value(val_at(C, slot[u]), ck[u], g[u], info[u]);
     }
-    TokInfo si[SNAP];
-    int2 meta[SNAP];
 #pragma unroll
     for (int u = 0; u < SNAP; ++u) {
       if (!on[u]) continue;
-      si[u] = src_info[info[u] & SRC_MASK];
-      if (P.arc_meta32) {
-        const u32 m = __ldg(&P.arc_meta32[g[u]]);
-        meta[u] = make_int2((int)(m & 0xFFFFu), (int)((m >> 16) & 0x7FFFu) | (int)(m & META_DEST_EPS));
-      } else {
-        meta[u] = __ldg(&P.arc_meta[g[u]]);
-      }
-    }
-    u32 nrec = 0;
-#pragma unroll
-    for (int u = 0; u < SNAP; ++u) nrec += (on[u] && meta[u].x != 0) ? 1u : 0u;
-    u32 r = nrec ? atomicAdd(&sh.rec_n, nrec) : 0u;
-    n_rec_logical += nrec;
-#pragma unroll
-    for (int u = 0; u < SNAP; ++u) {
-      if (!on[u]) continue;
-      TokInfo ni;
-      ni.bp = si[u].bp;
-      ni.depth = si[u].depth;
-      ni.hits = si[u].hits + ((info[u] >> BOOST_SHIFT) & 1);
-      ni.last_il = round == 0 ? (int)((u32)meta[u].y & ~META_DEST_EPS) : si[u].last_il;
-      if (meta[u].x != 0) {
-        if (r < P.arena_cap) {
-          C.arena[r] = make_int2(meta[u].x, si[u].bp);
-          ni.bp = (int)r;
-          ni.depth = si[u].depth + 1;
-        } else {
-          set_error(sh, E_CAP);
-        }
-        ++r;
-      }
       const u32 row = row_base + i0 + u * BLOCK;
-      C.flog_state[row] = d[u] | (((u32)meta[u].y & META_DEST_EPS) ? ROW_EPS : 0u);
+      C.flog_state[row] = d[u] | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
       C.flog_ck[row] = ck[u];
-      C.flog_info[row] = ni;
+      C.flog_aux[row] = make_uint2(info[u], g[u]);
       *row_at(C, slot[u]) = row;
       if (imp[u]) atomicOr(&C.flog_state[oldrow[u]], ROW_DEAD);
       mck = min(mck, ck[u]);
     }
   }
-  if (n_rec_logical) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec_logical);
   if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
+}
+
+// Labels of a global arc id (olabel, ilabel).
+__device__ __forceinline__ void arc_labels(const DecodeParams &P, u32 g, u32 &ol, u32 &il) {
+  if (P.arc_meta32) {
+    const u32 m = __ldg(&P.arc_meta32[g]);
+    ol = m & 0xFFFFu;
+    il = (m >> 16) & 0x7FFFu;
+  } else {
+    const int2 m = __ldg(&P.arc_meta[g]);
+    ol = (u32)m.x;
+    il = (u32)m.y & ~META_DEST_EPS;
+  }
+}
+
+// Provenance of a surviving frontier row (decoder.py:385-393, 289-295): walks
+// the row's source links back to the token of the previous frame (or the
+// utterance start), then appends the emission records of the path's arcs with
+// olabel != 0, oldest first, and returns the token's provenance.  Source of a
+// row of round r >= 1: row round_base[r - 1] + src; of round 0: token src of
+// the previous frame's list (prev_tok).
+template <typename F, typename S>
+__device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 row,
+                               const TokInfo *prev_tok) {
+  TokInfo base;
+  base.bp = -1;
+  base.depth = 0;
+  base.hits = 0;
+  base.last_il = 0;
+  int hits = 0;
+  u32 nrec = 0, il = 0;
+  u32 cur = row;
+  while (true) {
+    const uint2 ax = C.flog_aux[cur];
+    if (ax.y == G_START) break;
+    hits += (int)((ax.x >> BOOST_SHIFT) & 1u);
+    nrec += (ax.x >> HASOL_SHIFT) & 1u;
+    const u32 round = ax.x >> ROUND_SHIFT, src = ax.x & SRC_MASK;
+    if (round == 0) {
+      u32 ol;
+      arc_labels(P, ax.y & G_MASK, ol, il);
+      base = prev_tok[src];
+      break;
+    }
+    cur = sh.round_base[round - 1] + src;
+  }
+  TokInfo t;
+  t.hits = base.hits + hits;
+  t.depth = base.depth + (int)nrec;
+  t.last_il = (int)il;
+  t.bp = base.bp;
+  if (nrec) {
+    const u32 r0 = atomicAdd(&sh.rec_n, nrec);
+    if (r0 + nrec > P.arena_cap) {
+      set_error(sh, E_CAP);
+      return t;
+    }
+    t.bp = (int)(r0 + nrec - 1);
+    u32 k = nrec;
+    cur = row;
+    while (k) {
+      const uint2 ax = C.flog_aux[cur];
+      if ((ax.x >> HASOL_SHIFT) & 1u) {
+        u32 ol, il2;
+        arc_labels(P, ax.y & G_MASK, ol, il2);
+        --k;
+        C.arena[r0 + k] = make_int2((int)ol, k ? (int)(r0 + k - 1) : base.bp);
+      }
+      const u32 round = ax.x >> ROUND_SHIFT;
+      if (round == 0) break;
+      cur = sh.round_base[round - 1] + (ax.x & SRC_MASK);
+    }
+  }
+  return t;
 }
 
 // _epsilon_rounds (decoder.py:250-316) starting from frontier rows
@@ -912,7 +983,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     if (sh.error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
     const u32 row_base = sh.flog_n;
-    snapshot<BLOCK>(P, C, sh, (u32)rounds, C.flog_info + fbase, n_app, row_base);
+    snapshot<BLOCK>(P, C, sh, (u32)rounds, n_app, row_base);
     __syncthreads();
     PROF_MARK(sh, PF_EPS_S);
     if (threadIdx.x == 0) sh.flog_n = row_base + n_app;
@@ -920,6 +991,35 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     if (sh.error) return;
     fbase = row_base;
     nf = n_app;
+  }
+  __syncthreads();
+}
+
+// Provenance of a new token list (token i comes from frontier row rows[i]):
+// resolve_row per token into tok_info_alt (the previous list's provenance is
+// still read through tok_info), then copied over tok_info.
+template <int BLOCK, typename F, typename S>
+__device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 n_tok,
+                              const u32 *rows, int best_row) {
+  if (threadIdx.x == 0) {
+    sh.max_depth = 0;
+    sh.best_last_il = 0;
+  }
+  __syncthreads();
+  int md = 0;
+  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) {
+    const u32 r = rows[i];
+    const TokInfo t = resolve_row(P, C, sh, r, C.tok_info);
+    md = max(md, t.depth);
+    C.tok_info_alt[i] = t;
+    if ((int)r == best_row) sh.best_last_il = t.last_il;
+  }
+  atomicMax(&sh.max_depth, md);
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) C.tok_info[i] = C.tok_info_alt[i];
+  if (threadIdx.x == 0) {
+    C.cs->max_depth = sh.max_depth;
+    C.cs->info.num_active = (int)n_tok;
   }
   __syncthreads();
 }
@@ -1068,10 +1168,8 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       ts = (u32)radix_select<BLOCK, 8, DB>(sh, hist, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
     }
   }
-  if (tid == 0) sh.max_depth = 0;
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_SEL);
-  int md = 0;
   u32 n_tok = 0;
   for (u32 base = 0; base < n_keep; base += TILE) {
     const u32 i0 = base + (u32)tid * QP;
@@ -1090,30 +1188,22 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       keep[q] = i0 + q < n_keep && (ck[q] < tc || (ck[q] == tc && s[q] <= ts));
       cnt += keep[q] ? 1u : 0u;
     }
-    TokInfo ti[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q)
-      if (keep[q]) ti[q] = C.flog_info[row[q]];
     u32 total;
     u32 p = n_tok + block_excl_scan<BLOCK>(cnt, total, sh.scan);
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
       if (!keep[q]) continue;
-      md = max(md, ti[q].depth);
       C.tok_state[p] = s[q];
       C.tok_cost[p] = key_cost(ck[q]);
-      C.tok_info[p] = ti[q];
+      C.scr_row[p] = row[q]; // survivors' rows in token order (p <= the slot just read)
       ++p;
     }
     n_tok += total;
   }
-  atomicMax(&sh.max_depth, md);
   __syncthreads();
+  finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, bi);
   if (tid == 0) {
-    C.cs->max_depth = sh.max_depth;
-    C.cs->info.num_active = (int)n_tok;
-    const TokInfo bti = C.flog_info[bi];
-    if (P.silence_ilabel > 0 && bti.last_il == P.silence_ilabel)
+    if (P.silence_ilabel > 0 && sh.best_last_il == P.silence_ilabel)
       C.cs->info.trailing_silence += 1;
     else
       C.cs->info.trailing_silence = 0;
@@ -1127,33 +1217,22 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
 template <int BLOCK, typename F, typename S>
 __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const u32 n_rows = sh.flog_n;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    sh.n_tok = 0;
-    sh.max_depth = 0;
-  }
-  __syncthreads();
-  int md = 0;
+  u32 n_tok = 0;
   for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
     const u32 i = i0 + threadIdx.x;
     const u32 st = i < n_rows ? C.flog_state[i] : ROW_DEAD;
     const bool live = !(st & ROW_DEAD);
-    const u32 p = warp_append(&sh.n_tok, live);
+    u32 total;
+    const u32 p = n_tok + block_excl_scan<BLOCK>(live ? 1u : 0u, total, sh.scan);
     if (live) {
-      const TokInfo ti = C.flog_info[i];
-      md = max(md, ti.depth);
       C.tok_state[p] = st & ROW_STATE;
       C.tok_cost[p] = key_cost(C.flog_ck[i]);
-      C.tok_info[p] = ti;
+      C.scr_row[p] = i;
     }
-  }
-  atomicMax(&sh.max_depth, md);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    C.cs->info.num_active = (int)sh.n_tok;
-    C.cs->max_depth = sh.max_depth;
+    n_tok += total;
   }
   __syncthreads();
+  finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, -1);
 }
 
 // Moves the channel to a fresh table epoch; the table is wiped when the
@@ -1163,7 +1242,7 @@ template <int BLOCK, typename F, typename S>
 __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   u32 e = C.cs->epoch + 1;
   if ((e & 0x7FFFFFFFu) == 0) e = 0x100; // 31-bit key epochs (wrap also wipes below)
-  if ((e & 0xFFu) == 0) {
+  if ((e & TAG_MASK) == 0) {
     if (F::hashed) {
       for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) {
         C.table[i].key = 0;
@@ -1181,7 +1260,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   if (threadIdx.x == 0) {
     C.cs->epoch = e;
     C.epoch = e;
-    C.etag = e & 0xFFu;
+    C.etag = e & TAG_MASK;
     sh.n_new = 0;
     sh.n_app = 0;
     sh.n_cand = 0;
@@ -1262,17 +1341,14 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     const bool on1[1] = {true};
     const u32 d1[1] = {d}, g1[1] = {0xFFFFFFFFu}, i1[1] = {C.etag << TAG_SHIFT};
     const u64 c1[1] = {cost_key(0.0)};
-    relax_batch<1>(P, C, sh, on1, d1, c1, g1, i1, 0u);
+    int rec1 = 0;
+    relax_batch<1>(P, C, sh, on1, d1, c1, g1, i1, 0u, rec1);
     // the start entry's slot is app_list[0]; its row 0 has no provenance
-    TokInfo t;
-    t.bp = -1;
-    t.depth = 0;
-    t.hits = 0;
-    t.last_il = 0;
     const u32 s0 = C.app_list[0] & ~APP_IMPROVED;
     C.flog_state[0] = d | ROW_EPS; // the closure reads the start state's epsilon range
     C.flog_ck[0] = cost_key(0.0);
-    C.flog_info[0] = t;
+    C.flog_aux[0] = make_uint2(0u, G_START);
+    sh.round_base[0] = 0;
     *row_at(C, s0) = 0;
     sh.flog_n = 1;
     sh.min_ck = cost_key(0.0);
@@ -1320,7 +1396,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     // no emitting arcs: every token dies (decoder.py:394-398)
     if (threadIdx.x == 0) cs->info.num_active = 0;
   } else {
-    snapshot<BLOCK>(P, C, sh, 0u, C.tok_info, n_app, 0u);
+    snapshot<BLOCK>(P, C, sh, 0u, n_app, 0u);
     __syncthreads();
     PROF_MARK(sh, PF_EMIT_S);
     if (threadIdx.x == 0) sh.flog_n = n_app;
@@ -1522,7 +1598,8 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.tok_info = P.tok_info + s * P.tok_cap;
     C.flog_state = P.flog_state + s * P.flog_cap;
     C.flog_ck = P.flog_ck + s * P.flog_cap;
-    C.flog_info = P.flog_info + s * P.flog_cap;
+    C.flog_aux = P.flog_aux + s * P.flog_cap;
+    C.tok_info_alt = P.tok_info_alt + s * P.tok_cap;
     C.app_list = P.app_list + s * P.tok_cap;
     C.scr_key = P.scr_key + s * P.flog_cap;
     C.scr_row = P.scr_row + s * P.flog_cap;
@@ -1534,7 +1611,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.path_words = P.path_words + s * P.path_cap;
     C.row = sh_row;
     C.epoch = C.cs->epoch;
-    C.etag = C.epoch & 0xFFu;
+    C.etag = C.epoch & TAG_MASK;
     C.ctx_mode = CTX_NONE;
     C.discount = 0.0;
     C.ctx_k = 0;
