@@ -87,7 +87,6 @@ struct ab_decoder {
   ChanState *chans = nullptr;
   Entry *table = nullptr;  // hashed
   u64 *vals = nullptr;     // direct
-  u32 *app_old = nullptr;  // direct
   u32 *tok_state = nullptr;
   double *tok_cost = nullptr;
   TokInfo *tok_info = nullptr;
@@ -491,6 +490,10 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->arena_cap = (u32)(cap.arena_records > 0 ? cap.arena_records
                                              : std::max<uint64_t>(1ull << 19, 8ull * d->flog_cap));
   d->arena_cap = (d->arena_cap + 31) & ~31u;
+  if (d->flog_cap > MAX_ROWS) {
+    delete d;
+    return fail(AB_ERR_INVALID, "frontier_rows too large (max %u)", MAX_ROWS);
+  }
   if ((uint64_t)d->arena_cap < 2ull * d->flog_cap) {
     delete d;
     return fail(AB_ERR_INVALID, "arena_records must be at least twice frontier_rows");
@@ -505,14 +508,13 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   const size_t hslots = d->hashed ? C * d->table_cap : 0, dslots = d->hashed ? 0 : C * d->table_cap;
   if (dmalloc(&d->chans, C, acc) || (hslots && dmalloc(&d->table, hslots, acc)) ||
       (dslots && dmalloc(&d->vals, 2 * dslots, acc)) ||
-      (dslots && dmalloc(&d->app_old, C * d->tok_cap, acc)) ||
       dmalloc(&d->tok_state, C * d->tok_cap, acc) || dmalloc(&d->tok_cost, C * d->tok_cap, acc) ||
       dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_aux, C * d->flog_cap, acc) ||
       dmalloc(&d->tok_info_alt, C * d->tok_cap, acc) ||
-      dmalloc(&d->app_list, C * d->tok_cap, acc) ||
+      dmalloc(&d->app_list, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
       dmalloc(&d->arena, 2 * C * d->arena_cap, acc) ||
@@ -551,7 +553,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
 extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
-  void *ptrs[] = {d->chans,     d->table,     d->vals,      d->app_old, d->tok_state, d->tok_cost, d->tok_info,
+  void *ptrs[] = {d->chans,     d->table,     d->vals, d->tok_state, d->tok_cost, d->tok_info,
                   d->flog_state, d->flog_ck,  d->flog_aux, d->tok_info_alt, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
@@ -802,7 +804,6 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.chans = d->chans;
   P.table = d->table;
   P.vals = d->vals;
-  P.app_old = d->app_old;
   P.table_cap = d->table_cap;
   P.table_mask = d->table_cap - 1;
   int lg = 0;

@@ -17,10 +17,11 @@
 //   emitting (c + w_eff) + score[il-1], epsilon c + w_eff, final c + final[s].
 //
 // Per-frame data flow (all per channel):
-//   token list --expand(emitting CSR)--> token table (128-bit CAS minimum)
-//   applied slots --snapshot--> frontier log rows (state, cost key, provenance)
-//   frontier rows --expand(epsilon CSR)--> table ... (Jacobi rounds)
+//   token list --expand(emitting CSR)--> token table (128-bit CAS minimum);
+//       every installed candidate owns a frontier row written before its CAS
+//   rows of round r --expand(epsilon CSR)--> table ... (Jacobi rounds)
 //   live frontier rows --prune (beam, exact top-k radix select)--> token list
+//   survivors --resolve (source links)--> provenance + emission records
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -33,28 +34,30 @@ typedef unsigned long long u64;
 typedef uint32_t u32;
 
 constexpr u64 KEY_EPOCH_MASK = 0x7FFFFFFF00000000ull;
-// value.info = round(6) | boosted(1) | olabel != 0 (1) | epoch tag(7) | src(17)
+// value.info = round(6) | epoch tag(7) | frontier row of the winner(19)
 constexpr int ROUND_SHIFT = 26;
-constexpr int BOOST_SHIFT = 25;
-constexpr int HASOL_SHIFT = 24;
-constexpr int TAG_SHIFT = 17;
+constexpr int TAG_SHIFT = 19;
 constexpr u32 TAG_MASK = 0x7Fu;
+constexpr u32 VROW_MASK = (1u << TAG_SHIFT) - 1;
+constexpr u32 MAX_ROWS = 1u << TAG_SHIFT;  // frontier rows per channel-frame
+constexpr u32 KILL_DISP = 0x80000000u;     // kill-queue entry: the row was displaced
 // arc records carry the destination's "has epsilon arcs" flag in bit 31 of the
 // arc id; every candidate into one destination has the same flag, so the
 // (cost, arc id) order inside a slot is unchanged (graphs have < 2^31 arcs)
 constexpr u32 G_DEST_EPS = 0x80000000u;
 constexpr u32 G_MASK = 0x7FFFFFFFu;
 constexpr u32 G_START = 0xFFFFFFFFu; // frontier row of the utterance-start token
-constexpr u32 SRC_BITS = 17;
-constexpr u32 SRC_MASK = (1u << SRC_BITS) - 1;
-constexpr u32 MAX_TOKENS = 1u << SRC_BITS;      // distinct tokens per channel-frame
+constexpr u32 MAX_TOKENS = 1u << 17;            // distinct tokens per channel-frame
 constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per channel
 constexpr int MAX_EPS_ROUNDS = 63;
-constexpr u32 ROW_DEAD = 0x80000000u;       // frontier-log row superseded later in the frame
-constexpr u32 ROW_EPS = 0x40000000u;        // row's state has epsilon out-arcs
-constexpr u32 ROW_STATE = 0x3FFFFFFFu;
+// frontier row word: state | flags
+constexpr u32 ROW_DEAD = 0x80000000u;  // superseded by a later round (an application, not a token)
+constexpr u32 ROW_DISP = 0x40000000u;  // displaced in its own round (not an application)
+constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
+constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
+constexpr u32 ROW_HASOL = 0x08000000u; // the winning arc has an output label (an emission record)
+constexpr u32 ROW_STATE = 0x07FFFFFFu;
 constexpr u32 META_DEST_EPS = 0x80000000u;  // arc_meta.y flag: the arc's destination has epsilon arcs
-constexpr u32 APP_IMPROVED = 0x80000000u;   // applied-list flag: slot existed this frame
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
 #ifndef AB_EXP_Q
@@ -63,12 +66,8 @@ constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L
 #ifndef AB_EXP_U
 #define AB_EXP_U 1
 #endif
-#ifndef AB_SNAP
-#define AB_SNAP 1
-#endif
 constexpr int EXP_Q = AB_EXP_Q; // inputs per thread per expansion tile (CSR range loads in flight)
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
-constexpr int SNAP = AB_SNAP;   // applied slots per thread in flight (snapshot)
 #ifndef AB_PRUNE_Q
 #define AB_PRUNE_Q 2
 #endif
@@ -202,7 +201,6 @@ struct DecodeParams {
   ChanState *chans;
   Entry *table;   // hashed
   u64 *vals;      // direct: [channel][table_cap][2]
-  u32 *app_old;   // direct: [channel][tok_cap] row superseded by an improving application
   u32 table_cap, table_mask, hash_shift;
   int hashed;
   u32 *tok_state;
@@ -432,7 +430,8 @@ struct Shared {
   u32 reds[32];
   int redi[32];
   u32 hist[256];
-  u32 round_base[MAX_EPS_ROUNDS + 2]; // first frontier row of each round of the frame
+  u32 n_kill;   // kill queue length of the current round
+  u32 emit_end; // rows below come from the emitting pass (their source is a token)
   int best_last_il;
 #ifdef AB_PROFILE
   unsigned long long prof[PF_N];
@@ -447,7 +446,6 @@ template <typename F, typename S> struct Chan {
   ChanState *cs;
   Entry *table;
   u64 *vals;
-  u32 *app_old;
   u32 *tok_state;
   double *tok_cost;
   TokInfo *tok_info;
@@ -508,73 +506,87 @@ __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.
 template <bool H> __device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
   return H ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
 }
-// value / frontier-row word of a slot (direct tables: the value's arc field)
+// value of a slot
 template <typename F, typename S> __device__ __forceinline__ u64 *val_at(const Chan<F, S> &C, u32 slot) {
   return F::hashed ? &C.table[slot].ck : C.vals + 2 * (size_t)slot;
 }
-template <typename F, typename S> __device__ __forceinline__ u32 *row_at(const Chan<F, S> &C, u32 slot) {
-  return F::hashed ? &C.table[slot].flog : reinterpret_cast<u32 *>(C.vals + 2 * (size_t)slot + 1);
-}
 
-// Value half of a relaxation (decoder.py:213-220 emitting, 277-308 epsilon):
-// CAS-128 minimum with the phase rule
-//   empty (stale tag)           -> take it: a new table entry
+// Relaxation (decoder.py:213-220 emitting, 277-308 epsilon) is a CAS-128
+// minimum on the slot's value with the phase rule
+//   empty (stale tag)           -> take it: a new token of this frame
 //   value from an earlier round -> replace iff strictly cheaper (cost only)
 //   value from this round       -> replace iff (cost, arc) is smaller
-// starting from the value already loaded in (vck, vg, vinfo).  Returns 0 (not
-// applied), 1 (new entry) or 2 (improved an entry of an earlier round).
+// A candidate that passes the check against the loaded value first writes its
+// frontier row {state | flags, cost key, (source, arc id)} at a freshly
+// reserved index, then installs (cost, arc, round | tag | row) by CAS.  The
+// value therefore always names the row of the slot's current winner; a CAS
+// that replaces a winner of the same round queues that row as displaced
+// (not an application), one that replaces an earlier round's winner queues it
+// as superseded (an application, no longer a token).  The queue is applied
+// after the round's barrier, so the rows of a round are final without a
+// second pass over the table.
 __device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 round, u32 etag, u64 vck, u32 vg,
                                              u32 vinfo) {
   const bool valid = ((vinfo >> TAG_SHIFT) & TAG_MASK) == etag;
   const u32 cround = vinfo >> ROUND_SHIFT;
   return !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
 }
-__device__ __forceinline__ int applied_code(u32 round, u32 etag, u32 old_info) {
-  if (((old_info >> TAG_SHIFT) & TAG_MASK) != etag) return 1;
-  return (old_info >> ROUND_SHIFT) < round ? 2 : 0;
+
+struct RelaxAcc {
+  u64 min_ck;  // cheapest installed candidate
+  u32 n_new;   // new tokens (capacity check)
+  u32 n_app;   // applications (decoder.py:285-287 stop rule)
+};
+
+// Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
+template <typename F, typename S>
+__device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 v) {
+  const u32 k = atomicAdd(&sh.n_kill, 1u);
+  if (k < P.flog_cap) C.app_list[k] = v;
+  else set_error(sh, E_CAP);
 }
-// Emission records the reference appends (decoder.py:385-389, 289-295) are
-// counted exactly without reading labels at snapshot time: every successful
-// CAS adds its own "olabel != 0" bit and, when it displaces a winner of the
-// same round, subtracts that winner's bit; the sum telescopes to the final
-// winners of each round.
-__device__ __forceinline__ int rec_delta(int code, u32 info, u32 old_info) {
-  return (int)((info >> HASOL_SHIFT) & 1u) - (code == 0 ? (int)((old_info >> HASOL_SHIFT) & 1u) : 0);
-}
-__device__ __forceinline__ int relax_value(u64 *e, u64 ck, u32 g, u32 info, u32 round, u32 etag,
-                                          u64 vck, u32 vg, u32 vinfo, u32 &old_g, int &rec) {
-  while (true) {
-    if (!value_better(ck, g, round, etag, vck, vg, vinfo)) return 0;
-    const u32 old_info = vinfo;
-    old_g = vg;
-    if (cas_value(e, vck, vg, vinfo, ck, g, info)) {
-      const int code = applied_code(round, etag, old_info);
-      rec += rec_delta(code, info, old_info);
-      return code;
-    }
+
+// Outcome of a successful CAS that replaced old_info.
+template <typename F, typename S>
+__device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
+                                          u32 round, u32 etag, u32 old_info, u64 ck) {
+  acc.min_ck = min(acc.min_ck, ck);
+  if (((old_info >> TAG_SHIFT) & TAG_MASK) != etag) {
+    acc.n_new++;
+    acc.n_app++;
+  } else if ((old_info >> ROUND_SHIFT) < round) {
+    acc.n_app++;
+    queue_kill(P, C, sh, old_info & VROW_MASK);
+  } else {
+    queue_kill(P, C, sh, (old_info & VROW_MASK) | KILL_DISP);
   }
 }
 
-// Records one application in the applied-slot list.  Direct tables keep the
-// frontier row of a slot's latest application in the value's arc field
-// (snapshot writes it; values of earlier rounds are compared by cost only), so
-// an improvement carries the row it supersedes (`old_g`) in app_old.
+// CAS retry loop after a lost race; the candidate's row is `row`.  A
+// candidate that stops being better marks its own row displaced.
 template <typename F, typename S>
-__device__ __forceinline__ void record_applied(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
-                                               u32 slot, int code, u32 old_g) {
-  if (code == 1 && atomicAdd(&sh.n_new, 1u) + 1u > P.tok_cap) set_error(sh, E_CAP);
-  const u32 ip = atomicAdd(&sh.n_app, 1u);
-  if (ip < P.tok_cap) {
-    C.app_list[ip] = slot | (code == 2 ? APP_IMPROVED : 0u);
-    if (!F::hashed && code == 2) C.app_old[ip] = old_g;
+__device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
+                            u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row) {
+  const u32 etag = C.etag;
+  while (true) {
+    if (!value_better(ck, g, round, etag, vck, vg, vinfo)) {
+      atomicOr(&C.flog_state[row], ROW_DISP);
+      return;
+    }
+    const u32 old_info = vinfo;
+    if (cas_value(v, vck, vg, vinfo, ck, g, info)) {
+      installed(P, C, sh, acc, round, etag, old_info, ck);
+      return;
+    }
   }
 }
 
 // Sequential relaxation with linear probing (hashed tables: the home slot
 // belongs to another state).  (key, vck, vg, vinfo) = contents of `slot`.
 template <typename F, typename S>
-__device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 d, u64 ck, u32 g,
-                            u32 info, u32 round, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
+__device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
+                                         u32 d, u64 ck, u32 g, u32 src, u32 rflags, u32 round, u32 slot,
+                                         u64 key, u64 vck, u32 vg, u32 vinfo) {
   const u64 ep = (u64)C.epoch << 32;
   u32 probes = 0;
   while (true) {
@@ -595,23 +607,28 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     ld_cg_head(&C.table[slot], key, fl);
     ld_cg_value(val_at(C, slot), vck, vg, vinfo);
   }
-  u32 old_g = 0;
-  int rec = 0;
-  const int r = relax_value(val_at(C, slot), ck, g, info, round, C.etag, vck, vg, vinfo, old_g, rec);
-  if (rec) atomicAdd(&sh.rec_logical, (unsigned long long)(long long)rec);
-  if (r) record_applied(P, C, sh, slot, r, old_g);
+  if (!value_better(ck, g, round, C.etag, vck, vg, vinfo)) return;
+  const u32 row = atomicAdd(&sh.flog_n, 1u);
+  if (row >= P.flog_cap) {
+    set_error(sh, E_CAP);
+    return;
+  }
+  C.flog_state[row] = d | rflags;
+  C.flog_ck[row] = ck;
+  C.flog_aux[row] = make_uint2(src, g);
+  const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
+  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row);
 }
 
 // Relaxation of U independent candidates of one thread.  Every memory step
-// is issued for all U candidates before any result is consumed, so a thread
-// keeps U table round trips in flight: loads of the entries, key claims
-// (hashed tables), value CAS-128s.  Lost races and probe chains fall back to
-// the sequential path.
+// is issued for all U candidates before any result is consumed: loads of the
+// slots, key claims (hashed tables), row writes, value CAS-128s.  Lost races
+// and probe chains fall back to the sequential path.
 template <int U, typename F, typename S>
-__device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh,
-                                            const bool (&on)[U], const u32 (&d)[U],
-                                            const u64 (&ck)[U], const u32 (&g)[U],
-                                            const u32 (&info)[U], u32 round, int &rec) {
+__device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
+                                            const bool (&on)[U], const u32 (&d)[U], const u64 (&ck)[U],
+                                            const u32 (&g)[U], const u32 (&src)[U], const u32 (&rflags)[U],
+                                            u32 round) {
   const u32 etag = C.etag;
   const u64 ep = (u64)C.epoch << 32;
   u32 slot[U];
@@ -646,62 +663,69 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (on[u] && !fast[u]) relax_probe<F, S>(P, C, sh, d[u], ck[u], g[u], info[u], round, slot[u], key[u], vck[u], vg[u], vinfo[u]);
+      if (on[u] && !fast[u])
+        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], round, slot[u], key[u], vck[u],
+                          vg[u], vinfo[u]);
   } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) fast[u] = on[u];
   }
   bool want[U];
-  u64 r0[U], r1[U];
+  u32 nw = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     want[u] = fast[u] && value_better(ck[u], g[u], round, etag, vck[u], vg[u], vinfo[u]);
-    if (want[u])
-      cas128(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u],
-             ((u64)info[u] << 32) | g[u], r0[u], r1[u]);
+    nw += want[u] ? 1u : 0u;
   }
-  int code[U];
-  u32 n_new = 0, n_app = 0;
+  if (!nw) return;
+  u32 row = atomicAdd(&sh.flog_n, nw);
+  if (row + nw > P.flog_cap) {
+    set_error(sh, E_CAP);
+    return;
+  }
+  u32 rows[U], ninfo[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    code[u] = 0;
+    rows[u] = 0;
+    ninfo[u] = 0;
     if (!want[u]) continue;
-    if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u])) {
-      code[u] = applied_code(round, etag, vinfo[u]);
-      rec += rec_delta(code[u], info[u], vinfo[u]);
-    } else {
-      code[u] = relax_value(val_at(C, slot[u]), ck[u], g[u], info[u], round, etag, r0[u], (u32)r1[u],
-                            (u32)(r1[u] >> 32), vg[u], rec);
-    }
-    n_app += code[u] != 0;
-    n_new += code[u] == 1;
+    rows[u] = row++;
+    C.flog_state[rows[u]] = d[u] | rflags[u];
+    C.flog_ck[rows[u]] = ck[u];
+    C.flog_aux[rows[u]] = make_uint2(src[u], g[u]);
+    ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
   }
-  if (n_new && atomicAdd(&sh.n_new, n_new) + n_new > P.tok_cap) set_error(sh, E_CAP);
-  if (n_app) {
-    u32 ip = atomicAdd(&sh.n_app, n_app);
+  u64 r0[U], r1[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!code[u]) continue;
-      if (ip < P.tok_cap) {
-        C.app_list[ip] = slot[u] | (code[u] == 2 ? APP_IMPROVED : 0u);
-        if (!F::hashed && code[u] == 2) C.app_old[ip] = vg[u];
-      }
-      ++ip;
-    }
+  for (int u = 0; u < U; ++u)
+    if (want[u])
+      cas128(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u], ((u64)ninfo[u] << 32) | g[u],
+             r0[u], r1[u]);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!want[u]) continue;
+    if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u]))
+      installed(P, C, sh, acc, round, etag, vinfo[u], ck[u]);
+    else
+      relax_retry(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
+                  (u32)(r1[u] >> 32), rows[u]);
   }
 }
 
 // Expansion of an input list (token list or frontier rows) over one CSR
 // (emitting or epsilon), in tiles of BLOCK * Q inputs:
 //   1. each thread loads Q consecutive inputs and their CSR ranges (all loads
-//      independent), one block scan of the out-degrees;
+//      independent; displaced frontier rows and states without arcs of the
+//      kind expand nothing), one block scan of the out-degrees;
 //   2. the tile's arcs are split into one contiguous range per thread; a
 //      thread walks its range U arcs at a time: U arc-record loads, U
 //      candidates (boost lookup fused into the cost add), one batched
 //      relaxation.
+// Candidates carry their source: token index (emitting pass) or absolute
+// frontier row (epsilon rounds), src_base + input index.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state,
-                       const u64 *in_ck, const double *in_cost, u32 n_in, u32 round) {
+                       const u64 *in_ck, const double *in_cost, u32 n_in, u32 src_base, u32 round) {
   constexpr u32 TILE = BLOCK * Q;
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
@@ -709,22 +733,24 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   const int tid = threadIdx.x;
   const u32 *off = EMIT ? P.e_off : P.x_off;
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
-  const u32 info_hi = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT);
+  RelaxAcc acc;
+  acc.min_ck = ~0ull;
+  acc.n_new = 0;
+  acc.n_app = 0;
   u32 arcs_seen = 0;
-  int rec = 0;
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
     u32 st[Q], a0[Q], cnt[Q];
     double c[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) st[q] = i0 + q < n_in ? in_state[i0 + q] : 0xFFFFFFFFu;
+    for (int q = 0; q < Q; ++q) st[q] = i0 + q < n_in ? in_state[i0 + q] : ROW_DISP;
 #pragma unroll
     for (int q = 0; q < Q; ++q) c[q] = i0 + q < n_in ? (in_ck ? key_cost(in_ck[i0 + q]) : in_cost[i0 + q]) : 0.0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (st[q] != 0xFFFFFFFFu && (EMIT || (st[q] & ROW_EPS))) {
+      if (EMIT ? (i0 + q < n_in) : ((st[q] & (ROW_EPS | ROW_DISP)) == ROW_EPS)) {
         const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
         a0[q] = __ldg(&off[s]);
         cnt[q] = __ldg(&off[s + 1]);
@@ -775,7 +801,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         if (on[u]) {
           while (t_pref[j + 1] <= k + u) ++j;
           a[u] = t_a0[j] + (k + u - t_pref[j]);
-          src[u] = base + j;
+          src[u] = src_base + base + j;
           cj[u] = t_cost[j];
         }
       }
@@ -791,11 +817,11 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         }
       }
       u64 ck[U];
-      u32 info[U];
+      u32 rflags[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         ck[u] = 0;
-        info[u] = 0;
+        rflags[u] = 0;
         if (on[u]) {
           // _effective_weights (decoder.py:234-240): boost fused into the cost add
           const bool bst = is_boosted(C, g[u] & G_MASK, ol[u]);
@@ -804,16 +830,17 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
           else cand = cj[u] + we;                                    // decoder.py:268
           ck[u] = cost_key(cand);
-          info[u] = info_hi | (bst ? (1u << BOOST_SHIFT) : 0u) | (ol[u] ? (1u << HASOL_SHIFT) : 0u) |
-                    (src[u] & SRC_MASK);
+          rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<U>(P, C, sh, on, d, ck, g, info, round, rec);
+      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, round);
       k += U;
     }
     __syncthreads();
   }
-  if (rec) atomicAdd(&sh.rec_logical, (unsigned long long)(long long)rec);
+  if (acc.min_ck != ~0ull) atomicMin(&sh.min_ck, acc.min_ck);
+  if (acc.n_app) atomicAdd(&sh.n_app, acc.n_app);
+  if (acc.n_new && atomicAdd(&sh.n_new, acc.n_new) + acc.n_new > P.tok_cap) set_error(sh, E_CAP);
   if (tid == 0) {
     sh.n_cand += arcs_seen;
     sh.cnt_tok += n_in;
@@ -822,66 +849,18 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   }
 }
 
-// Snapshot of the slots applied in one phase into the frontier log: one row
-// per application {state | flags, cost key, (info, arc id)} of the winner;
-// the slot is pointed at its row and the row of an improved slot's previous
-// application is retired.  Provenance (back-pointer, emission records, hits,
-// last ilabel) is not resolved here: prune resolves it for the survivors only
-// by walking the rows' source links (resolve_row).
+// Applies the round's kill queue (after the round's barrier): displaced rows
+// are not applications, superseded ones are applications but not tokens.
 template <int BLOCK, typename F, typename S>
-__device__ void snapshot(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 round, u32 n_app,
-                         u32 row_base) {
-  if (row_base + n_app > P.flog_cap) {
-    if (threadIdx.x == 0) set_error(sh, E_CAP);
-    return;
+__device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+  const u32 n = min(sh.n_kill, P.flog_cap);
+  for (u32 i = threadIdx.x; i < n; i += BLOCK) {
+    const u32 v = C.app_list[i];
+    atomicOr(&C.flog_state[v & VROW_MASK], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
   }
-  if (threadIdx.x == 0) sh.round_base[round] = row_base;
-  u64 mck = ~0ull;
-  for (u32 i0 = threadIdx.x; i0 < n_app; i0 += BLOCK * SNAP) {
-    u32 slot[SNAP], d[SNAP], g[SNAP], info[SNAP], oldrow[SNAP] = {};
-    u64 ck[SNAP];
-    bool on[SNAP], imp[SNAP];
-#pragma unroll
-    for (int u = 0; u < SNAP; ++u) {
-      const u32 i = i0 + u * BLOCK;
-      on[u] = i < n_app;
-      slot[u] = 0;
-      imp[u] = false;
-      if (!on[u]) continue;
-      const u32 a = C.app_list[i];
-      slot[u] = a & ~APP_IMPROVED;
-      imp[u] = (a & APP_IMPROVED) != 0;
-      oldrow[u] = (!F::hashed && imp[u]) ? C.app_old[i] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < SNAP; ++u) {
-      d[u] = 0;
-      ck[u] = 0;
-      g[u] = 0;
-      info[u] = 0;
-      if (!on[u]) continue;
-      if (F::hashed) {
-        u64 key;
-        ld_cg_head(&C.table[slot[u]], key, oldrow[u]);
-        d[u] = (u32)key;
-      } else {
-        d[u] = slot[u];
-      }
-      ld_cg_value(val_at(C, slot[u]), ck[u], g[u], info[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < SNAP; ++u) {
-      if (!on[u]) continue;
-      const u32 row = row_base + i0 + u * BLOCK;
-      C.flog_state[row] = d[u] | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
-      C.flog_ck[row] = ck[u];
-      C.flog_aux[row] = make_uint2(info[u], g[u]);
-      *row_at(C, slot[u]) = row;
-      if (imp[u]) atomicOr(&C.flog_state[oldrow[u]], ROW_DEAD);
-      mck = min(mck, ck[u]);
-    }
-  }
-  if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
+  __syncthreads();
+  if (threadIdx.x == 0) sh.n_kill = 0;
+  __syncthreads();
 }
 
 // Labels of a global arc id (olabel, ilabel).
@@ -898,11 +877,10 @@ __device__ __forceinline__ void arc_labels(const DecodeParams &P, u32 g, u32 &ol
 }
 
 // Provenance of a surviving frontier row (decoder.py:385-393, 289-295): walks
-// the row's source links back to the token of the previous frame (or the
-// utterance start), then appends the emission records of the path's arcs with
-// olabel != 0, oldest first, and returns the token's provenance.  Source of a
-// row of round r >= 1: row round_base[r - 1] + src; of round 0: token src of
-// the previous frame's list (prev_tok).
+// the row's source links back to the token of the previous frame (rows below
+// sh.emit_end are the emitting pass's, their source is a token index) or to
+// the utterance start, then appends the emission records of the path's arcs
+// with olabel != 0, oldest first, and returns the token's provenance.
 template <typename F, typename S>
 __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 row,
                                const TokInfo *prev_tok) {
@@ -911,22 +889,23 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   base.depth = 0;
   base.hits = 0;
   base.last_il = 0;
+  const u32 emit_end = sh.emit_end;
   int hits = 0;
   u32 nrec = 0, il = 0;
   u32 cur = row;
   while (true) {
     const uint2 ax = C.flog_aux[cur];
     if (ax.y == G_START) break;
-    hits += (int)((ax.x >> BOOST_SHIFT) & 1u);
-    nrec += (ax.x >> HASOL_SHIFT) & 1u;
-    const u32 round = ax.x >> ROUND_SHIFT, src = ax.x & SRC_MASK;
-    if (round == 0) {
+    const u32 fl = C.flog_state[cur];
+    hits += (fl & ROW_BOOST) ? 1 : 0;
+    nrec += (fl & ROW_HASOL) ? 1u : 0u;
+    if (cur < emit_end) {
       u32 ol;
       arc_labels(P, ax.y & G_MASK, ol, il);
-      base = prev_tok[src];
+      base = prev_tok[ax.x];
       break;
     }
-    cur = sh.round_base[round - 1] + src;
+    cur = ax.x;
   }
   TokInfo t;
   t.hits = base.hits + hits;
@@ -944,23 +923,23 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
     cur = row;
     while (k) {
       const uint2 ax = C.flog_aux[cur];
-      if ((ax.x >> HASOL_SHIFT) & 1u) {
+      if (C.flog_state[cur] & ROW_HASOL) {
         u32 ol, il2;
         arc_labels(P, ax.y & G_MASK, ol, il2);
         --k;
         C.arena[r0 + k] = make_int2((int)ol, k ? (int)(r0 + k - 1) : base.bp);
       }
-      const u32 round = ax.x >> ROUND_SHIFT;
-      if (round == 0) break;
-      cur = sh.round_base[round - 1] + (ax.x & SRC_MASK);
+      if (cur < emit_end) break;
+      cur = ax.x;
     }
   }
   return t;
 }
 
 // _epsilon_rounds (decoder.py:250-316) starting from frontier rows
-// [fbase, fbase + nf) of the frontier log.
-template <int BLOCK, int TPT, typename F, typename S>
+// [fbase, fbase + nf) of the frontier log; the rows of round r are
+// [end of round r - 1, sh.flog_n after round r).
+template <int BLOCK, typename F, typename S>
 __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 fbase, u32 nf) {
   int rounds = 0;
   while (true) {
@@ -969,31 +948,28 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       break;
     }
     rounds++;
+    const u32 row_base = sh.flog_n;
+    __syncthreads();
     if (threadIdx.x == 0) {
       sh.n_app = 0;
       sh.n_cand = 0;
     }
     __syncthreads();
-    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf,
+    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf, fbase,
                                        (u32)rounds);
     __syncthreads();
+    apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
     PROF_COUNT(sh, PF_ROUNDS, 1);
     const u32 n_cand = sh.n_cand, n_app = sh.n_app;
     if (sh.error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
-    const u32 row_base = sh.flog_n;
-    snapshot<BLOCK>(P, C, sh, (u32)rounds, n_app, row_base);
-    __syncthreads();
-    PROF_MARK(sh, PF_EPS_S);
-    if (threadIdx.x == 0) sh.flog_n = row_base + n_app;
-    __syncthreads();
-    if (sh.error) return;
     fbase = row_base;
-    nf = n_app;
+    nf = sh.flog_n - row_base;
   }
   __syncthreads();
 }
+
 
 // Provenance of a new token list (token i comes from frontier row rows[i]):
 // resolve_row per token into tok_info_alt (the previous list's provenance is
@@ -1116,23 +1092,26 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   u64 bk = ~0ull;
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
-  u32 n_keep = 0;
+  u32 n_keep = 0, n_rec = 0;
   for (u32 base = 0; base < n_rows; base += TILE) {
     const u32 i0 = base + (u32)tid * QP;
     u32 st[QP];
     u64 ck[QP];
 #pragma unroll
-    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DEAD;
+    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
 #pragma unroll
     for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
     u32 cnt = 0;
 #pragma unroll
-    for (int q = 0; q < QP; ++q) cnt += (!(st[q] & ROW_DEAD) && ck[q] <= thr_ck) ? 1u : 0u;
+    for (int q = 0; q < QP; ++q) {
+      cnt += (!(st[q] & (ROW_DEAD | ROW_DISP)) && ck[q] <= thr_ck) ? 1u : 0u;
+      n_rec += (st[q] & (ROW_DISP | ROW_HASOL)) == ROW_HASOL ? 1u : 0u;
+    }
     u32 total;
     u32 p = n_keep + block_excl_scan<BLOCK>(cnt, total, sh.scan);
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      if ((st[q] & ROW_DEAD) || ck[q] > thr_ck) continue;
+      if ((st[q] & (ROW_DEAD | ROW_DISP)) || ck[q] > thr_ck) continue;
       const u32 s = st[q] & ROW_STATE;
       C.scr_key[p] = ck[q];
       C.scr_row[p] = i0 + q;
@@ -1142,6 +1121,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     }
     n_keep += total;
   }
+  if (n_rec) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec); // emission records (store_len)
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_SCAN);
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
@@ -1220,8 +1200,9 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   u32 n_tok = 0;
   for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
     const u32 i = i0 + threadIdx.x;
-    const u32 st = i < n_rows ? C.flog_state[i] : ROW_DEAD;
-    const bool live = !(st & ROW_DEAD);
+    const u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
+    const bool live = !(st & (ROW_DEAD | ROW_DISP));
+    if ((st & (ROW_DISP | ROW_HASOL)) == ROW_HASOL) atomicAdd(&sh.rec_logical, 1ull);
     u32 total;
     const u32 p = n_tok + block_excl_scan<BLOCK>(live ? 1u : 0u, total, sh.scan);
     if (live) {
@@ -1265,6 +1246,8 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.n_app = 0;
     sh.n_cand = 0;
     sh.flog_n = 0;
+    sh.n_kill = 0;
+    sh.emit_end = 0;
     sh.min_ck = ~0ull;
   }
   __syncthreads();
@@ -1332,32 +1315,28 @@ __device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   __syncthreads();
 }
 
-// Puts the utterance-start token into a fresh epoch (decoder.py:243-247).
+// Puts the utterance-start token into a fresh epoch (decoder.py:243-247):
+// row 0, no source arc, always expanded by the closure.
 template <int BLOCK, typename F, typename S>
 __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   next_epoch<BLOCK>(P, C, sh);
   if (threadIdx.x == 0) {
-    const u32 d = (u32)P.start;
+    RelaxAcc acc;
+    acc.min_ck = ~0ull;
+    acc.n_new = acc.n_app = 0;
     const bool on1[1] = {true};
-    const u32 d1[1] = {d}, g1[1] = {0xFFFFFFFFu}, i1[1] = {C.etag << TAG_SHIFT};
+    const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS};
     const u64 c1[1] = {cost_key(0.0)};
-    int rec1 = 0;
-    relax_batch<1>(P, C, sh, on1, d1, c1, g1, i1, 0u, rec1);
-    // the start entry's slot is app_list[0]; its row 0 has no provenance
-    const u32 s0 = C.app_list[0] & ~APP_IMPROVED;
-    C.flog_state[0] = d | ROW_EPS; // the closure reads the start state's epsilon range
-    C.flog_ck[0] = cost_key(0.0);
-    C.flog_aux[0] = make_uint2(0u, G_START);
-    sh.round_base[0] = 0;
-    *row_at(C, s0) = 0;
-    sh.flog_n = 1;
+    relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, 0u);
+    sh.n_kill = 0;
+    sh.emit_end = 0;
     sh.min_ck = cost_key(0.0);
   }
   __syncthreads();
 }
 
 // advance_frame (decoder.py:341-411) for frame row C.row.
-template <int BLOCK, int TPT, typename F, typename S>
+template <int BLOCK, typename F, typename S>
 __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   ChanState *cs = C.cs;
   if (cs->info.status != AB_IDLE && cs->info.status != AB_DECODING) {
@@ -1377,7 +1356,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   }
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
-    epsilon_rounds<BLOCK, TPT>(P, C, sh, 0u, 1u); // utterance-start closure, no prune
+    epsilon_rounds<BLOCK>(P, C, sh, 0u, 1u); // utterance-start closure, no prune
     if (sh.error) return;
     rows_to_tokens<BLOCK>(P, C, sh);
     if (threadIdx.x == 0) cs->info.fresh = 0;
@@ -1387,22 +1366,19 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   next_epoch<BLOCK>(P, C, sh);
-  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u);
+  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u, 0u);
   __syncthreads();
+  apply_kills<BLOCK>(P, C, sh);
   PROF_MARK(sh, PF_EMIT_X);
   if (sh.error) return;
   const u32 n_app = sh.n_app;
+  if (threadIdx.x == 0) sh.emit_end = sh.flog_n;
+  __syncthreads();
   if (n_app == 0) {
     // no emitting arcs: every token dies (decoder.py:394-398)
     if (threadIdx.x == 0) cs->info.num_active = 0;
   } else {
-    snapshot<BLOCK>(P, C, sh, 0u, n_app, 0u);
-    __syncthreads();
-    PROF_MARK(sh, PF_EMIT_S);
-    if (threadIdx.x == 0) sh.flog_n = n_app;
-    __syncthreads();
-    if (sh.error) return;
-    epsilon_rounds<BLOCK, TPT>(P, C, sh, 0u, n_app);
+    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.emit_end);
     if (sh.error) return;
     prune<BLOCK>(P, C, sh);
   }
@@ -1592,7 +1568,6 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     const size_t s = (size_t)slot;
     C.table = P.table ? P.table + s * P.table_cap : nullptr;
     C.vals = P.vals ? P.vals + 2 * s * P.table_cap : nullptr;
-    C.app_old = P.app_old ? P.app_old + s * P.tok_cap : nullptr;
     C.tok_state = P.tok_state + s * P.tok_cap;
     C.tok_cost = P.tok_cost + s * P.tok_cap;
     C.tok_info = P.tok_info + s * P.tok_cap;
@@ -1600,7 +1575,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.flog_ck = P.flog_ck + s * P.flog_cap;
     C.flog_aux = P.flog_aux + s * P.flog_cap;
     C.tok_info_alt = P.tok_info_alt + s * P.tok_cap;
-    C.app_list = P.app_list + s * P.tok_cap;
+    C.app_list = P.app_list + s * P.flog_cap;
     C.scr_key = P.scr_key + s * P.flog_cap;
     C.scr_row = P.scr_row + s * P.flog_cap;
     C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
@@ -1660,7 +1635,6 @@ template <int BLOCK, typename F, typename S>
 #endif
 __global__ void __launch_bounds__(BLOCK, AB_MINB)
     decode_kernel(const __grid_constant__ DecodeParams P) {
-  constexpr int TPT = 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
   __shared__ Chan<F, S> C;
@@ -1712,7 +1686,7 @@ __global__ void __launch_bounds__(BLOCK, AB_MINB)
       }
       __syncthreads();
       PROF_MARK(sh, PF_ROW);
-      advance<BLOCK, TPT>(P, C, sh);
+      advance<BLOCK>(P, C, sh);
       if (sh.error) break;
       if (P.mode == AB_MODE_STREAM) {
         if (cs->info.frame_index % P.partial_every == 0) {
