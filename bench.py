@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--states", type=int, default=None)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-overhead", action="store_true", help="skip the unbiased / zero-discount runs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
     return p.parse_args()
@@ -179,6 +180,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profile_ref():
+    """DRAM bytes per channel-frame of the decode kernel from the committed ncu
+    summary (profiles/ncu_current.json) and the measured random-sector ceiling
+    (profiles/random_access_peak.json, bench_tools/random_access_peak.cu)."""
+    out = {}
+    p = ROOT / "profiles" / "ncu_current.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        k = d[0] if isinstance(d, list) else d
+        if "dram_bytes_per_channel_frame" in k:
+            out["dram_bytes_per_channel_frame"] = float(k["dram_bytes_per_channel_frame"])
+            out["ncu_source"] = "profiles/ncu_current.json"
+    q = ROOT / "profiles" / "random_access_peak.json"
+    if q.exists():
+        r = json.loads(q.read_text())
+        out["random_read_Gsectors_s"] = r.get("read16_64GB_Gsect_s")
+        out["random_cas_Gops_s"] = r.get("cas16_64GB_Gop_s")
+    return out
+
+
 def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -263,6 +284,8 @@ def run_b200(args, W, world, rank, local):
     t0 = time.time()
     dg = DeviceGraph(csr, device=local)
     handles = [dg.register_context(c.arc_indices, c.discount) for c in pool]
+    # same arc sets with discount 0: identical search, pure lookup cost (biasing overhead)
+    handles0 = [dg.register_context(c.arc_indices, 0.0) for c in pool]
     # emission arena: ~16 frames of appends (~45k records per channel-frame on
     # G_large); the in-kernel copying GC reclaims records of pruned paths
     big = W["states"] > 1_000_000
@@ -277,7 +300,8 @@ def run_b200(args, W, world, rank, local):
     def ctxs(seg, variant):
         if variant == "none" or not handles:
             return np.full(C, -1, dtype=np.int32)
-        return np.array([handles[ctx_index(c, seg, len(handles))] for c in range(C)], dtype=np.int32)
+        hs = handles0 if variant == "zero" else handles
+        return np.array([hs[ctx_index(c, seg, len(hs))] for c in range(C)], dtype=np.int32)
 
     def step(on_device=True, variant="biased", collect=False):
         kernel_ms = 0.0
@@ -328,6 +352,17 @@ def run_b200(args, W, world, rank, local):
     clocks.start()
     ms, outs = timed(args.steps)
     clk = clocks.stop()
+    # biasing overhead: the same decode without contexts and with
+    # zero-discount contexts (identical search, lookup cost only)
+    bias = {}
+    if not args.no_overhead:
+        t_none, _ = timed(1, variant="none")
+        t_zero, _ = timed(1, variant="zero")
+        t_bias = ms / args.steps
+        bias = {"unbiased_ms_per_step": t_none, "zero_discount_ms_per_step": t_zero,
+                "biased_ms_per_step": t_bias,
+                "zero_discount_overhead_pct": 100.0 * (t_zero / t_none - 1.0),
+                "discount_overhead_pct": 100.0 * (t_bias / t_none - 1.0)}
     first = step(collect=True)
     ms_max = max_over_ranks(ms, world, dev)
     frames_total = C * T * args.steps * world
@@ -337,6 +372,21 @@ def run_b200(args, W, world, rank, local):
     kms = outs[-1]["kernel_ms"]
     peak, peak_kind = hbm_peak()
     achieved = alg_bytes / (kms / 1000.0) / 1e9
+    # measured DRAM traffic (ncu, per channel-frame) scaled to one decode launch
+    # (one segment of all channels), and the random-sector view of the same run
+    pref = profile_ref()
+    traffic = None
+    random_access = None
+    if "dram_bytes_per_channel_frame" in pref:
+        bpcf = pref["dram_bytes_per_channel_frame"]
+        traffic = bpcf * C * Tseg
+        kernel_fps = C * T / (kms / 1000.0)
+        random_access = {"dram_bytes_per_channel_frame": bpcf,
+                         "dram_GBps_at_kernel_rate": bpcf * kernel_fps / 1e9,
+                         "sectors_Gps_at_kernel_rate": bpcf * kernel_fps / 32 / 1e9,
+                         "random_read_ceiling_Gsectors_s": pref.get("random_read_Gsectors_s"),
+                         "random_cas_ceiling_Gops_s": pref.get("random_cas_Gops_s"),
+                         "source": pref.get("ncu_source")}
     result = {
         "metric": "decoded frames/sec with biasing (1024-channel biased config, C3)",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -352,13 +402,16 @@ def run_b200(args, W, world, rank, local):
         "gpu_launches": outs[-1]["launches"] * args.steps,
         "clocks": clk,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "decode_kernel (whole frame loop; expand + epsilon + prune fused)",
                      "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": kms,
                      "per_channel_frame": {"N": n_tok / (C * T), "A_e": a_e / (C * T),
-                                           "A_eps": a_x / (C * T)}},
+                                           "A_eps": a_x / (C * T)},
+                     "random_access": random_access},
         "prep_s": prep,
     }
+    if bias:
+        result["biasing_overhead"] = bias
     if not args.no_e2e:
         for _ in range(1):
             step(on_device=False)

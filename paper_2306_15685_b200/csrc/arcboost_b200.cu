@@ -63,7 +63,7 @@ struct ab_graph {
   bool fmt16 = true; // f32 weights and 16-bit labels: 16-byte arc records
   std::vector<int32_t> olabels; // host copy for context classification
   std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
-  u32 *e_off = nullptr, *x_off = nullptr;
+  uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
   void *e_arcs = nullptr, *x_arcs = nullptr;
   int2 *arc_meta = nullptr;  // labels that do not fit the packed form
   u32 *arc_meta32 = nullptr; // olabel:16 | ilabel:15 | META_DEST_EPS
@@ -93,6 +93,7 @@ struct ab_decoder {
   u32 *flog_state = nullptr;
   u64 *flog_ck = nullptr;
   uint2 *flog_aux = nullptr;
+  u32 *eps_list = nullptr;
   TokInfo *tok_info_alt = nullptr;
   u32 *app_list = nullptr;
   u64 *scr_key = nullptr;
@@ -262,7 +263,12 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       meta32[a] = (u32)meta[a].x | ((u32)(meta[a].y & 0x7FFF) << 16) | ((u32)meta[a].y & META_DEST_EPS);
     meta.clear();
   }
-  if (dmalloc(&g->e_off, num_states + 1, acc) || dmalloc(&g->x_off, num_states + 1, acc) ||
+  std::vector<uint2> erng(num_states), xrng(num_states);
+  for (int s = 0; s < num_states; ++s) {
+    erng[s] = make_uint2(e_cnt[s], e_cnt[s + 1]);
+    xrng[s] = make_uint2(x_cnt[s], x_cnt[s + 1]);
+  }
+  if (dmalloc(&g->e_rng, num_states, acc) || dmalloc(&g->x_rng, num_states, acc) ||
       dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
       (pack ? dmalloc(&g->arc_meta32, meta32.size(), acc) : dmalloc(&g->arc_meta, meta.size(), acc)) ||
       dmalloc(&g->final_cost, num_states, acc)) {
@@ -273,8 +279,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   g->x_arcs = dx;
   g->bytes = acc;
   if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMemcpy(g->e_off, e_cnt.data(), (num_states + 1) * sizeof(u32), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(g->x_off, x_cnt.data(), (num_states + 1) * sizeof(u32), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->e_rng, erng.data(), num_states * sizeof(uint2), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->x_rng, xrng.data(), num_states * sizeof(uint2), cudaMemcpyHostToDevice) ||
       cudaMemcpy(de, eh.data(), eh.size(), cudaMemcpyHostToDevice) ||
       cudaMemcpy(dx, xh.data(), xh.size(), cudaMemcpyHostToDevice) ||
       (pack ? cudaMemcpy(g->arc_meta32, meta32.data(), meta32.size() * sizeof(u32), cudaMemcpyHostToDevice)
@@ -295,8 +301,8 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
     cudaFree(c.d_bits);
   }
   cudaFree(g->d_ctxs);
-  cudaFree(g->e_off);
-  cudaFree(g->x_off);
+  cudaFree(g->e_rng);
+  cudaFree(g->x_rng);
   cudaFree(g->e_arcs);
   cudaFree(g->x_arcs);
   cudaFree(g->arc_meta);
@@ -512,7 +518,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
       dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
-      dmalloc(&d->flog_aux, C * d->flog_cap, acc) ||
+      dmalloc(&d->flog_aux, C * d->flog_cap, acc) || dmalloc(&d->eps_list, C * d->flog_cap, acc) ||
       dmalloc(&d->tok_info_alt, C * d->tok_cap, acc) ||
       dmalloc(&d->app_list, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
@@ -554,7 +560,7 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->vals, d->tok_state, d->tok_cost, d->tok_info,
-                  d->flog_state, d->flog_ck,  d->flog_aux, d->tok_info_alt, d->app_list,
+                  d->flog_state, d->flog_ck,  d->flog_aux, d->eps_list, d->tok_info_alt, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
@@ -789,9 +795,9 @@ static int ensure_batch(ab_decoder *d, size_t n) {
 static void fill_params(ab_decoder *d, DecodeParams &P) {
   ab_graph *g = d->g;
   memset(&P, 0, sizeof(P));
-  P.e_off = g->e_off;
+  P.e_rng = g->e_rng;
   P.e_arcs = g->e_arcs;
-  P.x_off = g->x_off;
+  P.x_rng = g->x_rng;
   P.x_arcs = g->x_arcs;
   P.arc_meta = g->arc_meta;
   P.arc_meta32 = g->arc_meta32;
@@ -817,6 +823,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.flog_state = d->flog_state;
   P.flog_ck = d->flog_ck;
   P.flog_aux = d->flog_aux;
+  P.eps_list = d->eps_list;
   P.tok_info_alt = d->tok_info_alt;
   P.flog_cap = d->flog_cap;
   P.app_list = d->app_list;

@@ -57,6 +57,14 @@ constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
 constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
 constexpr u32 ROW_HASOL = 0x08000000u; // the winning arc has an output label (an emission record)
 constexpr u32 ROW_STATE = 0x07FFFFFFu;
+// frontier row aux word {source | AUX_BOOST | AUX_HASOL, arc id}: the
+// provenance walk reads one 8-byte word per step
+constexpr u32 AUX_BOOST = 0x80000000u;
+constexpr u32 AUX_HASOL = 0x40000000u;
+constexpr u32 AUX_SRC = 0x3FFFFFFFu;
+__device__ __forceinline__ u32 aux_src(u32 src, u32 rflags) {
+  return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u);
+}
 constexpr u32 META_DEST_EPS = 0x80000000u;  // arc_meta.y flag: the arc's destination has epsilon arcs
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
@@ -185,9 +193,9 @@ struct DevHyp {
 
 struct DecodeParams {
   // graph (device CSR split into emitting / epsilon arcs, fst.py:116-191)
-  const u32 *e_off;
+  const uint2 *e_rng; // per state {begin, end} of its emitting arcs
   const void *e_arcs;
-  const u32 *x_off;
+  const uint2 *x_rng; // per state {begin, end} of its epsilon arcs
   const void *x_arcs;
   const int2 *arc_meta; // [num_arcs] {olabel, ilabel | META_DEST_EPS} by global arc id
   const u32 *arc_meta32; // packed olabel:16 | ilabel:15 | META_DEST_EPS when labels fit (else null)
@@ -209,7 +217,8 @@ struct DecodeParams {
   u32 tok_cap;
   u32 *flog_state;
   u64 *flog_ck;
-  uint2 *flog_aux; // {winner info, arc id | G_DEST_EPS} per frontier row
+  uint2 *flog_aux; // {source | AUX flags, arc id | G_DEST_EPS} per frontier row
+  u32 *eps_list;   // [channel][flog_cap] rows whose state has epsilon arcs, in write order
   u32 flog_cap;
   TokInfo *tok_info_alt;
   u32 *app_list;
@@ -431,6 +440,7 @@ struct Shared {
   int redi[32];
   u32 hist[256];
   u32 n_kill;   // kill queue length of the current round
+  u32 eps_n;    // entries in the channel's epsilon-frontier list this frame
   u32 emit_end; // rows below come from the emitting pass (their source is a token)
   int best_last_il;
 #ifdef AB_PROFILE
@@ -452,6 +462,7 @@ template <typename F, typename S> struct Chan {
   u32 *flog_state;
   u64 *flog_ck;
   uint2 *flog_aux;
+  u32 *eps_list;
   TokInfo *tok_info_alt;
   u32 *app_list;
   u64 *scr_key;
@@ -475,6 +486,7 @@ template <typename F, typename S> struct Chan {
   // expansion tile (shared memory)
   u32 *t_a0;
   u32 *t_pref;
+  u32 *t_src;
   double *t_cost;
 };
 
@@ -615,7 +627,8 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   }
   C.flog_state[row] = d | rflags;
   C.flog_ck[row] = ck;
-  C.flog_aux[row] = make_uint2(src, g);
+  C.flog_aux[row] = make_uint2(aux_src(src, rflags), g);
+  if (rflags & ROW_EPS) C.eps_list[atomicAdd(&sh.eps_n, 1u)] = row;
   const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
   relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row);
 }
@@ -684,15 +697,20 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     return;
   }
   u32 rows[U], ninfo[U];
+  u32 ne = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
+  u32 ep_at = ne ? atomicAdd(&sh.eps_n, ne) : 0u;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
     ninfo[u] = 0;
     if (!want[u]) continue;
     rows[u] = row++;
+    if (rflags[u] & ROW_EPS) C.eps_list[ep_at++] = rows[u]; // next round's epsilon frontier
     C.flog_state[rows[u]] = d[u] | rflags[u];
     C.flog_ck[rows[u]] = ck[u];
-    C.flog_aux[rows[u]] = make_uint2(src[u], g[u]);
+    C.flog_aux[rows[u]] = make_uint2(aux_src(src[u], rflags[u]), g[u]);
     ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
   }
   u64 r0[U], r1[U];
@@ -712,26 +730,26 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   }
 }
 
-// Expansion of an input list (token list or frontier rows) over one CSR
-// (emitting or epsilon), in tiles of BLOCK * Q inputs:
+// Expansion of an input list over one CSR, in tiles of BLOCK * Q inputs:
+// the emitting pass expands the token list (source = token index), an
+// epsilon round the frontier rows listed in `list` (rows of the previous round
+// whose state has epsilon arcs, appended when they were written; displaced
+// ones are skipped; source = row index).
 //   1. each thread loads Q consecutive inputs and their CSR ranges (all loads
-//      independent; displaced frontier rows and states without arcs of the
-//      kind expand nothing), one block scan of the out-degrees;
-//   2. the tile's arcs are split into one contiguous range per thread; a
-//      thread walks its range U arcs at a time: U arc-record loads, U
-//      candidates (boost lookup fused into the cost add), one batched
-//      relaxation.
-// Candidates carry their source: token index (emitting pass) or absolute
-// frontier row (epsilon rounds), src_base + input index.
+//      independent), one block scan of the out-degrees;
+//   2. arcs k = tid, tid + BLOCK, ... (warp-coalesced arc records), U per
+//      thread in flight: arc-record loads, candidates (boost lookup fused
+//      into the cost add), one batched relaxation.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
-__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *in_state,
-                       const u64 *in_ck, const double *in_cost, u32 n_in, u32 src_base, u32 round) {
+__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *list, u32 n_in,
+                       u32 round) {
   constexpr u32 TILE = BLOCK * Q;
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
+  u32 *t_src = C.t_src;
   double *t_cost = C.t_cost;
   const int tid = threadIdx.x;
-  const u32 *off = EMIT ? P.e_off : P.x_off;
+  const uint2 *rng = EMIT ? P.e_rng : P.x_rng;
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
   RelaxAcc acc;
   acc.min_ck = ~0ull;
@@ -740,28 +758,31 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   u32 arcs_seen = 0;
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
-    u32 st[Q], a0[Q], cnt[Q];
-    double c[Q];
+    u32 idx[Q], st[Q], a0[Q], cnt[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) st[q] = i0 + q < n_in ? in_state[i0 + q] : ROW_DISP;
+    for (int q = 0; q < Q; ++q) idx[q] = i0 + q < n_in ? (EMIT ? i0 + q : list[i0 + q]) : 0xFFFFFFFFu;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) c[q] = i0 + q < n_in ? (in_ck ? key_cost(in_ck[i0 + q]) : in_cost[i0 + q]) : 0.0;
+    for (int q = 0; q < Q; ++q)
+      st[q] = idx[q] == 0xFFFFFFFFu ? ROW_DISP : (EMIT ? C.tok_state[idx[q]] : C.flog_state[idx[q]]);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const u32 j = (u32)tid * Q + q;
+      t_src[j] = idx[q];
+      if (idx[q] != 0xFFFFFFFFu) t_cost[j] = EMIT ? C.tok_cost[idx[q]] : key_cost(C.flog_ck[idx[q]]);
+    }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (EMIT ? (i0 + q < n_in) : ((st[q] & (ROW_EPS | ROW_DISP)) == ROW_EPS)) {
-        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
-        a0[q] = __ldg(&off[s]);
-        cnt[q] = __ldg(&off[s + 1]);
+      if (EMIT ? (idx[q] != 0xFFFFFFFFu) : !(st[q] & ROW_DISP)) {
+        const uint2 r = __ldg(&rng[EMIT ? st[q] : (st[q] & ROW_STATE)]);
+        a0[q] = r.x;
+        cnt[q] = r.y - r.x;
       }
     }
     u32 tsum = 0;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      cnt[q] -= a0[q];
-      tsum += cnt[q];
-    }
+    for (int q = 0; q < Q; ++q) tsum += cnt[q];
     u32 total;
     u32 run = block_excl_scan<BLOCK>(tsum, total, sh.scan);
 #pragma unroll
@@ -769,40 +790,35 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       const u32 j = (u32)tid * Q + q;
       t_a0[j] = a0[q];
       t_pref[j] = run;
-      t_cost[j] = c[q];
       run += cnt[q];
     }
     if (tid == 0) t_pref[TILE] = total;
     __syncthreads();
     arcs_seen += total;
-    const u32 per = (total + BLOCK - 1) / BLOCK;
-    u32 k = min((u32)tid * per, total);
-    const u32 ke = min(k + per, total);
-    u32 j = 0;
-    if (k < ke) { // largest j with t_pref[j] <= k
-      u32 lo = 0, hi = TILE - 1;
-      while (lo < hi) {
-        const u32 mid = (lo + hi + 1) >> 1;
-        if (t_pref[mid] <= k) lo = mid;
-        else hi = mid - 1;
-      }
-      j = lo;
-    }
-    while (k < ke) {
+    // arcs k = tid, tid + BLOCK, ...: the lanes of a warp read consecutive
+    // arc records (one state's arcs are contiguous), so a warp load touches
+    // few lines; each thread keeps U such arcs in flight
+    for (u32 k0 = tid; k0 < total; k0 += BLOCK * U) {
       bool on[U];
       u32 a[U], src[U];
       double cj[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        on[u] = k + u < ke;
+        const u32 k = k0 + u * BLOCK;
+        on[u] = k < total;
         a[u] = 0;
         src[u] = 0;
         cj[u] = 0.0;
         if (on[u]) {
-          while (t_pref[j + 1] <= k + u) ++j;
-          a[u] = t_a0[j] + (k + u - t_pref[j]);
-          src[u] = src_base + base + j;
-          cj[u] = t_cost[j];
+          u32 lo = 0, hi = TILE - 1; // largest j with t_pref[j] <= k (its range holds k)
+          while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (t_pref[mid] <= k) lo = mid;
+            else hi = mid - 1;
+          }
+          a[u] = t_a0[lo] + (k - t_pref[lo]);
+          src[u] = t_src[lo];
+          cj[u] = t_cost[lo];
         }
       }
       u32 d[U], g[U], il[U], ol[U];
@@ -834,7 +850,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         }
       }
       relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, round);
-      k += U;
     }
     __syncthreads();
   }
@@ -843,7 +858,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   if (acc.n_new && atomicAdd(&sh.n_new, acc.n_new) + acc.n_new > P.tok_cap) set_error(sh, E_CAP);
   if (tid == 0) {
     sh.n_cand += arcs_seen;
-    sh.cnt_tok += n_in;
+    if (EMIT) sh.cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
     if (EMIT) sh.cnt_emit += arcs_seen;
     else sh.cnt_eps += arcs_seen;
   }
@@ -896,16 +911,15 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   while (true) {
     const uint2 ax = C.flog_aux[cur];
     if (ax.y == G_START) break;
-    const u32 fl = C.flog_state[cur];
-    hits += (fl & ROW_BOOST) ? 1 : 0;
-    nrec += (fl & ROW_HASOL) ? 1u : 0u;
+    hits += (ax.x & AUX_BOOST) ? 1 : 0;
+    nrec += (ax.x & AUX_HASOL) ? 1u : 0u;
     if (cur < emit_end) {
       u32 ol;
       arc_labels(P, ax.y & G_MASK, ol, il);
-      base = prev_tok[ax.x];
+      base = prev_tok[ax.x & AUX_SRC];
       break;
     }
-    cur = ax.x;
+    cur = ax.x & AUX_SRC;
   }
   TokInfo t;
   t.hits = base.hits + hits;
@@ -923,40 +937,40 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
     cur = row;
     while (k) {
       const uint2 ax = C.flog_aux[cur];
-      if (C.flog_state[cur] & ROW_HASOL) {
+      if (ax.x & AUX_HASOL) {
         u32 ol, il2;
         arc_labels(P, ax.y & G_MASK, ol, il2);
         --k;
         C.arena[r0 + k] = make_int2((int)ol, k ? (int)(r0 + k - 1) : base.bp);
       }
       if (cur < emit_end) break;
-      cur = ax.x;
+      cur = ax.x & AUX_SRC;
     }
   }
   return t;
 }
 
-// _epsilon_rounds (decoder.py:250-316) starting from frontier rows
-// [fbase, fbase + nf) of the frontier log; the rows of round r are
-// [end of round r - 1, sh.flog_n after round r).
+// _epsilon_rounds (decoder.py:250-316).  The frontier of the next round is
+// the previous round's applications (n_front of them); the ones whose state
+// has epsilon arcs are eps_list[lo, hi).
 template <int BLOCK, typename F, typename S>
-__device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 fbase, u32 nf) {
+__device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
+                               u32 n_front) {
   int rounds = 0;
   while (true) {
-    if (!(nf > 0 && rounds < P.max_eps)) {
-      if (nf > 0 && threadIdx.x == 0) C.cs->info.eps_truncations += 1; // while-else 314-316
+    if (!(n_front > 0 && rounds < P.max_eps)) {
+      if (n_front > 0 && threadIdx.x == 0) C.cs->info.eps_truncations += 1; // while-else 314-316
       break;
     }
     rounds++;
-    const u32 row_base = sh.flog_n;
     __syncthreads();
     if (threadIdx.x == 0) {
       sh.n_app = 0;
       sh.n_cand = 0;
+      sh.cnt_tok += n_front; // token expansions of the reference's round
     }
     __syncthreads();
-    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.flog_state + fbase, C.flog_ck + fbase, nullptr, nf, fbase,
-                                       (u32)rounds);
+    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, (u32)rounds);
     __syncthreads();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
@@ -964,8 +978,9 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     const u32 n_cand = sh.n_cand, n_app = sh.n_app;
     if (sh.error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
-    fbase = row_base;
-    nf = sh.flog_n - row_base;
+    lo = hi;
+    hi = sh.eps_n;
+    n_front = n_app;
   }
   __syncthreads();
 }
@@ -1247,6 +1262,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.n_cand = 0;
     sh.flog_n = 0;
     sh.n_kill = 0;
+    sh.eps_n = 0;
     sh.emit_end = 0;
     sh.min_ck = ~0ull;
   }
@@ -1356,7 +1372,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   }
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
-    epsilon_rounds<BLOCK>(P, C, sh, 0u, 1u); // utterance-start closure, no prune
+    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, 1u); // utterance-start closure, no prune
     if (sh.error) return;
     rows_to_tokens<BLOCK>(P, C, sh);
     if (threadIdx.x == 0) cs->info.fresh = 0;
@@ -1366,7 +1382,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   next_epoch<BLOCK>(P, C, sh);
-  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, C.tok_state, nullptr, C.tok_cost, n_tok, 0u, 0u);
+  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
   __syncthreads();
   apply_kills<BLOCK>(P, C, sh);
   PROF_MARK(sh, PF_EMIT_X);
@@ -1378,7 +1394,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     // no emitting arcs: every token dies (decoder.py:394-398)
     if (threadIdx.x == 0) cs->info.num_active = 0;
   } else {
-    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.emit_end);
+    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, n_app);
     if (sh.error) return;
     prune<BLOCK>(P, C, sh);
   }
@@ -1556,7 +1572,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
 template <int BLOCK, typename F, typename S>
 __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh_row,
                               u32 *sh_ctx, u32 *t_a0 = nullptr, u32 *t_pref = nullptr,
-                              double *t_cost = nullptr) {
+                              double *t_cost = nullptr, u32 *t_src = nullptr) {
   const int slot = P.slots[b];
   const int h = P.chans[slot].info.context;
   __syncthreads(); // the previous channel of this CTA is done with C
@@ -1574,6 +1590,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.flog_state = P.flog_state + s * P.flog_cap;
     C.flog_ck = P.flog_ck + s * P.flog_cap;
     C.flog_aux = P.flog_aux + s * P.flog_cap;
+    C.eps_list = P.eps_list + s * P.flog_cap;
     C.tok_info_alt = P.tok_info_alt + s * P.tok_cap;
     C.app_list = P.app_list + s * P.flog_cap;
     C.scr_key = P.scr_key + s * P.flog_cap;
@@ -1596,6 +1613,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.t_a0 = t_a0;
     C.t_pref = t_pref;
     C.t_cost = t_cost;
+    C.t_src = t_src;
   }
   __syncthreads();
   if (h >= 0 && h < P.num_ctxs) {
@@ -1641,11 +1659,12 @@ __global__ void __launch_bounds__(BLOCK, AB_MINB)
   __shared__ double tile_cost[BLOCK * EXP_Q];
   __shared__ u32 tile_a0[BLOCK * EXP_Q];
   __shared__ u32 tile_pref[BLOCK * EXP_Q + 1];
+  __shared__ u32 tile_src[BLOCK * EXP_Q];
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
   for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
-    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost);
+    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src);
     ChanState *cs = C.cs;
     if (threadIdx.x == 0) {
       sh.error = 0;
