@@ -65,8 +65,6 @@ struct ab_graph {
   std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
   uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
   void *e_arcs = nullptr, *x_arcs = nullptr;
-  int2 *arc_meta = nullptr;  // labels that do not fit the packed form
-  u32 *arc_meta32 = nullptr; // olabel:16 | ilabel:15 | META_DEST_EPS
   double *final_cost = nullptr;
   size_t bytes = 0;
   std::vector<HostCtx> ctxs;
@@ -92,7 +90,7 @@ struct ab_decoder {
   TokInfo *tok_info = nullptr;
   u32 *flog_state = nullptr;
   u64 *flog_ck = nullptr;
-  uint2 *flog_aux = nullptr;
+  uint4 *flog_aux = nullptr;
   u32 *eps_list = nullptr;
   TokInfo *tok_info_alt = nullptr;
   u32 *app_list = nullptr;
@@ -187,7 +185,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     x_cnt[s + 1] += x_cnt[s];
   }
   const u32 n_e = e_cnt[num_states], n_x = x_cnt[num_states];
-  std::vector<int2> meta(std::max<int64_t>(num_arcs, 1));
   std::vector<double> fin(num_states, std::nan(""));
   for (int i = 0; i < num_finals; ++i) {
     int s = final_states[i];
@@ -224,7 +221,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
       const int dst = next_states[a];
       const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
-      meta[a] = make_int2(olabels[a], ilabels[a] | (dst_eps ? (int)META_DEST_EPS : 0));
       if (ilabels[a] != 0) {
         const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
         if (f16) {
@@ -251,18 +247,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   size_t acc = 0;
   unsigned char *de = nullptr, *dx = nullptr;
-  // packed 4-byte arc metadata when every label fits (halves the snapshot's random reads)
-  bool pack = true;
-  for (size_t a = 0; a < meta.size() && pack; ++a)
-    pack = meta[a].x >= 0 && meta[a].x < 65536 && (meta[a].y & ~(int)META_DEST_EPS) >= 0 &&
-           (meta[a].y & ~(int)META_DEST_EPS) < 32768;
-  std::vector<u32> meta32;
-  if (pack) {
-    meta32.resize(meta.size());
-    for (size_t a = 0; a < meta.size(); ++a)
-      meta32[a] = (u32)meta[a].x | ((u32)(meta[a].y & 0x7FFF) << 16) | ((u32)meta[a].y & META_DEST_EPS);
-    meta.clear();
-  }
   std::vector<uint2> erng(num_states), xrng(num_states);
   for (int s = 0; s < num_states; ++s) {
     erng[s] = make_uint2(e_cnt[s], e_cnt[s + 1]);
@@ -270,7 +254,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   if (dmalloc(&g->e_rng, num_states, acc) || dmalloc(&g->x_rng, num_states, acc) ||
       dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
-      (pack ? dmalloc(&g->arc_meta32, meta32.size(), acc) : dmalloc(&g->arc_meta, meta.size(), acc)) ||
       dmalloc(&g->final_cost, num_states, acc)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "device allocation for the graph failed (%zu bytes)", acc);
@@ -283,8 +266,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       cudaMemcpy(g->x_rng, xrng.data(), num_states * sizeof(uint2), cudaMemcpyHostToDevice) ||
       cudaMemcpy(de, eh.data(), eh.size(), cudaMemcpyHostToDevice) ||
       cudaMemcpy(dx, xh.data(), xh.size(), cudaMemcpyHostToDevice) ||
-      (pack ? cudaMemcpy(g->arc_meta32, meta32.data(), meta32.size() * sizeof(u32), cudaMemcpyHostToDevice)
-            : cudaMemcpy(g->arc_meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice)) ||
       cudaMemcpy(g->final_cost, fin.data(), num_states * sizeof(double), cudaMemcpyHostToDevice)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "graph upload failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -305,8 +286,6 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   cudaFree(g->x_rng);
   cudaFree(g->e_arcs);
   cudaFree(g->x_arcs);
-  cudaFree(g->arc_meta);
-  cudaFree(g->arc_meta32);
   cudaFree(g->final_cost);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -468,7 +447,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
     const uint64_t tk = std::min<uint64_t>(S, MAX_TOKENS);
     const uint64_t fl = cap.frontier_rows > 0 ? (uint64_t)cap.frontier_rows : std::max<uint64_t>(65536, 2 * tk);
     const uint64_t ar = cap.arena_records > 0 ? (uint64_t)cap.arena_records : std::max<uint64_t>(1ull << 19, 8 * fl);
-    const double per_ch_other = (double)tk * (4 + 8 + 16 + 4) + (double)fl * (4 + 8 + 16 + 8 + 4) +
+    const double per_ch_other = (double)tk * (4 + 8 + 16 + 16) + (double)fl * (4 + 8 + 16 + 4 + 4 + 8 + 4) +
                                 (double)ar * (2 * 8 + 2 * 4.0 / 32);
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
@@ -799,8 +778,6 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.e_arcs = g->e_arcs;
   P.x_rng = g->x_rng;
   P.x_arcs = g->x_arcs;
-  P.arc_meta = g->arc_meta;
-  P.arc_meta32 = g->arc_meta32;
   P.final_cost = g->final_cost;
   P.start = g->start;
   P.num_states = g->num_states;

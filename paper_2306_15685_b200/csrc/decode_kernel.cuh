@@ -65,7 +65,6 @@ constexpr u32 AUX_SRC = 0x3FFFFFFFu;
 __device__ __forceinline__ u32 aux_src(u32 src, u32 rflags) {
   return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u);
 }
-constexpr u32 META_DEST_EPS = 0x80000000u;  // arc_meta.y flag: the arc's destination has epsilon arcs
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
 #ifndef AB_EXP_Q
@@ -197,8 +196,6 @@ struct DecodeParams {
   const void *e_arcs;
   const uint2 *x_rng; // per state {begin, end} of its epsilon arcs
   const void *x_arcs;
-  const int2 *arc_meta; // [num_arcs] {olabel, ilabel | META_DEST_EPS} by global arc id
-  const u32 *arc_meta32; // packed olabel:16 | ilabel:15 | META_DEST_EPS when labels fit (else null)
   const double *final_cost; // NaN = not final
   int start;
   int num_states;
@@ -217,7 +214,7 @@ struct DecodeParams {
   u32 tok_cap;
   u32 *flog_state;
   u64 *flog_ck;
-  uint2 *flog_aux; // {source | AUX flags, arc id | G_DEST_EPS} per frontier row
+  uint4 *flog_aux; // {source | AUX flags, arc id | G_DEST_EPS, olabel, ilabel} per frontier row
   u32 *eps_list;   // [channel][flog_cap] rows whose state has epsilon arcs, in write order
   u32 flog_cap;
   TokInfo *tok_info_alt;
@@ -461,7 +458,7 @@ template <typename F, typename S> struct Chan {
   TokInfo *tok_info;
   u32 *flog_state;
   u64 *flog_ck;
-  uint2 *flog_aux;
+  uint4 *flog_aux;
   u32 *eps_list;
   TokInfo *tok_info_alt;
   u32 *app_list;
@@ -597,8 +594,8 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
 // belongs to another state).  (key, vck, vg, vinfo) = contents of `slot`.
 template <typename F, typename S>
 __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
-                                         u32 d, u64 ck, u32 g, u32 src, u32 rflags, u32 round, u32 slot,
-                                         u64 key, u64 vck, u32 vg, u32 vinfo) {
+                                         u32 d, u64 ck, u32 g, u32 src, u32 rflags, u32 lab_ol, u32 lab_il,
+                                         u32 round, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
   const u64 ep = (u64)C.epoch << 32;
   u32 probes = 0;
   while (true) {
@@ -627,7 +624,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   }
   C.flog_state[row] = d | rflags;
   C.flog_ck[row] = ck;
-  C.flog_aux[row] = make_uint2(aux_src(src, rflags), g);
+  C.flog_aux[row] = make_uint4(aux_src(src, rflags), g, lab_ol, lab_il);
   if (rflags & ROW_EPS) C.eps_list[atomicAdd(&sh.eps_n, 1u)] = row;
   const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
   relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row);
@@ -641,7 +638,7 @@ template <int U, typename F, typename S>
 __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
                                             const bool (&on)[U], const u32 (&d)[U], const u64 (&ck)[U],
                                             const u32 (&g)[U], const u32 (&src)[U], const u32 (&rflags)[U],
-                                            u32 round) {
+                                            const u32 (&ol)[U], const u32 (&il)[U], u32 round) {
   const u32 etag = C.etag;
   const u64 ep = (u64)C.epoch << 32;
   u32 slot[U];
@@ -677,8 +674,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (on[u] && !fast[u])
-        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], round, slot[u], key[u], vck[u],
-                          vg[u], vinfo[u]);
+        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], ol[u], il[u], round, slot[u],
+                          key[u], vck[u], vg[u], vinfo[u]);
   } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) fast[u] = on[u];
@@ -710,7 +707,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     if (rflags[u] & ROW_EPS) C.eps_list[ep_at++] = rows[u]; // next round's epsilon frontier
     C.flog_state[rows[u]] = d[u] | rflags[u];
     C.flog_ck[rows[u]] = ck[u];
-    C.flog_aux[rows[u]] = make_uint2(aux_src(src[u], rflags[u]), g[u]);
+    C.flog_aux[rows[u]] = make_uint4(aux_src(src[u], rflags[u]), g[u], ol[u], il[u]);
     ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
   }
   u64 r0[U], r1[U];
@@ -849,7 +846,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, round);
+      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
     }
     __syncthreads();
   }
@@ -878,19 +875,6 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   __syncthreads();
 }
 
-// Labels of a global arc id (olabel, ilabel).
-__device__ __forceinline__ void arc_labels(const DecodeParams &P, u32 g, u32 &ol, u32 &il) {
-  if (P.arc_meta32) {
-    const u32 m = __ldg(&P.arc_meta32[g]);
-    ol = m & 0xFFFFu;
-    il = (m >> 16) & 0x7FFFu;
-  } else {
-    const int2 m = __ldg(&P.arc_meta[g]);
-    ol = (u32)m.x;
-    il = (u32)m.y & ~META_DEST_EPS;
-  }
-}
-
 // Provenance of a surviving frontier row (decoder.py:385-393, 289-295): walks
 // the row's source links back to the token of the previous frame (rows below
 // sh.emit_end are the emitting pass's, their source is a token index) or to
@@ -909,13 +893,12 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   u32 nrec = 0, il = 0;
   u32 cur = row;
   while (true) {
-    const uint2 ax = C.flog_aux[cur];
+    const uint4 ax = C.flog_aux[cur];
     if (ax.y == G_START) break;
     hits += (ax.x & AUX_BOOST) ? 1 : 0;
     nrec += (ax.x & AUX_HASOL) ? 1u : 0u;
     if (cur < emit_end) {
-      u32 ol;
-      arc_labels(P, ax.y & G_MASK, ol, il);
+      il = ax.w;
       base = prev_tok[ax.x & AUX_SRC];
       break;
     }
@@ -936,12 +919,10 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
     u32 k = nrec;
     cur = row;
     while (k) {
-      const uint2 ax = C.flog_aux[cur];
+      const uint4 ax = C.flog_aux[cur];
       if (ax.x & AUX_HASOL) {
-        u32 ol, il2;
-        arc_labels(P, ax.y & G_MASK, ol, il2);
         --k;
-        C.arena[r0 + k] = make_int2((int)ol, k ? (int)(r0 + k - 1) : base.bp);
+        C.arena[r0 + k] = make_int2((int)ax.z, k ? (int)(r0 + k - 1) : base.bp);
       }
       if (cur < emit_end) break;
       cur = ax.x & AUX_SRC;
@@ -1341,9 +1322,9 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     acc.min_ck = ~0ull;
     acc.n_new = acc.n_app = 0;
     const bool on1[1] = {true};
-    const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS};
+    const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
-    relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, 0u);
+    relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, z1, z1, 0u);
     sh.n_kill = 0;
     sh.emit_end = 0;
     sh.min_ck = cost_key(0.0);
