@@ -274,7 +274,7 @@ def test_context_switch_per_segment():
 
 
 def test_g_large_subset():
-    """C3/C5 graph (5M states / 20M arcs, hashed token table): a channel subset
+    """C3/C5 graph (5M states / 20M arcs, direct token table): a channel subset
     against the oracle."""
     import paper_2306_15685_b200 as ab
     from paper_2306_15685_b200 import synth
@@ -306,3 +306,41 @@ def test_margin_suite_on_device():
             got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
             assert got == expect_hyps(u[key]), (u["utt_id"], key)
         assert res.hypotheses[-1].words == u["transcript"]
+
+
+def test_hashed_token_table_matches_reference(small_cases, monkeypatch):
+    """The hashed token table (graphs whose direct table does not fit the
+    memory budget): forced with table_slots < num_states, so linear probing,
+    key claims and slot collisions are exercised; same golden fixtures and
+    oracle as the direct table."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import device, synth
+
+    n_hashed = 0
+    for c in small_cases[:200]:
+        csr, scores, ctx, cfg = case_inputs(c)
+        if csr.num_states < 3:
+            continue
+        # fewer slots than states selects the hashed table (rounded up to a power of two)
+        monkeypatch.setattr(device, "DEFAULT_CAPACITY", device.Capacity(table_slots=csr.num_states - 1))
+        n_hashed += 1
+        res, ch = _decode(csr, scores, ctx, cfg)
+        e = c["expect"]
+        if e["error"] is not None:
+            assert res.error is not None, c["name"]
+            continue
+        assert res.error is None, (c["name"], res.error)
+        got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
+        assert got == expect_hyps(e), c["name"]
+        assert len(ch.store) == e["store_len"], c["name"]
+    assert n_hashed > 100
+    monkeypatch.setattr(device, "DEFAULT_CAPACITY", device.Capacity(table_slots=16384))
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 1, num_labels=2000)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=5)
+    scores = synth.channel_scores(7, 0, 40, 2000)
+    res, ch = _decode(csr, scores, ctx, cfg)
+    assert res.error is None, res.error
+    want, rc, info = _oracle(csr, scores, ctx, cfg)
+    assert rc == 0
+    _same(res.hypotheses, want, "G_small hashed")
