@@ -23,6 +23,8 @@
 //   live frontier rows --prune (beam, exact top-k radix select)--> token list
 //   survivors --resolve (source links)--> provenance + emission records
 #pragma once
+#include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -371,6 +373,19 @@ __device__ __forceinline__ void block_argmin(u64 &key, u32 &state, int &idx, u64
   __syncthreads();
 }
 
+// Reservation of n consecutive entries on a shared counter, aggregated over
+// the lanes that are converged here (one shared atomic per group): the
+// entries of a warp are contiguous, so its stores to them coalesce.
+__device__ __forceinline__ u32 agg_reserve(u32 *counter, u32 n) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group grp = cg::coalesced_threads();
+  const u32 excl = cg::exclusive_scan(grp, n, cg::plus<u32>());
+  const u32 total = grp.shfl(excl + n, grp.size() - 1);
+  u32 base = 0;
+  if (grp.thread_rank() == 0 && total) base = atomicAdd(counter, total);
+  return grp.shfl(base, 0) + excl;
+}
+
 // warp-aggregated append to a shared counter: one smem atomic per warp.
 // Must be reached by every lane of the warp (pred may differ).
 __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
@@ -688,7 +703,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     nw += want[u] ? 1u : 0u;
   }
   if (!nw) return;
-  u32 row = atomicAdd(&sh.flog_n, nw);
+  u32 row = agg_reserve(&sh.flog_n, nw);
   if (row + nw > P.flog_cap) {
     set_error(sh, E_CAP);
     return;
@@ -697,7 +712,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   u32 ne = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
-  u32 ep_at = ne ? atomicAdd(&sh.eps_n, ne) : 0u;
+  u32 ep_at = agg_reserve(&sh.eps_n, ne);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
