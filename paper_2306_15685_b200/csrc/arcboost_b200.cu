@@ -113,7 +113,9 @@ struct ab_decoder {
   int *d_packw = nullptr;
   long long *d_packoff = nullptr; // [2n]
   size_t stage_cap = 0;
-  void *d_stage = nullptr;
+  void *d_stage = nullptr; // two chunk buffers of host score rows (end-to-end path)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   int last_launches = 0;
@@ -548,6 +550,9 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   for (void *p : ptrs) cudaFree(p);
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
+  for (auto e : d->ev_copy)
+    if (e) cudaEventDestroy(e);
+  if (d->copy_stream) cudaStreamDestroy(d->copy_stream);
   delete d;
 }
 
@@ -799,6 +804,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.tok_cap = d->tok_cap;
   P.flog_state = d->flog_state;
   P.flog_ck = d->flog_ck;
+  P.final_chunk = 1;
   P.flog_aux = d->flog_aux;
   P.eps_list = d->eps_list;
   P.tok_info_alt = d->tok_info_alt;
@@ -814,6 +820,10 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.path_words = d->path_words;
   P.path_cap = d->path_cap;
 }
+
+#ifndef AB_STAGE_CHUNKS
+#define AB_STAGE_CHUNKS 4 // host-score chunks per ab_decode call (copy/decode overlap)
+#endif
 
 static size_t dyn_smem_max() { return CTX_SMEM_WORDS * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
 
@@ -953,15 +963,52 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   cudaStream_t st = a->stream ? (cudaStream_t)a->stream : g->stream;
   const bool s64 = a->scores_dtype == AB_F64;
   const size_t esz = s64 ? 8 : 4;
-  const void *scores = a->scores;
+  (void)rows;
   int rc;
-  if (!a->scores_on_device) {
-    // e2e path: host rows -> device staging inside the call
-    size_t need = (size_t)rows * g->L * esz;
-    if ((rc = grow((unsigned char **)&d->d_stage, d->stage_cap, need, d->bytes))) return rc;
-    if (need) CK(cudaMemcpyAsync(d->d_stage, a->scores, need, cudaMemcpyHostToDevice, st));
-    scores = d->d_stage;
+  // Host scores (the end-to-end path): frames [f0, f0 + Tc) of every channel
+  // are staged chunk by chunk into two device buffers on a copy stream; the
+  // copy of chunk c + 1 overlaps the decode of chunk c.  Utterances continue
+  // across chunks; only the last chunk finalizes (decoder.py:498-501).
+  const bool host = !a->scores_on_device;
+  int K = 1;
+  int64_t Tc = maxT;
+  if (host && maxT > 0) {
+    K = (int)std::min<int64_t>(maxT, AB_STAGE_CHUNKS);
+    Tc = (maxT + K - 1) / K;
   }
+  const size_t rowb = (size_t)g->L * esz;
+  const size_t bufsz = host ? (size_t)n * (size_t)Tc * rowb : 0;
+  if (host) {
+    if ((rc = grow((unsigned char **)&d->d_stage, d->stage_cap, 2 * std::max<size_t>(bufsz, 1), d->bytes)))
+      return rc;
+    if (!d->copy_stream) CK(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
+    for (auto &e : d->ev_copy)
+      if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  long long stride = n > 1 ? soff[1] - soff[0] : 0;
+  bool uniform = true;
+  for (int i = 1; i < n && uniform; ++i) uniform = soff[i] - soff[i - 1] == stride;
+  auto stage = [&](int c) -> int {
+    unsigned char *dst = (unsigned char *)d->d_stage + (size_t)(c & 1) * bufsz;
+    const unsigned char *src = (const unsigned char *)a->scores;
+    const int64_t f0 = (int64_t)c * Tc;
+    bool full = uniform && stride >= 0;
+    for (int i = 0; i < n && full; ++i) full = frames[i] - f0 >= Tc;
+    if (full && n > 0) {
+      CK(cudaMemcpy2DAsync(dst, Tc * rowb, src + ((size_t)soff[0] + (size_t)f0 * g->L) * esz,
+                           std::max<size_t>((size_t)stride * esz, Tc * rowb), Tc * rowb, n,
+                           cudaMemcpyHostToDevice, d->copy_stream));
+    } else {
+      for (int i = 0; i < n; ++i) {
+        const int64_t fr = std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), Tc);
+        if (fr > 0)
+          CK(cudaMemcpyAsync(dst + (size_t)i * Tc * rowb, src + ((size_t)soff[i] + (size_t)f0 * g->L) * esz,
+                             (size_t)fr * rowb, cudaMemcpyHostToDevice, d->copy_stream));
+      }
+    }
+    CK(cudaEventRecord(d->ev_copy[c & 1], d->copy_stream));
+    return AB_OK;
+  };
   if ((rc = ensure_batch(d, n))) return rc;
   const int stream_mode = a->mode == AB_MODE_STREAM;
   const int hyp_stride = stream_mode ? 2 * (int)std::min<int64_t>(maxT, 1 << 20) + 2 : 1;
@@ -971,7 +1018,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     return rc;
   DecodeParams P;
   fill_params(d, P);
-  P.scores = scores;
+  P.scores = a->scores;
   P.mode = a->mode;
   P.beam = cf.beam;
   P.max_active = cf.max_active;
@@ -991,16 +1038,34 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   P.frames = d->d_frames;
   P.score_off = d->d_soff;
   const size_t smem = dyn_smem(g->L, s64);
-  // active set: channels with frames left (all, on the first launch)
-  std::vector<int> act(n);
-  for (int i = 0; i < n; ++i) act[i] = i;
-  std::vector<int> remaining = frames;
-  std::vector<long long> cur_off = soff;
+  std::vector<int> act;
+  std::vector<int> remaining(n);
+  std::vector<long long> cur_off(n);
   std::vector<int> hn, he, hd;
   std::vector<long long> hw, hoffs;
   std::vector<DevHyp> ph;
   std::vector<int> pw;
   float total_ms = 0.f;
+  if (host && (rc = stage(0))) return rc;
+  for (int c = 0; c < K; ++c) {
+  const int64_t f0 = (int64_t)c * Tc;
+  const bool last = c == K - 1;
+  P.final_chunk = last ? 1 : 0;
+  if (host) {
+    CK(cudaStreamWaitEvent(st, d->ev_copy[c & 1], 0));
+    P.scores = (const unsigned char *)d->d_stage + (size_t)(c & 1) * bufsz;
+  }
+  // active set: channels with frames in this chunk (every channel in the last
+  // chunk: a stream ends with its final hypothesis)
+  act.clear();
+  for (int i = 0; i < n; ++i) {
+    if (d->res_err[i]) continue;
+    const int64_t fr = host ? std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), Tc) : frames[i];
+    if (fr > 0 || last) act.push_back(i);
+    remaining[i] = (int)fr;
+    cur_off[i] = host ? (long long)i * Tc * g->L : soff[i];
+  }
+  bool staged_next = !host || last;
   while (!act.empty()) {
     const int m = (int)act.size();
     std::vector<int> ls(m), lf(m);
@@ -1039,6 +1104,10 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     if (le != cudaSuccess) return fail(AB_ERR_CUDA, "decode launch: %s", cudaGetErrorString(le));
     d->last_launches += 1;
     CK(cudaEventRecord(d->ev1, st));
+    if (!staged_next) { // next chunk's copy runs under this launch
+      if ((rc = stage(c + 1))) return rc;
+      staged_next = true;
+    }
     // pack + read back
     hn.resize(m);
     he.resize(m);
@@ -1102,6 +1171,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       if (remaining[i] > 0) next.push_back(i);
     }
     act.swap(next);
+  }
   }
   d->last_ms = total_ms;
 #ifdef AB_PROFILE

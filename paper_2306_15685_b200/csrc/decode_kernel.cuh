@@ -237,6 +237,7 @@ struct DecodeParams {
   const long long *score_off;
   const void *scores;
   int mode;
+  int final_chunk; // stream mode: the frames of this launch end the streams (finalize)
   // config (decoder.py:33-48)
   double beam;
   int max_active, max_eps, partial_every, endpoint_silence_frames, silence_ilabel;
@@ -1720,7 +1721,7 @@ __global__ void __launch_bounds__(BLOCK, AB_MINB)
       PROF_MARK(sh, PF_HYP);
     }
     const bool done = t == T;
-    if (P.mode == AB_MODE_STREAM && !sh.error && done) {
+    if (P.mode == AB_MODE_STREAM && !sh.error && done && P.final_chunk) {
       if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(P, C, sh, n_out++);
       __syncthreads();
       if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
