@@ -101,7 +101,7 @@ struct ab_decoder {
   int *path_rec = nullptr, *path_words = nullptr;
   // per-call buffers (grown on demand)
   size_t batch_cap = 0;
-  int *d_slots = nullptr, *d_frames = nullptr, *d_nhyps = nullptr, *d_errors = nullptr,
+  int *d_slots = nullptr, *d_frames = nullptr, *d_sframes = nullptr, *d_nhyps = nullptr, *d_errors = nullptr,
       *d_done = nullptr;
   long long *d_soff = nullptr, *d_wused = nullptr;
   size_t hyps_cap = 0;
@@ -544,7 +544,7 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
                   d->flog_state, d->flog_ck,  d->flog_aux, d->eps_list, d->tok_info_alt, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
-                  d->d_slots,   d->d_frames,  d->d_nhyps,   d->d_errors, d->d_done,
+                  d->d_slots,   d->d_frames,  d->d_sframes, d->d_nhyps,   d->d_errors, d->d_done,
                   d->d_soff,    d->d_wused,   d->d_hyps,    d->d_words,  d->d_packh,
                   d->d_packw,   d->d_packoff, d->d_stage, d->d_infos, d->d_islots};
   for (void *p : ptrs) cudaFree(p);
@@ -757,6 +757,7 @@ static int ensure_batch(ab_decoder *d, size_t n) {
   if (n <= d->batch_cap) return AB_OK;
   cudaFree(d->d_slots);
   cudaFree(d->d_frames);
+  cudaFree(d->d_sframes);
   cudaFree(d->d_nhyps);
   cudaFree(d->d_errors);
   cudaFree(d->d_done);
@@ -766,6 +767,7 @@ static int ensure_batch(ab_decoder *d, size_t n) {
   size_t nc = std::max<size_t>(n, 64);
   CK(cudaMalloc(&d->d_slots, nc * sizeof(int)));
   CK(cudaMalloc(&d->d_frames, nc * sizeof(int)));
+  CK(cudaMalloc(&d->d_sframes, nc * sizeof(int)));
   CK(cudaMalloc(&d->d_nhyps, nc * sizeof(int)));
   CK(cudaMalloc(&d->d_errors, nc * sizeof(int)));
   CK(cudaMalloc(&d->d_done, nc * sizeof(int)));
@@ -992,12 +994,12 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     unsigned char *dst = (unsigned char *)d->d_stage + (size_t)(c & 1) * bufsz;
     const unsigned char *src = (const unsigned char *)a->scores;
     const int64_t f0 = (int64_t)c * Tc;
-    bool full = uniform && stride >= 0;
+    // one 2D copy when the channels' rows are equally strided and disjoint
+    bool full = uniform && stride >= Tc * (int64_t)g->L;
     for (int i = 0; i < n && full; ++i) full = frames[i] - f0 >= Tc;
     if (full && n > 0) {
       CK(cudaMemcpy2DAsync(dst, Tc * rowb, src + ((size_t)soff[0] + (size_t)f0 * g->L) * esz,
-                           std::max<size_t>((size_t)stride * esz, Tc * rowb), Tc * rowb, n,
-                           cudaMemcpyHostToDevice, d->copy_stream));
+                           (size_t)stride * esz, Tc * rowb, n, cudaMemcpyHostToDevice, d->copy_stream));
     } else {
       for (int i = 0; i < n; ++i) {
         const int64_t fr = std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), Tc);
@@ -1036,6 +1038,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   P.words_used = d->d_wused;
   P.slots = d->d_slots;
   P.frames = d->d_frames;
+  P.stream_frames = d->d_sframes;
   P.score_off = d->d_soff;
   const size_t smem = dyn_smem(g->L, s64);
   std::vector<int> act;
@@ -1068,13 +1071,15 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   bool staged_next = !host || last;
   while (!act.empty()) {
     const int m = (int)act.size();
-    std::vector<int> ls(m), lf(m);
+    std::vector<int> ls(m), lf(m), lt(m);
     std::vector<long long> lo(m);
     for (int j = 0; j < m; ++j) {
       ls[j] = slots[act[j]];
       lf[j] = remaining[act[j]];
+      lt[j] = frames[act[j]];
       lo[j] = cur_off[act[j]];
     }
+    CK(cudaMemcpyAsync(d->d_sframes, lt.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d->d_slots, ls.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d->d_frames, lf.data(), m * sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d->d_soff, lo.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));

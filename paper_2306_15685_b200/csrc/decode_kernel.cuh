@@ -233,7 +233,8 @@ struct DecodeParams {
   // batch
   int n;
   const int *slots;
-  const int *frames;
+  const int *frames;        // frames of this launch
+  const int *stream_frames; // frames of the whole ab_decode call (chunked host staging)
   const long long *score_off;
   const void *scores;
   int mode;
@@ -1722,7 +1723,8 @@ __global__ void __launch_bounds__(BLOCK, AB_MINB)
     }
     const bool done = t == T;
     if (P.mode == AB_MODE_STREAM && !sh.error && done && P.final_chunk) {
-      if (cs->info.frame_index > 0 || T == 0) finalize<BLOCK>(P, C, sh, n_out++);
+      // decoder.py:498-501: final hypothesis if frames were consumed or the stream is empty
+      if (cs->info.frame_index > 0 || P.stream_frames[b] == 0) finalize<BLOCK>(P, C, sh, n_out++);
       __syncthreads();
       if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
     }
