@@ -91,8 +91,7 @@ struct ab_decoder {
   u32 *flog_state = nullptr;
   u64 *flog_ck = nullptr;
   uint4 *flog_aux = nullptr;
-  u32 *eps_list = nullptr;
-  TokInfo *tok_info_alt = nullptr;
+  uint4 *eps_list = nullptr;
   u32 *app_list = nullptr;
   u64 *scr_key = nullptr;
   u32 *scr_row = nullptr;
@@ -449,7 +448,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
     const uint64_t tk = std::min<uint64_t>(S, MAX_TOKENS);
     const uint64_t fl = cap.frontier_rows > 0 ? (uint64_t)cap.frontier_rows : std::max<uint64_t>(65536, 2 * tk);
     const uint64_t ar = cap.arena_records > 0 ? (uint64_t)cap.arena_records : std::max<uint64_t>(1ull << 19, 8 * fl);
-    const double per_ch_other = (double)tk * (4 + 8 + 16 + 16) + (double)fl * (4 + 8 + 16 + 4 + 4 + 8 + 4) +
+    const double per_ch_other = (double)tk * (4 + 8 + 16 + 16) + (double)fl * (4 + 8 + 16 + 16 + 4 + 8 + 4) +
                                 (double)ar * (2 * 8 + 2 * 4.0 / 32);
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
@@ -496,11 +495,11 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   if (dmalloc(&d->chans, C, acc) || (hslots && dmalloc(&d->table, hslots, acc)) ||
       (dslots && dmalloc(&d->vals, 2 * dslots, acc)) ||
       dmalloc(&d->tok_state, C * d->tok_cap, acc) || dmalloc(&d->tok_cost, C * d->tok_cap, acc) ||
-      dmalloc(&d->tok_info, C * d->tok_cap, acc) ||
+      dmalloc(&d->tok_info, 2 * C * d->tok_cap, acc) ||
       dmalloc(&d->flog_state, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_aux, C * d->flog_cap, acc) || dmalloc(&d->eps_list, C * d->flog_cap, acc) ||
-      dmalloc(&d->tok_info_alt, C * d->tok_cap, acc) ||
+
       dmalloc(&d->app_list, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
@@ -541,7 +540,7 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   if (!d) return;
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->vals, d->tok_state, d->tok_cost, d->tok_info,
-                  d->flog_state, d->flog_ck,  d->flog_aux, d->eps_list, d->tok_info_alt, d->app_list,
+                  d->flog_state, d->flog_ck,  d->flog_aux, d->eps_list, d->app_list,
                   d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_sframes, d->d_nhyps,   d->d_errors, d->d_done,
@@ -730,8 +729,11 @@ extern "C" int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, dou
   if (states) CK(cudaMemcpy(states, d->tok_state + base, m * sizeof(u32), cudaMemcpyDeviceToHost));
   if (costs) CK(cudaMemcpy(costs, d->tok_cost + base, m * sizeof(double), cudaMemcpyDeviceToHost));
   if (hits) {
+    ChanState cs;
+    CK(cudaMemcpy(&cs, d->chans + ch, sizeof(ChanState), cudaMemcpyDeviceToHost));
+    const size_t tbase = (2 * (size_t)ch + (cs.tok_half & 1u)) * d->tok_cap;
     std::vector<TokInfo> ti(m);
-    CK(cudaMemcpy(ti.data(), d->tok_info + base, m * sizeof(TokInfo), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ti.data(), d->tok_info + tbase, m * sizeof(TokInfo), cudaMemcpyDeviceToHost));
     for (int i = 0; i < m; ++i) hits[i] = ti[i].hits;
   }
   return AB_OK;
@@ -809,7 +811,6 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.final_chunk = 1;
   P.flog_aux = d->flog_aux;
   P.eps_list = d->eps_list;
-  P.tok_info_alt = d->tok_info_alt;
   P.flog_cap = d->flog_cap;
   P.app_list = d->app_list;
   P.scr_key = d->scr_key;

@@ -63,9 +63,12 @@ constexpr u32 ROW_STATE = 0x07FFFFFFu;
 // provenance walk reads one 8-byte word per step
 constexpr u32 AUX_BOOST = 0x80000000u;
 constexpr u32 AUX_HASOL = 0x40000000u;
-constexpr u32 AUX_SRC = 0x3FFFFFFFu;
-__device__ __forceinline__ u32 aux_src(u32 src, u32 rflags) {
-  return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u);
+constexpr u32 AUX_START = 0x20000000u; // the utterance-start row (no source arc)
+constexpr u32 AUX_SRC = 0x1FFFFFFFu;
+constexpr u32 NO_EPS = 0xFFFFFFFFu;    // aux.y of a row that is not in the epsilon-frontier list
+__device__ __forceinline__ u32 aux_src(u32 src, u32 rflags, u32 g) {
+  return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u) |
+         (g == G_START ? AUX_START : 0u);
 }
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
@@ -182,7 +185,8 @@ struct ChanState {
   int max_depth;  // deepest token path in the current token list
   int arena_half; // which half of the channel's arena is live (copying GC)
   u32 rec_phys;   // records physically in the live half
-  u32 pad[3];
+  u32 tok_half;   // which half of the channel's token-provenance buffer is current
+  u32 pad[2];
 };
 
 struct DevHyp {
@@ -216,10 +220,10 @@ struct DecodeParams {
   u32 tok_cap;
   u32 *flog_state;
   u64 *flog_ck;
-  uint4 *flog_aux; // {source | AUX flags, arc id | G_DEST_EPS, olabel, ilabel} per frontier row
-  u32 *eps_list;   // [channel][flog_cap] rows whose state has epsilon arcs, in write order
+  uint4 *flog_aux; // {source | AUX flags, epsilon-list position, olabel, ilabel} per frontier row
+  uint4 *eps_list; // [channel][flog_cap] {row, state | flags, cost key}: rows whose state has
+                   // epsilon arcs, in write order (the next round's frontier)
   u32 flog_cap;
-  TokInfo *tok_info_alt;
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_row;
@@ -476,8 +480,8 @@ template <typename F, typename S> struct Chan {
   u32 *flog_state;
   u64 *flog_ck;
   uint4 *flog_aux;
-  u32 *eps_list;
-  TokInfo *tok_info_alt;
+  uint4 *eps_list;
+  TokInfo *tok_info_alt; // the other half of the channel's provenance buffer
   u32 *app_list;
   u64 *scr_key;
   u32 *scr_row;
@@ -592,11 +596,13 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
 // candidate that stops being better marks its own row displaced.
 template <typename F, typename S>
 __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
-                            u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row) {
+                            u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row,
+                            u32 eps_pos) {
   const u32 etag = C.etag;
   while (true) {
     if (!value_better(ck, g, round, etag, vck, vg, vinfo)) {
       atomicOr(&C.flog_state[row], ROW_DISP);
+      if (eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
       return;
     }
     const u32 old_info = vinfo;
@@ -641,10 +647,14 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   }
   C.flog_state[row] = d | rflags;
   C.flog_ck[row] = ck;
-  C.flog_aux[row] = make_uint4(aux_src(src, rflags), g, lab_ol, lab_il);
-  if (rflags & ROW_EPS) C.eps_list[atomicAdd(&sh.eps_n, 1u)] = row;
+  u32 epos = NO_EPS;
+  if (rflags & ROW_EPS) {
+    epos = atomicAdd(&sh.eps_n, 1u);
+    C.eps_list[epos] = make_uint4(row, d | rflags, (u32)ck, (u32)(ck >> 32));
+  }
+  C.flog_aux[row] = make_uint4(aux_src(src, rflags, g), epos, lab_ol, lab_il);
   const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
-  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row);
+  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos);
 }
 
 // Relaxation of U independent candidates of one thread.  Every memory step
@@ -710,7 +720,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     set_error(sh, E_CAP);
     return;
   }
-  u32 rows[U], ninfo[U];
+  u32 rows[U], ninfo[U], eps_pos[U];
   u32 ne = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
@@ -719,12 +729,16 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
     ninfo[u] = 0;
+    eps_pos[u] = NO_EPS;
     if (!want[u]) continue;
     rows[u] = row++;
-    if (rflags[u] & ROW_EPS) C.eps_list[ep_at++] = rows[u]; // next round's epsilon frontier
+    if (rflags[u] & ROW_EPS) { // next round's epsilon frontier
+      eps_pos[u] = ep_at++;
+      C.eps_list[eps_pos[u]] = make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32));
+    }
     C.flog_state[rows[u]] = d[u] | rflags[u];
     C.flog_ck[rows[u]] = ck[u];
-    C.flog_aux[rows[u]] = make_uint4(aux_src(src[u], rflags[u]), g[u], ol[u], il[u]);
+    C.flog_aux[rows[u]] = make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]);
     ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
   }
   u64 r0[U], r1[U];
@@ -740,7 +754,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
       installed(P, C, sh, acc, round, etag, vinfo[u], ck[u]);
     else
       relax_retry(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
-                  (u32)(r1[u] >> 32), rows[u]);
+                  (u32)(r1[u] >> 32), rows[u], eps_pos[u]);
   }
 }
 
@@ -755,7 +769,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 //      thread in flight: arc-record loads, candidates (boost lookup fused
 //      into the cost add), one batched relaxation.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
-__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const u32 *list, u32 n_in,
+__device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const uint4 *list, u32 n_in,
                        u32 round) {
   constexpr u32 TILE = BLOCK * Q;
   u32 *t_a0 = C.t_a0;
@@ -773,16 +787,32 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
+    if (EMIT) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) idx[q] = i0 + q < n_in ? (EMIT ? i0 + q : list[i0 + q]) : 0xFFFFFFFFu;
+      for (int q = 0; q < Q; ++q) idx[q] = i0 + q < n_in ? i0 + q : 0xFFFFFFFFu;
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
-      st[q] = idx[q] == 0xFFFFFFFFu ? ROW_DISP : (EMIT ? C.tok_state[idx[q]] : C.flog_state[idx[q]]);
+      for (int q = 0; q < Q; ++q) st[q] = idx[q] == 0xFFFFFFFFu ? ROW_DISP : C.tok_state[idx[q]];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const u32 j = (u32)tid * Q + q;
-      t_src[j] = idx[q];
-      if (idx[q] != 0xFFFFFFFFu) t_cost[j] = EMIT ? C.tok_cost[idx[q]] : key_cost(C.flog_ck[idx[q]]);
+      for (int q = 0; q < Q; ++q) {
+        const u32 j = (u32)tid * Q + q;
+        t_src[j] = idx[q];
+        if (idx[q] != 0xFFFFFFFFu) t_cost[j] = C.tok_cost[idx[q]];
+      }
+    } else {
+      // epsilon-frontier entries carry the row's state, flags and cost
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const u32 j = (u32)tid * Q + q;
+        idx[q] = 0xFFFFFFFFu;
+        st[q] = ROW_DISP;
+        if (i0 + q < n_in) {
+          const uint4 e = list[i0 + q];
+          idx[q] = e.x;
+          st[q] = e.y;
+          t_cost[j] = key_cost(((u64)e.w << 32) | e.z);
+        }
+        t_src[j] = idx[q];
+      }
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -885,7 +915,12 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   const u32 n = min(sh.n_kill, P.flog_cap);
   for (u32 i = threadIdx.x; i < n; i += BLOCK) {
     const u32 v = C.app_list[i];
-    atomicOr(&C.flog_state[v & VROW_MASK], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    const u32 row = v & VROW_MASK;
+    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    if (v & KILL_DISP) { // a displaced row leaves the epsilon frontier too
+      const u32 ep = C.flog_aux[row].y;
+      if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) sh.n_kill = 0;
@@ -911,7 +946,7 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   u32 cur = row;
   while (true) {
     const uint4 ax = C.flog_aux[cur];
-    if (ax.y == G_START) break;
+    if (ax.x & AUX_START) break;
     hits += (ax.x & AUX_BOOST) ? 1 : 0;
     nrec += (ax.x & AUX_HASOL) ? 1u : 0u;
     if (cur < emit_end) {
@@ -985,8 +1020,9 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
 
 
 // Provenance of a new token list (token i comes from frontier row rows[i]):
-// resolve_row per token into tok_info_alt (the previous list's provenance is
-// still read through tok_info), then copied over tok_info.
+// resolve_row per token into the idle half of the provenance buffer (the
+// previous list's provenance is still read through tok_info), then the halves
+// swap.
 template <int BLOCK, typename F, typename S>
 __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 n_tok,
                               const u32 *rows, int best_row) {
@@ -1005,10 +1041,14 @@ __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared
   }
   atomicMax(&sh.max_depth, md);
   __syncthreads();
-  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) C.tok_info[i] = C.tok_info_alt[i];
   if (threadIdx.x == 0) {
     C.cs->max_depth = sh.max_depth;
     C.cs->info.num_active = (int)n_tok;
+    C.cs->tok_half ^= 1u;
+    Chan<F, S> &M = const_cast<Chan<F, S> &>(C);
+    TokInfo *t = M.tok_info;
+    M.tok_info = M.tok_info_alt;
+    M.tok_info_alt = t;
   }
   __syncthreads();
 }
@@ -1584,12 +1624,12 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.vals = P.vals ? P.vals + 2 * s * P.table_cap : nullptr;
     C.tok_state = P.tok_state + s * P.tok_cap;
     C.tok_cost = P.tok_cost + s * P.tok_cap;
-    C.tok_info = P.tok_info + s * P.tok_cap;
+    C.tok_info = P.tok_info + (2 * s + (C.cs->tok_half & 1u)) * P.tok_cap;
+    C.tok_info_alt = P.tok_info + (2 * s + ((C.cs->tok_half & 1u) ^ 1u)) * P.tok_cap;
     C.flog_state = P.flog_state + s * P.flog_cap;
     C.flog_ck = P.flog_ck + s * P.flog_cap;
     C.flog_aux = P.flog_aux + s * P.flog_cap;
     C.eps_list = P.eps_list + s * P.flog_cap;
-    C.tok_info_alt = P.tok_info_alt + s * P.tok_cap;
     C.app_list = P.app_list + s * P.flog_cap;
     C.scr_key = P.scr_key + s * P.flog_cap;
     C.scr_row = P.scr_row + s * P.flog_cap;
