@@ -41,6 +41,10 @@ sys.path.insert(0, str(ROOT))
 
 L = 2000
 CTX_POOL = 256
+# BASELINE.json metric: value = decoded frames/s with biasing; the biasing
+# overhead and the expand kernel's GB/s are the "biasing_overhead" and
+# "roofline" objects of the same line
+METRIC = "decoded frames/sec with biasing; biasing overhead %; arc-expand HBM GB/s"
 
 
 def parse():
@@ -59,6 +63,8 @@ def parse():
     p.add_argument("--no-overhead", action="store_true", help="skip the unbiased / zero-discount runs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
+    p.add_argument("--c4-kind", choices=["words", "arcs"], default="words",
+                   help="c4 contexts: unigram word sets (density x L words) or uniform random arcs")
     return p.parse_args()
 
 
@@ -209,15 +215,18 @@ def hbm_peak():
 
 # ------------------------------------------------------------------ workload
 
-def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense=None):
+def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense=None, kind="words"):
     from paper_2306_15685_b200 import synth
 
     t0 = time.time()
     csr = synth.benchmark_graph(W["states"], 4, L, seed=421, f32_weights=True)
     pool = []
     if want_contexts:
-        if dense is not None:
+        if dense is not None and kind == "arcs":
             pool = [synth.dense_context(csr, dense, 2000 + i) for i in range(8)]
+        elif dense is not None:
+            pool = synth.unigram_contexts(csr, max(1, int(round(dense * L))), range(2000, 2008),
+                                          num_labels=L)
         else:
             n_pool = CTX_POOL if W["channels"] > 1 else 1
             pool = synth.unigram_contexts(csr, 20, range(1000, 1000 + n_pool), num_labels=L)
@@ -278,7 +287,8 @@ def run_b200(args, W, world, rank, local):
     Tseg = T // S
     assert Tseg * S == T
     dense = args.density if args.workload == "c4" else None
-    csr, pool, scores_np, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense)
+    csr, pool, scores_np, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense,
+                                              kind=args.c4_kind)
     cfg = ab.DecoderConfig(beam=13.0, max_active=7000, max_epsilon_expansion=20,
                            partial_every=W["partial_every"])
     t0 = time.time()
@@ -388,7 +398,7 @@ def run_b200(args, W, world, rank, local):
                          "random_cas_ceiling_Gops_s": pref.get("random_cas_Gops_s"),
                          "source": pref.get("ncu_source")}
     result = {
-        "metric": "decoded frames/sec with biasing (1024-channel biased config, C3)",
+        "metric": METRIC,
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 accumulate (f32 weights/scores)",
@@ -462,7 +472,7 @@ def run_reference(args, W, world, rank):
         f_all += nfr
     v = f_all / t_all
     return {
-        "metric": "decoded frames/sec with biasing (1024-channel biased config, C3)",
+        "metric": METRIC,
         "value": v, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_all / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
