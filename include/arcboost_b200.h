@@ -185,6 +185,20 @@ int ab_finalize(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words, int32_t 
 int ab_last_kernel_ms(ab_decoder *d, float *ms);
 int ab_last_launch_count(ab_decoder *d, int32_t *launches);
 
+/* Paper Alg. 1 (biasing.py:174-285 find_boost_arcs / compile_context): the
+   arc indices a context boosts for a batch of word-label entities over the
+   host CSR (row_offsets[num_states + 1], olabels / next_states[num_arcs]).
+   Entity e is labels[ent_offsets[e] .. ent_offsets[e + 1]).  ent_status[e] =
+   1 compiled, 0 unmatched, -1 invalid (empty or containing epsilon).  The
+   sorted union is written to out_arcs (at most out_cap; *n_out = its size,
+   call again with a larger buffer if *n_out > out_cap).  CPU, num_threads
+   threads (0 = all). */
+int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,
+                       const int32_t *olabels, const int32_t *next_states, int32_t n_entities,
+                       const int64_t *ent_offsets, const int32_t *labels,
+                       int32_t max_epsilon_depth, int32_t num_threads, int64_t *out_arcs,
+                       int64_t out_cap, int64_t *n_out, int32_t *ent_status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,12 +30,14 @@ from .decoder import (
     partial_hypothesis,
     switch_context,
 )
+from .compiler import BoostCompileConfig, compile_context, find_boost_arcs
 from .device import BatchDecoder, Capacity, DeviceGraph, device_graph
 from .fst import EPSILON, Arc, CsrFst, Fst, build_csr, csr_from_arrays, parse_text_fst
 from .scores import ScoreMatrix
 
 __all__ = [
-    "EPSILON", "Arc", "BatchDecoder", "BiasingCompileError", "BiasingContext", "Capacity",
+    "EPSILON", "Arc", "BatchDecoder", "BiasingCompileError", "BiasingContext", "BoostCompileConfig",
+    "Capacity", "compile_context", "find_boost_arcs",
     "Channel", "ChannelResult", "ChannelStatus", "ContextRegistry", "CsrFst", "DecodeError",
     "DecoderConfig", "DeviceGraph", "Fst", "Hypothesis", "ScoreMatrix", "UnknownContextError",
     "advance_frame", "build_csr", "csr_from_arrays", "decode_batch", "detect_endpoint",

@@ -134,6 +134,8 @@ SIGNATURES = {
     "ab_channels_init": (_I32, [_P, _I32, _P, _P]),
     "ab_channels_set_context": (_I32, [_P, _I32, _P, _P]),
     "ab_channels_get": (_I32, [_P, _I32, _P, _P]),
+    "ab_compile_context": (_I32, [_I32, _I64, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I64,
+                                  C.POINTER(_I64), _P]),
 }
 
 _lib = None

@@ -5,9 +5,9 @@ to them (biasing.py:320-349).
 On the device every registered context becomes an entry of the context store
 (shared-memory sorted list for sparse contexts, HBM bitset for dense ones), so
 a per-channel context switch is a handle swap.  Compiling entity lists into
-arc indices (paper Alg. 1, biasing.py:174-285) is not part of the decode path
-and is not provided here; contexts compiled by the reference (or by any tool)
-are accepted as-is, including via ``BiasingContext.from_json_dict``.
+arc indices (paper Alg. 1, biasing.py:174-285) is ``compiler.py`` (native);
+contexts compiled by the reference (or by any tool) are accepted as-is,
+including via ``BiasingContext.from_json_dict``.
 """
 
 from __future__ import annotations

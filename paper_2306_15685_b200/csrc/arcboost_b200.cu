@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "context_compiler.h"
 #include "decode_kernel.cuh"
 
 using namespace ab;
@@ -1294,6 +1295,36 @@ extern "C" int ab_partial(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words
 extern "C" int ab_finalize(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words,
                            int32_t words_cap) {
   return one_hyp(d, ch, AB_FINAL, hyp, words, words_cap);
+}
+
+extern "C" int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,
+                                  const int32_t *olabels, const int32_t *next_states,
+                                  int32_t n_entities, const int64_t *ent_offsets,
+                                  const int32_t *labels, int32_t max_epsilon_depth,
+                                  int32_t num_threads, int64_t *out_arcs, int64_t out_cap,
+                                  int64_t *n_out, int32_t *ent_status) {
+  if (num_states < 1 || num_arcs < 0 || !row_offsets || (num_arcs && (!olabels || !next_states)))
+    return fail(AB_ERR_INVALID, "invalid graph arrays");
+  if (n_entities < 0 || (n_entities && (!ent_offsets || !ent_status)) || !n_out)
+    return fail(AB_ERR_INVALID, "invalid entity arrays");
+  if (max_epsilon_depth < 0) return fail(AB_ERR_INVALID, "max_epsilon_depth must be >= 0");
+  if (row_offsets[0] != 0 || row_offsets[num_states] != num_arcs)
+    return fail(AB_ERR_INVALID, "row_offsets must start at 0 and end at num_arcs");
+  for (int64_t a = 0; a < num_arcs; ++a)
+    if (olabels[a] < 0 || next_states[a] < 0 || next_states[a] >= num_states)
+      return fail(AB_ERR_INVALID, "arc %lld: label or next state out of range", (long long)a);
+  for (int32_t e = 0; e < n_entities; ++e)
+    if (ent_offsets[e + 1] < ent_offsets[e]) return fail(AB_ERR_INVALID, "entity offsets decrease");
+  ab::CompileGraph G{num_states, num_arcs, row_offsets, olabels, next_states};
+  G.index();
+  int32_t threads = num_threads > 0 ? num_threads : (int32_t)std::max(1u, std::thread::hardware_concurrency());
+  const std::vector<int64_t> all = ab::compile_entities(G, n_entities, ent_offsets, labels,
+                                                        max_epsilon_depth, threads, ent_status);
+  *n_out = (int64_t)all.size();
+  if (out_arcs)
+    std::copy(all.begin(), all.begin() + std::min<int64_t>((int64_t)all.size(), std::max<int64_t>(out_cap, 0)),
+              out_arcs);
+  return AB_OK;
 }
 
 extern "C" int ab_last_kernel_ms(ab_decoder *d, float *ms) {
