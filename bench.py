@@ -366,8 +366,10 @@ def run_b200(args, W, world, rank, local):
     # zero-discount contexts (identical search, lookup cost only)
     bias = {}
     if not args.no_overhead:
-        t_none, _ = timed(1, variant="none")
-        t_zero, _ = timed(1, variant="zero")
+        step(variant="none")
+        t_none = timed(args.steps, variant="none")[0] / args.steps
+        step(variant="zero")
+        t_zero = timed(args.steps, variant="zero")[0] / args.steps
         t_bias = ms / args.steps
         bias = {"unbiased_ms_per_step": t_none, "zero_discount_ms_per_step": t_zero,
                 "biased_ms_per_step": t_bias,

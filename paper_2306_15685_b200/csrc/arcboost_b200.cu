@@ -831,13 +831,23 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
 
 static size_t dyn_smem_max() { return CTX_SMEM_WORDS * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
 
+// CTA size per batch: few channels get more threads each (a channel's frame
+// is one CTA's work), many channels fill the SMs with 256-thread CTAs.
 static int pick_block(int n) {
   const char *env = getenv("AB_BLOCK");
   if (env) {
     int b = atoi(env);
-    if (b == 256) return b;
+    if (b == 256 || b == 512 || b == 1024) return b;
   }
-  (void)n;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+  }
+  if (n <= sms) return 1024;
+  if (n <= 2 * sms) return 512;
   return 256;
 }
 
@@ -871,6 +881,8 @@ template <typename F, typename S>
 static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, size_t smem,
                                    cudaStream_t st) {
   switch (block) {
+  case 512: return launch_decode<512, F, S>(P, grid, smem, st);
+  case 1024: return launch_decode<1024, F, S>(P, grid, smem, st);
   default: return launch_decode<256, F, S>(P, grid, smem, st);
   }
 }

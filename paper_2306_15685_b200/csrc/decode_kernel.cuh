@@ -1689,7 +1689,7 @@ template <int BLOCK, typename F, typename S>
 #ifndef AB_MINB
 #define AB_MINB 4
 #endif
-__global__ void __launch_bounds__(BLOCK, AB_MINB)
+__global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB * 256 / BLOCK) : 1)
     decode_kernel(const __grid_constant__ DecodeParams P) {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
