@@ -1124,28 +1124,91 @@ __device__ u64 radix_select(Shared &sh, u32 *hist, u32 n, KeyFn keyf, u64 lo, u6
 }
 
 // _prune (decoder.py:319-334) + _best_token_pos (337-338) + silence
-// bookkeeping (400-407) over the live rows of the frame's frontier log.
-//   scan:   rows QP per thread (loads first), live and within the beam ->
-//           compacted (cost key, row, state) by block scan;
-//   select: if more than max_active survive, exact top-k by (cost, state):
-//           radix select on the cost keys, then on states for ties;
-//   output: survivors -> token list (provenance gathered QP per thread).
+// bookkeeping (400-407) over the live rows of the frame's frontier log, in two
+// passes over the rows (state, cost key):
+//   1. live rows within the beam: count, emission records, best token, and a
+//      histogram of the first radix digit of their cost keys (below the
+//      highest bit where best and best + beam differ);
+//   2. if more than max_active are within the beam, the digit bucket holding
+//      the max_active-th key splits them: rows below it survive, rows in it
+//      are set aside; otherwise every row within the beam survives.
+// The set-aside bucket (typically a few hundred rows) is resolved exactly by
+// (cost, state) with radix selects over its keys and then its states.
 template <int BLOCK, typename F, typename S>
 __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   constexpr int QP = PRUNE_Q;
   constexpr u32 TILE = BLOCK * QP;
-  // the digit histogram lives in the expansion tile (BLOCK * EXP_Q words)
+  // digit histograms live in the expansion tile (BLOCK * EXP_Q words)
   constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : (BLOCK * EXP_Q >= 1024) ? 10 : (BLOCK * EXP_Q >= 512) ? 9 : 8;
   const int tid = threadIdx.x;
   const u32 n_rows = sh.flog_n;
   const u64 best_ck = sh.min_ck;
-  const double thr = key_cost(best_ck) + P.beam;
-  const u64 thr_ck = cost_key(thr);
-  u32 *scr_state = C.app_list; // the applied-slot list is free until the next frame
+  const u64 thr_ck = cost_key(key_cost(best_ck) + P.beam);
+  u32 *hist = C.t_a0;
+  u32 *scr_state = C.app_list; // the kill queue is free until the next frame
+  // first digit: bits [lowbit, pos] of keys in [best, thr] (higher bits are shared)
+  const int pos = best_ck == thr_ck ? 0 : 63 - __clzll(best_ck ^ thr_ck);
+  const int lowbit = pos >= DB - 1 ? pos - (DB - 1) : 0;
+  const u32 nbk = 1u << (pos - lowbit + 1);
+  const u64 prefix = pos >= 63 ? 0ull : (best_ck & ~((1ull << (pos + 1)) - 1));
+  for (u32 b = tid; b < nbk; b += BLOCK) hist[b] = 0;
+  if (tid == 0) sh.n_keep = 0;
+  __syncthreads();
   u64 bk = ~0ull;
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
-  u32 n_keep = 0, n_rec = 0;
+  u32 n_in = 0, n_rec = 0;
+  for (u32 i0 = (u32)tid * QP; i0 < n_rows; i0 += TILE) {
+    u32 st[QP];
+    u64 ck[QP];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      n_rec += (st[q] & (ROW_DISP | ROW_HASOL)) == ROW_HASOL ? 1u : 0u;
+      if ((st[q] & (ROW_DEAD | ROW_DISP)) || ck[q] > thr_ck) continue;
+      ++n_in;
+      atomicAdd(&hist[(ck[q] >> lowbit) & (nbk - 1)], 1u);
+      const u32 s = st[q] & ROW_STATE;
+      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
+    }
+  }
+  if (n_rec) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec); // emission records (store_len)
+  if (n_in) atomicAdd(&sh.n_keep, n_in);
+  __syncthreads();
+  PROF_MARK(sh, PF_PRUNE_SCAN);
+  const u32 n_keep = sh.n_keep;
+  block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
+  const bool select = n_keep > (u32)P.max_active;
+  u64 key_lo = ~0ull, key_hi = ~0ull; // select: rows below key_lo survive, [key_lo, key_hi] set aside
+  u32 need = 0;
+  if (select) {
+    const u32 want = (u32)P.max_active;
+    const u32 per = (nbk + BLOCK - 1) / BLOCK;
+    const u32 b0 = min((u32)tid * per, nbk), b1 = min(b0 + per, nbk);
+    u32 lsum = 0;
+    for (u32 b = b0; b < b1; ++b) lsum += hist[b];
+    u32 total;
+    const u32 excl = block_excl_scan<BLOCK>(lsum, total, sh.scan);
+    if (excl < want && want <= excl + lsum) {
+      u32 cum = excl, b = b0;
+      for (; b < b1; ++b) {
+        if (cum + hist[b] >= want) break;
+        cum += hist[b];
+      }
+      sh.sel = b;
+      sh.cum = cum;
+    }
+    __syncthreads();
+    key_lo = prefix | ((u64)sh.sel << lowbit);
+    key_hi = key_lo | ((1ull << lowbit) - 1);
+    need = want - sh.cum;
+  }
+  // pass 2: survivors -> token list; the split bucket -> set aside (members)
+  u32 n_tok = 0, n_mem = 0;
+  u32 *mem_row = C.scr_row + P.flog_cap; // members' rows grow down from the top of scr_row
   for (u32 base = 0; base < n_rows; base += TILE) {
     const u32 i0 = base + (u32)tid * QP;
     u32 st[QP];
@@ -1154,84 +1217,85 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
 #pragma unroll
     for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
-    u32 cnt = 0;
+    u32 ns = 0, nm = 0;
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      cnt += (!(st[q] & (ROW_DEAD | ROW_DISP)) && ck[q] <= thr_ck) ? 1u : 0u;
-      n_rec += (st[q] & (ROW_DISP | ROW_HASOL)) == ROW_HASOL ? 1u : 0u;
+      const bool in = !(st[q] & (ROW_DEAD | ROW_DISP)) && ck[q] <= thr_ck;
+      ns += (in && ck[q] < key_lo) ? 1u : 0u;
+      nm += (in && select && ck[q] >= key_lo && ck[q] <= key_hi) ? 1u : 0u;
     }
-    u32 total;
-    u32 p = n_keep + block_excl_scan<BLOCK>(cnt, total, sh.scan);
+    u32 tot_s, tot_m;
+    u32 ps = n_tok + block_excl_scan<BLOCK>(ns, tot_s, sh.scan);
+    u32 pm = n_mem + block_excl_scan<BLOCK>(nm, tot_m, sh.scan);
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
       if ((st[q] & (ROW_DEAD | ROW_DISP)) || ck[q] > thr_ck) continue;
       const u32 s = st[q] & ROW_STATE;
-      C.scr_key[p] = ck[q];
-      C.scr_row[p] = i0 + q;
-      scr_state[p] = s;
-      ++p;
-      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
+      if (ck[q] < key_lo) {
+        C.tok_state[ps] = s;
+        C.tok_cost[ps] = key_cost(ck[q]);
+        C.scr_row[ps] = i0 + q;
+        ++ps;
+      } else if (select && ck[q] <= key_hi) {
+        C.scr_key[pm] = ck[q];
+        scr_state[pm] = s;
+        *(mem_row - 1 - pm) = i0 + q;
+        ++pm;
+      }
     }
-    n_keep += total;
-  }
-  if (n_rec) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec); // emission records (store_len)
-  __syncthreads();
-  PROF_MARK(sh, PF_PRUNE_SCAN);
-  block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
-  u64 tc = ~0ull;
-  u32 ts = 0xFFFFFFFFu;
-  if (n_keep > (u32)P.max_active) {
-    u32 need = (u32)P.max_active;
-    u32 *hist = C.t_a0;
-    auto kf = [&](u32 i, bool &ok) -> u64 {
-      ok = true;
-      return C.scr_key[i];
-    };
-    bool exact;
-    tc = radix_select<BLOCK, 8, DB>(sh, hist, n_keep, kf, best_ck, thr_ck, need, exact);
-    if (exact) {
-      // ties at the threshold cost: the smallest states survive
-      auto sf = [&](u32 i, bool &ok) -> u64 {
-        const u64 k = C.scr_key[i];
-        const u32 s = scr_state[i];
-        ok = k == tc;
-        return (u64)s;
-      };
-      bool exact2;
-      ts = (u32)radix_select<BLOCK, 8, DB>(sh, hist, n_keep, sf, 0ull, 0xFFFFFFFFull, need, exact2);
-    }
+    n_tok += tot_s;
+    n_mem += tot_m;
   }
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_SEL);
-  u32 n_tok = 0;
-  for (u32 base = 0; base < n_keep; base += TILE) {
-    const u32 i0 = base + (u32)tid * QP;
-    u64 ck[QP];
-    u32 row[QP], s[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_keep ? C.scr_key[i0 + q] : ~0ull;
-#pragma unroll
-    for (int q = 0; q < QP; ++q) row[q] = i0 + q < n_keep ? C.scr_row[i0 + q] : 0u;
-#pragma unroll
-    for (int q = 0; q < QP; ++q) s[q] = i0 + q < n_keep ? scr_state[i0 + q] : 0xFFFFFFFFu;
-    bool keep[QP];
-    u32 cnt = 0;
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      keep[q] = i0 + q < n_keep && (ck[q] < tc || (ck[q] == tc && s[q] <= ts));
-      cnt += keep[q] ? 1u : 0u;
+  if (select && need > 0) {
+    if (n_tok + n_mem + need > P.flog_cap) { // survivors' rows would reach the set-aside rows
+      if (tid == 0) set_error(sh, E_CAP);
+      __syncthreads();
+      return;
     }
-    u32 total;
-    u32 p = n_tok + block_excl_scan<BLOCK>(cnt, total, sh.scan);
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      if (!keep[q]) continue;
-      C.tok_state[p] = s[q];
-      C.tok_cost[p] = key_cost(ck[q]);
-      C.scr_row[p] = row[q]; // survivors' rows in token order (p <= the slot just read)
-      ++p;
+    // exact (cost, state) order inside the bucket
+    u64 tc = ~0ull;
+    u32 ts = 0xFFFFFFFFu;
+    if (n_mem > need) {
+      u32 nd = need;
+      auto kf = [&](u32 i, bool &ok) -> u64 {
+        ok = true;
+        return C.scr_key[i];
+      };
+      bool exact;
+      tc = radix_select<BLOCK, 8, DB>(sh, hist, n_mem, kf, key_lo, key_hi, nd, exact);
+      if (exact) { // ties at the threshold cost: the smallest states survive
+        auto sf = [&](u32 i, bool &ok) -> u64 {
+          const u64 k = C.scr_key[i];
+          const u32 s = scr_state[i];
+          ok = k == tc;
+          return (u64)s;
+        };
+        bool exact2;
+        ts = (u32)radix_select<BLOCK, 8, DB>(sh, hist, n_mem, sf, 0ull, 0xFFFFFFFFull, nd, exact2);
+      }
     }
-    n_tok += total;
+    for (u32 base = 0; base < n_mem; base += BLOCK) {
+      const u32 m = base + tid;
+      bool keep = false;
+      u64 k = 0;
+      u32 s = 0, r = 0;
+      if (m < n_mem) {
+        k = C.scr_key[m];
+        s = scr_state[m];
+        r = *(mem_row - 1 - m);
+        keep = k < tc || (k == tc && s <= ts);
+      }
+      u32 total;
+      const u32 p = n_tok + block_excl_scan<BLOCK>(keep ? 1u : 0u, total, sh.scan);
+      if (keep) {
+        C.tok_state[p] = s;
+        C.tok_cost[p] = key_cost(k);
+        C.scr_row[p] = r;
+      }
+      n_tok += total;
+    }
   }
   __syncthreads();
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, bi);
