@@ -927,11 +927,12 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   __syncthreads();
 }
 
-// Provenance of a surviving frontier row (decoder.py:385-393, 289-295): walks
-// the row's source links back to the token of the previous frame (rows below
-// sh.emit_end are the emitting pass's, their source is a token index) or to
-// the utterance start, then appends the emission records of the path's arcs
-// with olabel != 0, oldest first, and returns the token's provenance.
+// Provenance of a surviving frontier row (decoder.py:385-393, 289-295): one
+// walk over the row's source links back to the token of the previous frame
+// (rows below sh.emit_end are the emitting pass's; their source is a token
+// index) or to the utterance start.  Each arc with olabel != 0 on the way
+// gets an emission record; a record is written once the next older record of
+// the chain is known, so the chain is walked only once.
 template <typename F, typename S>
 __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 row,
                                const TokInfo *prev_tok) {
@@ -941,14 +942,25 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   base.hits = 0;
   base.last_il = 0;
   const u32 emit_end = sh.emit_end;
-  int hits = 0;
-  u32 nrec = 0, il = 0;
+  int hits = 0, nrec = 0, newest = -1, pend = -1;
+  u32 pend_ol = 0, il = 0;
   u32 cur = row;
   while (true) {
     const uint4 ax = C.flog_aux[cur];
     if (ax.x & AUX_START) break;
     hits += (ax.x & AUX_BOOST) ? 1 : 0;
-    nrec += (ax.x & AUX_HASOL) ? 1u : 0u;
+    if (ax.x & AUX_HASOL) {
+      const u32 r = atomicAdd(&sh.rec_n, 1u);
+      if (r >= P.arena_cap) {
+        set_error(sh, E_CAP);
+        break;
+      }
+      if (pend >= 0) C.arena[pend] = make_int2((int)pend_ol, (int)r); // r is the older record
+      else newest = (int)r;
+      pend = (int)r;
+      pend_ol = ax.z;
+      ++nrec;
+    }
     if (cur < emit_end) {
       il = ax.w;
       base = prev_tok[ax.x & AUX_SRC];
@@ -956,30 +968,12 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
     }
     cur = ax.x & AUX_SRC;
   }
+  if (pend >= 0) C.arena[pend] = make_int2((int)pend_ol, base.bp);
   TokInfo t;
   t.hits = base.hits + hits;
-  t.depth = base.depth + (int)nrec;
+  t.depth = base.depth + nrec;
   t.last_il = (int)il;
-  t.bp = base.bp;
-  if (nrec) {
-    const u32 r0 = atomicAdd(&sh.rec_n, nrec);
-    if (r0 + nrec > P.arena_cap) {
-      set_error(sh, E_CAP);
-      return t;
-    }
-    t.bp = (int)(r0 + nrec - 1);
-    u32 k = nrec;
-    cur = row;
-    while (k) {
-      const uint4 ax = C.flog_aux[cur];
-      if (ax.x & AUX_HASOL) {
-        --k;
-        C.arena[r0 + k] = make_int2((int)ax.z, k ? (int)(r0 + k - 1) : base.bp);
-      }
-      if (cur < emit_end) break;
-      cur = ax.x & AUX_SRC;
-    }
-  }
+  t.bp = newest >= 0 ? newest : base.bp;
   return t;
 }
 
@@ -1372,7 +1366,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
 }
 
 // Copying collector for the emission arena: records reachable from the token
-// list move to the other half in arena order (ids stay monotone), everything
+// list move to the other half, keeping their relative order, everything
 // else (records of pruned or superseded tokens) is dropped.  Words never
 // change: only record ids do, so the prefix-sharing path is reset.
 template <int BLOCK, typename F, typename S>
