@@ -31,7 +31,9 @@ enum {
   AB_ERR_STATUS = 4,       /* lifecycle misuse (decoder.py:352-353, 430-433) */
   AB_ERR_CAPACITY = 5,     /* a device capacity (token table, arena, output) was exceeded */
   AB_ERR_UNKNOWN_CTX = 6,  /* UnknownContextError (biasing.py:27) */
-  AB_ERR_WIDTH = 7         /* frame width != emitting-label count (decoder.py:354-359) */
+  AB_ERR_WIDTH = 7,        /* frame width != emitting-label count (decoder.py:354-359) */
+  AB_ERR_PARSE = 8,        /* FstParseError (fst.py:24): malformed graph text */
+  AB_ERR_STRUCTURE = 9     /* FstStructureError (fst.py:28) */
 };
 
 enum { AB_IDLE = 0, AB_DECODING = 1, AB_ENDPOINTED = 2, AB_FINISHED = 3 };
@@ -53,6 +55,7 @@ enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2, AB_CTX_LABELS = 3 };
 enum { AB_MAX_TOKENS = 131072, AB_MAX_HASH_SLOTS = 4194304, AB_MAX_EPSILON_ROUNDS = 63 };
 
 typedef struct ab_graph ab_graph;
+typedef struct ab_fst ab_fst; /* a parsed graph on the host (state-major CSR) */
 typedef struct ab_decoder ab_decoder;
 
 /* DecoderConfig (decoder.py:33-48). */
@@ -193,6 +196,22 @@ int ab_last_launch_count(ab_decoder *d, int32_t *launches);
    sorted union is written to out_arcs (at most out_cap; *n_out = its size,
    call again with a larger buffer if *n_out > out_cap).  CPU, num_threads
    threads (0 = all). */
+/* Graph ingest (fst.py:165-275 parse_text_fst + build_csr + _fingerprint):
+   OpenFst-style text -> host CSR.  ab_fst_parse parses a text buffer;
+   ab_fst_load parses a file and, with use_cache, reads / writes a binary
+   cache at cache_path (reused while the source's size and mtime match).
+   num_states_hint < 0 = none.  AB_ERR_PARSE / AB_ERR_STRUCTURE carry the
+   reference's messages.  ab_fst_arrays copies the CSR out (arrays sized from
+   ab_fst_info); ab_graph_create_from_fst uploads it directly. */
+int ab_fst_parse(const char *text, int64_t len, int64_t num_states_hint, ab_fst **out);
+int ab_fst_load(const char *path, int64_t num_states_hint, int32_t use_cache, const char *cache_path,
+                int32_t *cache_hit, ab_fst **out);
+int ab_fst_info(const ab_fst *f, int32_t *start, int64_t *num_states, int64_t *num_arcs,
+                int32_t *num_finals, char *fingerprint65);
+int ab_fst_arrays(const ab_fst *f, int64_t *row_offsets, int32_t *ilabels, int32_t *olabels,
+                  int32_t *next_states, double *weights, int32_t *final_states, double *final_costs);
+void ab_fst_destroy(ab_fst *f);
+int ab_graph_create_from_fst(int32_t device, const ab_fst *f, ab_graph **out);
 int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,
                        const int32_t *olabels, const int32_t *next_states, int32_t n_entities,
                        const int64_t *ent_offsets, const int32_t *labels,

@@ -23,6 +23,8 @@ AB_ERR_STATUS = 4
 AB_ERR_CAPACITY = 5
 AB_ERR_UNKNOWN_CTX = 6
 AB_ERR_WIDTH = 7
+AB_ERR_PARSE = 8
+AB_ERR_STRUCTURE = 9
 
 AB_IDLE, AB_DECODING, AB_ENDPOINTED, AB_FINISHED = 0, 1, 2, 3
 AB_PARTIAL, AB_FINAL = 0, 1
@@ -134,6 +136,13 @@ SIGNATURES = {
     "ab_channels_init": (_I32, [_P, _I32, _P, _P]),
     "ab_channels_set_context": (_I32, [_P, _I32, _P, _P]),
     "ab_channels_get": (_I32, [_P, _I32, _P, _P]),
+    "ab_fst_parse": (_I32, [C.c_char_p, _I64, _I64, C.POINTER(_P)]),
+    "ab_fst_load": (_I32, [C.c_char_p, _I64, _I32, C.c_char_p, C.POINTER(_I32), C.POINTER(_P)]),
+    "ab_fst_info": (_I32, [_P, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32),
+                           C.c_char_p]),
+    "ab_fst_arrays": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "ab_fst_destroy": (None, [_P]),
+    "ab_graph_create_from_fst": (_I32, [_I32, _P, C.POINTER(_P)]),
     "ab_compile_context": (_I32, [_I32, _I64, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I64,
                                   C.POINTER(_I64), _P]),
 }

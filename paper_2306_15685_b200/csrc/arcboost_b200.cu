@@ -14,7 +14,10 @@
 #include <string>
 #include <vector>
 
+#include <sys/stat.h>
+
 #include "context_compiler.h"
+#include "graph_ingest.h"
 #include "decode_kernel.cuh"
 
 using namespace ab;
@@ -1307,6 +1310,100 @@ extern "C" int ab_partial(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words
 extern "C" int ab_finalize(ab_decoder *d, int32_t ch, ab_hyp *hyp, int32_t *words,
                            int32_t words_cap) {
   return one_hyp(d, ch, AB_FINAL, hyp, words, words_cap);
+}
+
+struct ab_fst {
+  ab::HostFst F;
+};
+
+extern "C" int ab_fst_parse(const char *text, int64_t len, int64_t num_states_hint, ab_fst **out) {
+  if (!out || (!text && len)) return fail(AB_ERR_INVALID, "null argument");
+  *out = nullptr;
+  ab_fst *f = new ab_fst();
+  std::string err;
+  const int rc = ab::parse_text_fst(text ? text : "", (size_t)std::max<int64_t>(len, 0), num_states_hint, f->F, err);
+  if (rc) {
+    delete f;
+    return fail(rc == 1 ? AB_ERR_PARSE : AB_ERR_STRUCTURE, "%s", err.c_str());
+  }
+  *out = f;
+  return AB_OK;
+}
+
+extern "C" int ab_fst_load(const char *path, int64_t num_states_hint, int32_t use_cache, const char *cache_path,
+                           int32_t *cache_hit, ab_fst **out) {
+  if (!path || !out) return fail(AB_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (cache_hit) *cache_hit = 0;
+  struct stat st;
+  if (stat(path, &st) != 0) return fail(AB_ERR_INVALID, "cannot stat %s", path);
+  const int64_t mtime = (int64_t)st.st_mtim.tv_sec * 1000000000ll + st.st_mtim.tv_nsec;
+  ab_fst *f = new ab_fst();
+  if (use_cache && cache_path && num_states_hint < 0 && ab::load_cache(cache_path, f->F, (int64_t)st.st_size, mtime)) {
+    if (cache_hit) *cache_hit = 1;
+    *out = f;
+    return AB_OK;
+  }
+  FILE *fp = fopen(path, "rb");
+  if (!fp) {
+    delete f;
+    return fail(AB_ERR_INVALID, "cannot open %s", path);
+  }
+  std::vector<char> buf((size_t)st.st_size);
+  const size_t got = buf.empty() ? 0 : fread(buf.data(), 1, buf.size(), fp);
+  fclose(fp);
+  if (got != buf.size()) {
+    delete f;
+    return fail(AB_ERR_INVALID, "short read of %s", path);
+  }
+  std::string err;
+  const int rc = ab::parse_text_fst(buf.data(), buf.size(), num_states_hint, f->F, err);
+  if (rc) {
+    delete f;
+    return fail(rc == 1 ? AB_ERR_PARSE : AB_ERR_STRUCTURE, "%s", err.c_str());
+  }
+  if (use_cache && cache_path && num_states_hint < 0) ab::save_cache(cache_path, f->F, (int64_t)st.st_size, mtime);
+  *out = f;
+  return AB_OK;
+}
+
+extern "C" int ab_fst_info(const ab_fst *f, int32_t *start, int64_t *num_states, int64_t *num_arcs,
+                           int32_t *num_finals, char *fingerprint65) {
+  if (!f) return fail(AB_ERR_INVALID, "null fst");
+  if (start) *start = f->F.start;
+  if (num_states) *num_states = f->F.num_states;
+  if (num_arcs) *num_arcs = (int64_t)f->F.il.size();
+  if (num_finals) *num_finals = (int32_t)f->F.fstate.size();
+  if (fingerprint65) {
+    memcpy(fingerprint65, f->F.fingerprint.data(), 64);
+    fingerprint65[64] = 0;
+  }
+  return AB_OK;
+}
+
+extern "C" int ab_fst_arrays(const ab_fst *f, int64_t *row_offsets, int32_t *ilabels, int32_t *olabels,
+                             int32_t *next_states, double *weights, int32_t *final_states, double *final_costs) {
+  if (!f) return fail(AB_ERR_INVALID, "null fst");
+  const ab::HostFst &F = f->F;
+  if (row_offsets) std::copy(F.ro.begin(), F.ro.end(), row_offsets);
+  if (ilabels) std::copy(F.il.begin(), F.il.end(), ilabels);
+  if (olabels) std::copy(F.ol.begin(), F.ol.end(), olabels);
+  if (next_states) std::copy(F.ns.begin(), F.ns.end(), next_states);
+  if (weights) std::copy(F.w.begin(), F.w.end(), weights);
+  if (final_states) std::copy(F.fstate.begin(), F.fstate.end(), final_states);
+  if (final_costs) std::copy(F.fcost.begin(), F.fcost.end(), final_costs);
+  return AB_OK;
+}
+
+extern "C" void ab_fst_destroy(ab_fst *f) { delete f; }
+
+extern "C" int ab_graph_create_from_fst(int32_t device, const ab_fst *f, ab_graph **out) {
+  if (!f || !out) return fail(AB_ERR_INVALID, "null argument");
+  const ab::HostFst &F = f->F;
+  if (F.num_states > INT32_MAX) return fail(AB_ERR_INVALID, "too many states");
+  return ab_graph_create(device, F.start, (int32_t)F.num_states, (int64_t)F.il.size(), F.ro.data(), F.il.data(),
+                         F.ol.data(), F.ns.data(), F.w.data(), (int32_t)F.fstate.size(), F.fstate.data(),
+                         F.fcost.data(), out);
 }
 
 extern "C" int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,

@@ -25,6 +25,14 @@ class FstError(ValueError):
     """Malformed graph input."""
 
 
+class FstParseError(FstError):
+    """Malformed graph or symbol-table text (reference fst.py:24)."""
+
+
+class FstStructureError(FstError):
+    """Structurally invalid graph (reference fst.py:28)."""
+
+
 @dataclass(frozen=True)
 class Arc:
     ilabel: int
@@ -193,3 +201,82 @@ def parse_text_fst(text: str | Iterable[str]) -> Fst:
     for s, a in arcs_in:
         adj[s].append(a)
     return Fst(start=start, num_states=top + 1, arcs=adj, finals=finals)
+
+
+# --------------------------------------------------------------- native ingest
+def _native_fst(handle) -> CsrFst:
+    """CsrFst from a native ab_fst handle (the handle is destroyed)."""
+    import ctypes as C
+
+    from . import _lib
+
+    lib = _lib.load()
+    try:
+        start = C.c_int32()
+        S = C.c_int64()
+        A = C.c_int64()
+        nf = C.c_int32()
+        fp = C.create_string_buffer(65)
+        _lib.check(lib.ab_fst_info(handle, C.byref(start), C.byref(S), C.byref(A), C.byref(nf), fp))
+        ro = np.empty(S.value + 1, dtype=np.int64)
+        il = np.empty(A.value, dtype=np.int32)
+        ol = np.empty(A.value, dtype=np.int32)
+        ns = np.empty(A.value, dtype=np.int32)
+        w = np.empty(A.value, dtype=np.float64)
+        fs = np.empty(nf.value, dtype=np.int32)
+        fc = np.empty(nf.value, dtype=np.float64)
+        _lib.check(lib.ab_fst_arrays(handle, ro.ctypes.data, il.ctypes.data, ol.ctypes.data,
+                                     ns.ctypes.data, w.ctypes.data, fs.ctypes.data, fc.ctypes.data))
+    finally:
+        lib.ab_fst_destroy(handle)
+    return CsrFst(start=start.value, row_offsets=ro, ilabels=il.astype(np.int64),
+                  olabels=ol.astype(np.int64), next_states=ns.astype(np.int64), weights=w,
+                  finals={int(s): float(c) for s, c in zip(fs, fc)},
+                  _fingerprint=fp.value.decode())
+
+
+def _ingest_call(fn, *args):
+    import ctypes as C
+
+    from . import _lib
+
+    h = C.c_void_p()
+    rc = fn(*args, C.byref(h))
+    if rc == _lib.AB_ERR_PARSE:
+        raise FstParseError(_lib.load().ab_last_error().decode("utf-8", "replace"))
+    if rc == _lib.AB_ERR_STRUCTURE:
+        raise FstStructureError(_lib.load().ab_last_error().decode("utf-8", "replace"))
+    _lib.check(rc)
+    return h.value
+
+
+def parse_text_fst_csr(text: str | bytes, num_states_hint: int | None = None) -> CsrFst:
+    """parse_text_fst + build_csr (reference fst.py:165-275) natively: the
+    state-major CSR and the reference fingerprint straight from the text."""
+    from . import _lib
+
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = _ingest_call(_lib.load().ab_fst_parse, data, len(data),
+                     -1 if num_states_hint is None else int(num_states_hint))
+    return _native_fst(h)
+
+
+def load_fst(path, num_states_hint: int | None = None, cache: bool = True,
+             cache_path=None) -> CsrFst:
+    """Graph file -> CsrFst.  With ``cache`` a binary copy of the CSR is kept
+    next to the file (``<path>.abcsr``) and reused while the file's size and
+    modification time are unchanged."""
+    import ctypes as C
+    import os
+
+    from . import _lib
+
+    path = os.fspath(path)
+    cp = os.fspath(cache_path) if cache_path is not None else path + ".abcsr"
+    hit = C.c_int32()
+    h = _ingest_call(_lib.load().ab_fst_load, path.encode(),
+                     -1 if num_states_hint is None else int(num_states_hint), 1 if cache else 0,
+                     cp.encode(), C.byref(hit))
+    csr = _native_fst(h)
+    csr.cache_hit = bool(hit.value)
+    return csr
