@@ -186,7 +186,7 @@ struct ChanState {
   int arena_half; // which half of the channel's arena is live (copying GC)
   u32 rec_phys;   // records physically in the live half
   u32 tok_half;   // which half of the channel's token-provenance buffer is current
-  u32 pad[2];
+  double prev_best; // best token cost of the previous frame (cost histogram window)
 };
 
 struct DevHyp {
@@ -456,7 +456,11 @@ struct Shared {
   u64 redk[32];
   u32 reds[32];
   int redi[32];
-  u32 hist[256];
+  // live rows of the frame by cost bucket, kept while rows are written and
+  // killed (prune finds its split bucket without a pass over the rows)
+  u32 fhist[1024];
+  double hbase, hscale;
+  int n_rec_frame; // emission records of the frame (olabel != 0 applications)
   u32 n_kill;   // kill queue length of the current round
   u32 eps_n;    // entries in the channel's epsilon-frontier list this frame
   u32 emit_end; // rows below come from the emitting pass (their source is a token)
@@ -507,6 +511,14 @@ template <typename F, typename S> struct Chan {
   u32 *t_src;
   double *t_cost;
 };
+
+constexpr u32 NB_HIST = 1024;
+constexpr double HIST_PER_BEAM = 256.0; // buckets per beam width
+// Cost bucket of the frame's histogram: monotone in the cost, clamped at both ends.
+__device__ __forceinline__ u32 hbucket(const Shared &sh, double c) {
+  const double x = (c - sh.hbase) * sh.hscale;
+  return x <= 0.0 ? 0u : (x >= (double)(NB_HIST - 1) ? NB_HIST - 1 : (u32)x);
+}
 
 // BiasingContext.boosted_mask (biasing.py:108-117) in the representation the
 // context store chose for this context.
@@ -566,6 +578,7 @@ struct RelaxAcc {
   u64 min_ck;  // cheapest installed candidate
   u32 n_new;   // new tokens (capacity check)
   u32 n_app;   // applications (decoder.py:285-287 stop rule)
+  int n_rec;   // rows written with an output label (emission records, net of self-displacement)
 };
 
 // Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
@@ -579,12 +592,16 @@ __device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, 
 // Outcome of a successful CAS that replaced old_info.
 template <typename F, typename S>
 __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
-                                          u32 round, u32 etag, u32 old_info, u64 ck) {
+                                          u32 round, u32 etag, u32 old_info, u64 old_ck, u64 ck) {
   acc.min_ck = min(acc.min_ck, ck);
   if (((old_info >> TAG_SHIFT) & TAG_MASK) != etag) {
     acc.n_new++;
     acc.n_app++;
-  } else if ((old_info >> ROUND_SHIFT) < round) {
+    return;
+  }
+  // the replaced winner's row leaves the live rows (its cost is the CAS's expected key)
+  atomicSub(&sh.fhist[hbucket(sh, key_cost(old_ck))], 1u);
+  if ((old_info >> ROUND_SHIFT) < round) {
     acc.n_app++;
     queue_kill(P, C, sh, old_info & VROW_MASK);
   } else {
@@ -597,17 +614,20 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
 template <typename F, typename S>
 __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
                             u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row,
-                            u32 eps_pos) {
+                            u32 eps_pos, bool hasol) {
   const u32 etag = C.etag;
   while (true) {
     if (!value_better(ck, g, round, etag, vck, vg, vinfo)) {
       atomicOr(&C.flog_state[row], ROW_DISP);
       if (eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
+      atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
+      acc.n_rec -= hasol ? 1 : 0;
       return;
     }
     const u32 old_info = vinfo;
+    const u64 old_ck = vck;
     if (cas_value(v, vck, vg, vinfo, ck, g, info)) {
-      installed(P, C, sh, acc, round, etag, old_info, ck);
+      installed(P, C, sh, acc, round, etag, old_info, old_ck, ck);
       return;
     }
   }
@@ -653,8 +673,11 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     C.eps_list[epos] = make_uint4(row, d | rflags, (u32)ck, (u32)(ck >> 32));
   }
   C.flog_aux[row] = make_uint4(aux_src(src, rflags, g), epos, lab_ol, lab_il);
+  atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
+  acc.n_rec += (rflags & ROW_HASOL) ? 1 : 0;
   const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
-  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos);
+  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos,
+              (rflags & ROW_HASOL) != 0);
 }
 
 // Relaxation of U independent candidates of one thread.  Every memory step
@@ -739,6 +762,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     C.flog_state[rows[u]] = d[u] | rflags[u];
     C.flog_ck[rows[u]] = ck[u];
     C.flog_aux[rows[u]] = make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]);
+    atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
+    acc.n_rec += (rflags[u] & ROW_HASOL) ? 1 : 0;
     ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
   }
   u64 r0[U], r1[U];
@@ -751,10 +776,10 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   for (int u = 0; u < U; ++u) {
     if (!want[u]) continue;
     if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u]))
-      installed(P, C, sh, acc, round, etag, vinfo[u], ck[u]);
+      installed(P, C, sh, acc, round, etag, vinfo[u], vck[u], ck[u]);
     else
       relax_retry(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
-                  (u32)(r1[u] >> 32), rows[u], eps_pos[u]);
+                  (u32)(r1[u] >> 32), rows[u], eps_pos[u], (rflags[u] & ROW_HASOL) != 0);
   }
 }
 
@@ -783,6 +808,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   acc.min_ck = ~0ull;
   acc.n_new = 0;
   acc.n_app = 0;
+  acc.n_rec = 0;
   u32 arcs_seen = 0;
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
@@ -898,6 +924,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     __syncthreads();
   }
   if (acc.min_ck != ~0ull) atomicMin(&sh.min_ck, acc.min_ck);
+  if (acc.n_rec) atomicAdd(&sh.n_rec_frame, acc.n_rec);
   if (acc.n_app) atomicAdd(&sh.n_app, acc.n_app);
   if (acc.n_new && atomicAdd(&sh.n_new, acc.n_new) + acc.n_new > P.tok_cap) set_error(sh, E_CAP);
   if (tid == 0) {
@@ -916,8 +943,9 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   for (u32 i = threadIdx.x; i < n; i += BLOCK) {
     const u32 v = C.app_list[i];
     const u32 row = v & VROW_MASK;
-    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
-    if (v & KILL_DISP) { // a displaced row leaves the epsilon frontier too
+    const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    if (v & KILL_DISP) { // a displaced row is no application (no record) and leaves the epsilon frontier
+      if (old & ROW_HASOL) atomicSub(&sh.n_rec_frame, 1);
       const u32 ep = C.flog_aux[row].y;
       if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
     }
@@ -1118,94 +1146,69 @@ __device__ u64 radix_select(Shared &sh, u32 *hist, u32 n, KeyFn keyf, u64 lo, u6
 }
 
 // _prune (decoder.py:319-334) + _best_token_pos (337-338) + silence
-// bookkeeping (400-407) over the live rows of the frame's frontier log, in two
-// passes over the rows (state, cost key):
-//   1. live rows within the beam: count, emission records, best token, and a
-//      histogram of the first radix digit of their cost keys (below the
-//      highest bit where best and best + beam differ);
-//   2. if more than max_active are within the beam, the digit bucket holding
-//      the max_active-th key splits them: rows below it survive, rows in it
-//      are set aside; otherwise every row within the beam survives.
-// The set-aside bucket (typically a few hundred rows) is resolved exactly by
-// (cost, state) with radix selects over its keys and then its states.
+// bookkeeping (400-407) over the live rows of the frame's frontier log.  The
+// frame's cost histogram (kept while rows were written and killed) gives the
+// bucket holding the max_active-th live row within the beam; one pass over
+// the rows (state, cost key) then takes every live row of a lower bucket
+// (all within the beam) and sets the split bucket's rows within the beam
+// aside (typically a few hundred), which are resolved exactly by (cost,
+// state) with radix selects over their keys and then their states.  Bucket
+// order is cost order, so the result is the exact top max_active.
 template <int BLOCK, typename F, typename S>
 __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   constexpr int QP = PRUNE_Q;
   constexpr u32 TILE = BLOCK * QP;
-  // digit histograms live in the expansion tile (BLOCK * EXP_Q words)
+  // digit histograms of the split-bucket selection live in the expansion tile
   constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : (BLOCK * EXP_Q >= 1024) ? 10 : (BLOCK * EXP_Q >= 512) ? 9 : 8;
   const int tid = threadIdx.x;
   const u32 n_rows = sh.flog_n;
   const u64 best_ck = sh.min_ck;
-  const u64 thr_ck = cost_key(key_cost(best_ck) + P.beam);
-  u32 *hist = C.t_a0;
+  const double thr = key_cost(best_ck) + P.beam;
+  const u64 thr_ck = cost_key(thr);
   u32 *scr_state = C.app_list; // the kill queue is free until the next frame
-  // first digit: bits [lowbit, pos] of keys in [best, thr] (higher bits are shared)
-  const int pos = best_ck == thr_ck ? 0 : 63 - __clzll(best_ck ^ thr_ck);
-  const int lowbit = pos >= DB - 1 ? pos - (DB - 1) : 0;
-  const u32 nbk = 1u << (pos - lowbit + 1);
-  const u64 prefix = pos >= 63 ? 0ull : (best_ck & ~((1ull << (pos + 1)) - 1));
-  for (u32 b = tid; b < nbk; b += BLOCK) hist[b] = 0;
-  if (tid == 0) sh.n_keep = 0;
-  __syncthreads();
-  u64 bk = ~0ull;
-  u32 bs = 0xFFFFFFFFu;
-  int bi = -1;
-  u32 n_in = 0, n_rec = 0;
-  for (u32 i0 = (u32)tid * QP; i0 < n_rows; i0 += TILE) {
-    u32 st[QP];
-    u64 ck[QP];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
-#pragma unroll
-    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      n_rec += (st[q] & (ROW_DISP | ROW_HASOL)) == ROW_HASOL ? 1u : 0u;
-      if ((st[q] & (ROW_DEAD | ROW_DISP)) || ck[q] > thr_ck) continue;
-      ++n_in;
-      atomicAdd(&hist[(ck[q] >> lowbit) & (nbk - 1)], 1u);
-      const u32 s = st[q] & ROW_STATE;
-      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
-    }
-  }
-  if (n_rec) atomicAdd(&sh.rec_logical, (unsigned long long)n_rec); // emission records (store_len)
-  if (n_in) atomicAdd(&sh.n_keep, n_in);
-  __syncthreads();
-  PROF_MARK(sh, PF_PRUNE_SCAN);
-  const u32 n_keep = sh.n_keep;
-  block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
-  const bool select = n_keep > (u32)P.max_active;
-  u64 key_lo = ~0ull, key_hi = ~0ull; // select: rows below key_lo survive, [key_lo, key_hi] set aside
-  u32 need = 0;
-  if (select) {
-    const u32 want = (u32)P.max_active;
-    const u32 per = (nbk + BLOCK - 1) / BLOCK;
-    const u32 b0 = min((u32)tid * per, nbk), b1 = min(b0 + per, nbk);
+  if (tid == 0 && sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
+  // split bucket: the first bucket where the live rows below and in it reach
+  // max_active; buckets below the threshold's bucket are entirely in the beam
+  const u32 bt = hbucket(sh, thr);
+  const u32 want = (u32)P.max_active;
+  {
+    constexpr u32 PER = NB_HIST / BLOCK > 0 ? NB_HIST / BLOCK : 1;
+    const u32 b0 = min((u32)tid * PER, bt + 1), b1 = min(b0 + PER, bt + 1);
     u32 lsum = 0;
-    for (u32 b = b0; b < b1; ++b) lsum += hist[b];
+    for (u32 b = b0; b < b1; ++b) lsum += sh.fhist[b];
     u32 total;
     const u32 excl = block_excl_scan<BLOCK>(lsum, total, sh.scan);
+    if (tid == 0) {
+      sh.sel = bt;
+      sh.cum = 0xFFFFFFFFu; // marks "not reached below bt"
+    }
+    __syncthreads();
     if (excl < want && want <= excl + lsum) {
       u32 cum = excl, b = b0;
       for (; b < b1; ++b) {
-        if (cum + hist[b] >= want) break;
-        cum += hist[b];
+        if (cum + sh.fhist[b] >= want) break;
+        cum += sh.fhist[b];
       }
-      sh.sel = b;
-      sh.cum = cum;
+      if (b < bt) {
+        sh.sel = b;
+        sh.cum = cum;
+      }
     }
     __syncthreads();
-    key_lo = prefix | ((u64)sh.sel << lowbit);
-    key_hi = key_lo | ((1ull << lowbit) - 1);
-    need = want - sh.cum;
   }
-  // pass 2: survivors -> token list; the split bucket -> set aside (members)
+  const u32 split = sh.sel;
+  u32 below = sh.cum; // live rows in buckets < split (when the split is below bt)
+  __syncthreads();
+  // pass over the rows: survivors (bucket < split) -> token list; split
+  // bucket within the beam -> set aside; best (cost, state)
+  u64 bk = ~0ull;
+  u32 bs = 0xFFFFFFFFu;
+  int bi = -1;
   u32 n_tok = 0, n_mem = 0;
-  u32 *mem_row = C.scr_row + P.flog_cap; // members' rows grow down from the top of scr_row
+  u32 *mem_row = C.scr_row + P.flog_cap; // set-aside rows grow down from the top of scr_row
   for (u32 base = 0; base < n_rows; base += TILE) {
     const u32 i0 = base + (u32)tid * QP;
-    u32 st[QP];
+    u32 st[QP], bq[QP];
     u64 ck[QP];
 #pragma unroll
     for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
@@ -1214,23 +1217,25 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     u32 ns = 0, nm = 0;
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      const bool in = !(st[q] & (ROW_DEAD | ROW_DISP)) && ck[q] <= thr_ck;
-      ns += (in && ck[q] < key_lo) ? 1u : 0u;
-      nm += (in && select && ck[q] >= key_lo && ck[q] <= key_hi) ? 1u : 0u;
+      const bool live = !(st[q] & (ROW_DEAD | ROW_DISP));
+      bq[q] = live ? hbucket(sh, key_cost(ck[q])) : NB_HIST;
+      ns += (live && bq[q] < split) ? 1u : 0u;
+      nm += (live && bq[q] == split && ck[q] <= thr_ck) ? 1u : 0u;
     }
     u32 tot_s, tot_m;
     u32 ps = n_tok + block_excl_scan<BLOCK>(ns, tot_s, sh.scan);
     u32 pm = n_mem + block_excl_scan<BLOCK>(nm, tot_m, sh.scan);
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      if ((st[q] & (ROW_DEAD | ROW_DISP)) || ck[q] > thr_ck) continue;
+      if (bq[q] > split || (bq[q] == split && ck[q] > thr_ck)) continue;
       const u32 s = st[q] & ROW_STATE;
-      if (ck[q] < key_lo) {
+      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
+      if (bq[q] < split) {
         C.tok_state[ps] = s;
         C.tok_cost[ps] = key_cost(ck[q]);
         C.scr_row[ps] = i0 + q;
         ++ps;
-      } else if (select && ck[q] <= key_hi) {
+      } else {
         C.scr_key[pm] = ck[q];
         scr_state[pm] = s;
         *(mem_row - 1 - pm) = i0 + q;
@@ -1240,25 +1245,39 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     n_tok += tot_s;
     n_mem += tot_m;
   }
-  __syncthreads();
-  PROF_MARK(sh, PF_PRUNE_SEL);
-  if (select && need > 0) {
+  block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
+  PROF_MARK(sh, PF_PRUNE_SCAN);
+  if (below == 0xFFFFFFFFu) below = n_tok; // split at bt: everything below survives
+  const u32 need = want > below ? want - below : 0u;
+  if (n_mem > need) {
     if (n_tok + n_mem + need > P.flog_cap) { // survivors' rows would reach the set-aside rows
       if (tid == 0) set_error(sh, E_CAP);
       __syncthreads();
       return;
     }
-    // exact (cost, state) order inside the bucket
+    // exact (cost, state) order inside the split bucket
     u64 tc = ~0ull;
     u32 ts = 0xFFFFFFFFu;
-    if (n_mem > need) {
+    if (need > 0) {
       u32 nd = need;
+      u64 lo = ~0ull, hi = 0ull;
+      for (u32 m = tid; m < n_mem; m += BLOCK) {
+        const u64 k = C.scr_key[m];
+        lo = min(lo, k);
+        hi = max(hi, k);
+      }
+      u32 dummy_s = 0;
+      int dummy_i = 0;
+      block_argmin<BLOCK>(lo, dummy_s, dummy_i, sh.redk, sh.reds, sh.redi);
+      u64 nhi = ~hi;
+      block_argmin<BLOCK>(nhi, dummy_s, dummy_i, sh.redk, sh.reds, sh.redi);
+      hi = ~nhi;
       auto kf = [&](u32 i, bool &ok) -> u64 {
         ok = true;
         return C.scr_key[i];
       };
       bool exact;
-      tc = radix_select<BLOCK, 8, DB>(sh, hist, n_mem, kf, key_lo, key_hi, nd, exact);
+      tc = radix_select<BLOCK, 8, DB>(sh, C.t_a0, n_mem, kf, lo, hi, nd, exact);
       if (exact) { // ties at the threshold cost: the smallest states survive
         auto sf = [&](u32 i, bool &ok) -> u64 {
           const u64 k = C.scr_key[i];
@@ -1267,7 +1286,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
           return (u64)s;
         };
         bool exact2;
-        ts = (u32)radix_select<BLOCK, 8, DB>(sh, hist, n_mem, sf, 0ull, 0xFFFFFFFFull, nd, exact2);
+        ts = (u32)radix_select<BLOCK, 8, DB>(sh, C.t_a0, n_mem, sf, 0ull, 0xFFFFFFFFull, nd, exact2);
       }
     }
     for (u32 base = 0; base < n_mem; base += BLOCK) {
@@ -1275,7 +1294,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       bool keep = false;
       u64 k = 0;
       u32 s = 0, r = 0;
-      if (m < n_mem) {
+      if (m < n_mem && need > 0) {
         k = C.scr_key[m];
         s = scr_state[m];
         r = *(mem_row - 1 - m);
@@ -1290,14 +1309,29 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       }
       n_tok += total;
     }
+  } else if (n_mem > 0) { // the whole split bucket survives
+    for (u32 base = 0; base < n_mem; base += BLOCK) {
+      const u32 m = base + tid;
+      const bool keep = m < n_mem;
+      u32 total;
+      const u32 p = n_tok + block_excl_scan<BLOCK>(keep ? 1u : 0u, total, sh.scan);
+      if (keep) {
+        C.tok_state[p] = scr_state[m];
+        C.tok_cost[p] = key_cost(C.scr_key[m]);
+        C.scr_row[p] = *(mem_row - 1 - m);
+      }
+      n_tok += total;
+    }
   }
   __syncthreads();
+  PROF_MARK(sh, PF_PRUNE_SEL);
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, bi);
   if (tid == 0) {
     if (P.silence_ilabel > 0 && sh.best_last_il == P.silence_ilabel)
       C.cs->info.trailing_silence += 1;
     else
       C.cs->info.trailing_silence = 0;
+    C.cs->prev_best = key_cost(best_ck);
   }
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_OUT);
@@ -1325,11 +1359,15 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   }
   __syncthreads();
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, -1);
+  if (threadIdx.x == 0) C.cs->prev_best = key_cost(sh.min_ck);
+  __syncthreads();
 }
 
 // Moves the channel to a fresh table epoch; the table is wiped when the
-// 8-bit epoch tag would wrap, so a tag is never reused while stale values
-// carrying it can still be in the table.
+// 7-bit epoch tag would wrap, so a tag is never reused while stale values
+// carrying it can still be in the table.  Also opens the frame's cost
+// histogram: buckets of beam / HIST_PER_BEAM from one beam below the previous
+// frame's best cost (values outside clamp into the end buckets).
 template <int BLOCK, typename F, typename S>
 __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   u32 e = C.cs->epoch + 1;
@@ -1348,6 +1386,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     }
     e += 1;
   }
+  for (u32 b = threadIdx.x; b < NB_HIST; b += BLOCK) sh.fhist[b] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     C.cs->epoch = e;
@@ -1361,6 +1400,9 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.eps_n = 0;
     sh.emit_end = 0;
     sh.min_ck = ~0ull;
+    sh.n_rec_frame = 0;
+    sh.hbase = C.cs->prev_best - P.beam;
+    sh.hscale = HIST_PER_BEAM / P.beam;
   }
   __syncthreads();
 }
@@ -1436,6 +1478,7 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     RelaxAcc acc;
     acc.min_ck = ~0ull;
     acc.n_new = acc.n_app = 0;
+    acc.n_rec = 0;
     const bool on1[1] = {true};
     const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
