@@ -189,7 +189,6 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     e_cnt[s + 1] += e_cnt[s];
     x_cnt[s + 1] += x_cnt[s];
   }
-  const u32 n_e = e_cnt[num_states], n_x = x_cnt[num_states];
   std::vector<double> fin(num_states, std::nan(""));
   for (int i = 0; i < num_finals; ++i) {
     int s = final_states[i];
@@ -216,13 +215,36 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     delete g;
     return fail(AB_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
   }
-  // build the split arc arrays (arc order inside each state preserved)
+  // build the split arc arrays (arc order inside each state preserved).
+  // Fmt16: a state's block of up to four 16-B records never straddles a
+  // 64-byte DRAM atom (it is moved to the next atom if it would), longer
+  // blocks start on an atom: one random block read is as few atoms as its
+  // size allows.
   const bool f16 = g->fmt16;
   size_t esz = f16 ? sizeof(EArc16) : sizeof(EArc24);
   size_t xsz = f16 ? sizeof(XArc16) : sizeof(XArc24);
-  std::vector<unsigned char> eh(std::max<size_t>(n_e, 1) * esz, 0), xh(std::max<size_t>(n_x, 1) * xsz, 0);
+  std::vector<u32> e_beg(num_states), x_beg(num_states);
+  uint64_t e_tot = 0, x_tot = 0;
+  auto place = [&](uint64_t &cur, u32 cnt) -> u32 {
+    if (f16 && cnt) {
+      constexpr uint64_t ATOM = 4; // records per 64-byte atom
+      if (cnt > ATOM || (cur % ATOM) + cnt > ATOM) cur = (cur + ATOM - 1) / ATOM * ATOM;
+    }
+    const u32 b = (u32)cur;
+    cur += cnt;
+    return b;
+  };
   for (int s = 0; s < num_states; ++s) {
-    u32 pe = e_cnt[s], px = x_cnt[s];
+    e_beg[s] = place(e_tot, e_cnt[s + 1] - e_cnt[s]);
+    x_beg[s] = place(x_tot, x_cnt[s + 1] - x_cnt[s]);
+  }
+  if (e_tot >= 0xFFFFFFFFull || x_tot >= 0xFFFFFFFFull) {
+    delete g;
+    return fail(AB_ERR_INVALID, "too many arcs after block alignment");
+  }
+  std::vector<unsigned char> eh(std::max<size_t>(e_tot, 1) * esz, 0), xh(std::max<size_t>(x_tot, 1) * xsz, 0);
+  for (int s = 0; s < num_states; ++s) {
+    u32 pe = e_beg[s], px = x_beg[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
       const int dst = next_states[a];
       const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
@@ -254,8 +276,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   unsigned char *de = nullptr, *dx = nullptr;
   std::vector<uint2> erng(num_states), xrng(num_states);
   for (int s = 0; s < num_states; ++s) {
-    erng[s] = make_uint2(e_cnt[s], e_cnt[s + 1]);
-    xrng[s] = make_uint2(x_cnt[s], x_cnt[s + 1]);
+    erng[s] = make_uint2(e_beg[s], e_beg[s] + (e_cnt[s + 1] - e_cnt[s]));
+    xrng[s] = make_uint2(x_beg[s], x_beg[s] + (x_cnt[s + 1] - x_cnt[s]));
   }
   if (dmalloc(&g->e_rng, num_states, acc) || dmalloc(&g->x_rng, num_states, acc) ||
       dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
