@@ -517,7 +517,8 @@ constexpr double HIST_PER_BEAM = 256.0; // buckets per beam width
 // Cost bucket of the frame's histogram: monotone in the cost, clamped at both ends.
 __device__ __forceinline__ u32 hbucket(const Shared &sh, double c) {
   const double x = (c - sh.hbase) * sh.hscale;
-  return x <= 0.0 ? 0u : (x >= (double)(NB_HIST - 1) ? NB_HIST - 1 : (u32)x);
+  // !(x > 0) also catches NaN (an infinite beam makes the scale 0 and the base -inf)
+  return !(x > 0.0) ? 0u : (x >= (double)(NB_HIST - 1) ? NB_HIST - 1 : (u32)x);
 }
 
 // BiasingContext.boosted_mask (biasing.py:108-117) in the representation the

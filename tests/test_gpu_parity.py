@@ -344,3 +344,22 @@ def test_hashed_token_table_matches_reference(small_cases, monkeypatch):
     want, rc, info = _oracle(csr, scores, ctx, cfg)
     assert rc == 0
     _same(res.hypotheses, want, "G_small hashed")
+
+
+@pytest.mark.parametrize("beam,max_active", [(float("inf"), 500), (0.25, 7000), (13.0, 1)])
+def test_extreme_beams_and_caps(beam, max_active):
+    """Infinite beam (max_active alone prunes), a beam narrower than the cost
+    spread, and max_active = 1: the prune's cost-bucket split stays exact."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctx = synth.unigram_context(csr, 20, 9, num_labels=2000)
+    cfg = ab.DecoderConfig(beam=beam, max_active=max_active, partial_every=7)
+    scores = synth.channel_scores(13, 0, 30, 2000)
+    res, ch = _decode(csr, scores, ctx, cfg)
+    assert res.error is None, res.error
+    want, rc, info = _oracle(csr, scores, ctx, cfg)
+    assert rc == 0
+    _same(res.hypotheses, want, f"beam {beam} max_active {max_active}")
+    assert len(ch.store) == info["store_len"]
