@@ -33,7 +33,8 @@ enum {
   AB_ERR_UNKNOWN_CTX = 6,  /* UnknownContextError (biasing.py:27) */
   AB_ERR_WIDTH = 7,        /* frame width != emitting-label count (decoder.py:354-359) */
   AB_ERR_PARSE = 8,        /* FstParseError (fst.py:24): malformed graph text */
-  AB_ERR_STRUCTURE = 9     /* FstStructureError (fst.py:28) */
+  AB_ERR_STRUCTURE = 9,    /* FstStructureError (fst.py:28) */
+  AB_ERR_SCORE_FORMAT = 10 /* ScoreFormatError (scores.py:15) */
 };
 
 enum { AB_IDLE = 0, AB_DECODING = 1, AB_ENDPOINTED = 2, AB_FINISHED = 3 };
@@ -56,6 +57,7 @@ enum { AB_MAX_TOKENS = 131072, AB_MAX_HASH_SLOTS = 4194304, AB_MAX_EPSILON_ROUND
 
 typedef struct ab_graph ab_graph;
 typedef struct ab_fst ab_fst; /* a parsed graph on the host (state-major CSR) */
+typedef struct ab_scores ab_scores; /* a parsed score matrix on the host */
 typedef struct ab_decoder ab_decoder;
 
 /* DecoderConfig (decoder.py:33-48). */
@@ -212,6 +214,13 @@ int ab_fst_arrays(const ab_fst *f, int64_t *row_offsets, int32_t *ilabels, int32
                   int32_t *next_states, double *weights, int32_t *final_states, double *final_costs);
 void ab_fst_destroy(ab_fst *f);
 int ab_graph_create_from_fst(int32_t device, const ab_fst *f, ab_graph **out);
+/* Score ingest (scores.py:52-96 parse_score_matrix / load_score_matrix):
+   the text format into a host [num_frames, num_ilabels] f64 matrix with the
+   reference's checks; AB_ERR_SCORE_FORMAT carries its messages. */
+int ab_scores_parse(const char *text, int64_t len, ab_scores **out);
+int ab_scores_info(const ab_scores *s, int64_t *num_frames, int64_t *num_ilabels, double *frame_duration);
+int ab_scores_copy(const ab_scores *s, double *costs);
+void ab_scores_destroy(ab_scores *s);
 int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,
                        const int32_t *olabels, const int32_t *next_states, int32_t n_entities,
                        const int64_t *ent_offsets, const int32_t *labels,

@@ -25,6 +25,7 @@ AB_ERR_UNKNOWN_CTX = 6
 AB_ERR_WIDTH = 7
 AB_ERR_PARSE = 8
 AB_ERR_STRUCTURE = 9
+AB_ERR_SCORE_FORMAT = 10
 
 AB_IDLE, AB_DECODING, AB_ENDPOINTED, AB_FINISHED = 0, 1, 2, 3
 AB_PARTIAL, AB_FINAL = 0, 1
@@ -143,6 +144,10 @@ SIGNATURES = {
     "ab_fst_arrays": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "ab_fst_destroy": (None, [_P]),
     "ab_graph_create_from_fst": (_I32, [_I32, _P, C.POINTER(_P)]),
+    "ab_scores_parse": (_I32, [C.c_char_p, _I64, C.POINTER(_P)]),
+    "ab_scores_info": (_I32, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(C.c_double)]),
+    "ab_scores_copy": (_I32, [_P, _P]),
+    "ab_scores_destroy": (None, [_P]),
     "ab_compile_context": (_I32, [_I32, _I64, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I64,
                                   C.POINTER(_I64), _P]),
 }

@@ -18,6 +18,7 @@
 
 #include "context_compiler.h"
 #include "graph_ingest.h"
+#include "score_ingest.h"
 #include "decode_kernel.cuh"
 
 using namespace ab;
@@ -1427,6 +1428,41 @@ extern "C" int ab_graph_create_from_fst(int32_t device, const ab_fst *f, ab_grap
                          F.ol.data(), F.ns.data(), F.w.data(), (int32_t)F.fstate.size(), F.fstate.data(),
                          F.fcost.data(), out);
 }
+
+struct ab_scores {
+  ab::HostScores S;
+};
+
+extern "C" int ab_scores_parse(const char *text, int64_t len, ab_scores **out) {
+  if (!out || (!text && len)) return fail(AB_ERR_INVALID, "null argument");
+  *out = nullptr;
+  ab_scores *s = new ab_scores();
+  std::string err;
+  const int rc = ab::parse_score_text(text ? text : "", (size_t)std::max<int64_t>(len, 0), s->S, err);
+  if (rc) {
+    delete s;
+    return fail(rc == 1 ? AB_ERR_SCORE_FORMAT : AB_ERR_INVALID, "%s", err.c_str());
+  }
+  *out = s;
+  return AB_OK;
+}
+
+extern "C" int ab_scores_info(const ab_scores *s, int64_t *num_frames, int64_t *num_ilabels,
+                              double *frame_duration) {
+  if (!s) return fail(AB_ERR_INVALID, "null scores");
+  if (num_frames) *num_frames = s->S.T;
+  if (num_ilabels) *num_ilabels = s->S.L;
+  if (frame_duration) *frame_duration = s->S.dur;
+  return AB_OK;
+}
+
+extern "C" int ab_scores_copy(const ab_scores *s, double *costs) {
+  if (!s || (!costs && !s->S.costs.empty())) return fail(AB_ERR_INVALID, "null argument");
+  std::copy(s->S.costs.begin(), s->S.costs.end(), costs);
+  return AB_OK;
+}
+
+extern "C" void ab_scores_destroy(ab_scores *s) { delete s; }
 
 extern "C" int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_offsets,
                                   const int32_t *olabels, const int32_t *next_states,
