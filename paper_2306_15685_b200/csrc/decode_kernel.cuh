@@ -81,7 +81,7 @@ constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L
 constexpr int EXP_Q = AB_EXP_Q; // inputs per thread per expansion tile (CSR range loads in flight)
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
 #ifndef AB_PRUNE_Q
-#define AB_PRUNE_Q 2
+#define AB_PRUNE_Q 4
 #endif
 constexpr int PRUNE_Q = AB_PRUNE_Q; // rows per thread in flight (prune)
 

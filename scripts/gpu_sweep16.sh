@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+run() { timeout 300 python bench.py --frames 100 --segments 1 --steps 2 --warmup 1 --no-e2e --no-cpu --no-overhead 2>&1 | grep '^{' | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value']))"; }
+: > gpurun_out/sweep16.log
+for v in PQ4 PQ8 PQ4 PQ8; do
+  echo "== $v : $(ARCBOOST_B200_LIB=paper_2306_15685_b200/libarcboost_b200_$v.so run)" >> gpurun_out/sweep16.log
+done
