@@ -227,6 +227,19 @@ int ab_compile_context(int32_t num_states, int64_t num_arcs, const int64_t *row_
                        int32_t max_epsilon_depth, int32_t num_threads, int64_t *out_arcs,
                        int64_t out_cap, int64_t *n_out, int32_t *ent_status);
 
+/* Run scoring (metrics.py:26-83 align / compute_wer), words as integer ids.
+   ab_align: the minimum-edit-distance alignment with the reference's
+   backtrace tie order (match, substitution, deletion, insertion); kind[i] in
+   {0 match, 1 substitution, 2 deletion, 3 insertion}, ref_pos / hyp_pos -1
+   where absent.  *n_ops is the full count (<= nr + nh); at most cap ops are
+   written.  ab_edit_distances: the edit distance of each of n pairs (words
+   ref[ref_off[p]:ref_off[p+1]] vs hyp[...]), pairs over num_threads host
+   threads (0 = all). */
+int ab_align(const int32_t *ref, int64_t nr, const int32_t *hyp, int64_t nh, int8_t *kind,
+             int32_t *ref_pos, int32_t *hyp_pos, int64_t cap, int64_t *n_ops);
+int ab_edit_distances(int64_t n, const int64_t *ref_off, const int32_t *ref, const int64_t *hyp_off,
+                      const int32_t *hyp, int32_t num_threads, int64_t *dist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,14 +30,34 @@ from .decoder import (
     partial_hypothesis,
     switch_context,
 )
-from .compiler import BoostCompileConfig, compile_context, find_boost_arcs
+from .compiler import (
+    BoostCompileConfig,
+    EntityList,
+    compile_context,
+    find_boost_arcs,
+    load_registry,
+    read_context_manifest,
+)
 from .device import BatchDecoder, Capacity, DeviceGraph, device_graph
-from .fst import EPSILON, Arc, CsrFst, Fst, build_csr, csr_from_arrays, parse_text_fst
+from .fst import (
+    EPSILON,
+    Arc,
+    CsrFst,
+    Fst,
+    SymbolTable,
+    SymbolTableError,
+    build_csr,
+    csr_from_arrays,
+    parse_symbol_table,
+    parse_text_fst,
+)
 from .scores import ScoreMatrix
+from . import harness, metrics
 
 __all__ = [
     "EPSILON", "Arc", "BatchDecoder", "BiasingCompileError", "BiasingContext", "BoostCompileConfig",
-    "Capacity", "compile_context", "find_boost_arcs",
+    "Capacity", "EntityList", "SymbolTable", "SymbolTableError", "compile_context", "find_boost_arcs",
+    "harness", "load_registry", "metrics", "parse_symbol_table", "read_context_manifest",
     "Channel", "ChannelResult", "ChannelStatus", "ContextRegistry", "CsrFst", "DecodeError",
     "DecoderConfig", "DeviceGraph", "Fst", "Hypothesis", "ScoreMatrix", "UnknownContextError",
     "advance_frame", "build_csr", "csr_from_arrays", "decode_batch", "detect_endpoint",

@@ -150,6 +150,8 @@ SIGNATURES = {
     "ab_scores_destroy": (None, [_P]),
     "ab_compile_context": (_I32, [_I32, _I64, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _I64,
                                   C.POINTER(_I64), _P]),
+    "ab_align": (_I32, [_P, _I64, _P, _I64, _P, _P, _P, _I64, C.POINTER(_I64)]),
+    "ab_edit_distances": (_I32, [_I64, _P, _P, _P, _P, _I32, _P]),
 }
 
 _lib = None

@@ -13,12 +13,13 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import Sequence
+from pathlib import Path
+from typing import Iterable, Sequence
 
 import numpy as np
 
 from . import _lib
-from .biasing import BiasingCompileError, BiasingContext, ContextStats
+from .biasing import BiasingCompileError, BiasingContext, ContextRegistry, ContextStats
 
 EPSILON = 0
 
@@ -101,6 +102,11 @@ def compile_context(fst, symtab, entities, cfg: BoostCompileConfig, id: str,
     (biasing.py:236-285): duplicate entities are compiled once, entities with
     an out-of-vocabulary word are skipped whole and counted (or raise with
     ``skip_oov=False``)."""
+    return _compile_context_arrays(csr_arrays(fst), symtab, entities, cfg, id, threads)
+
+
+def _compile_context_arrays(arrays, symtab, entities, cfg: BoostCompileConfig, id: str,
+                            threads: int = 0) -> BiasingContext:
     stats = ContextStats()
     seen: set[tuple[str, ...]] = set()
     todo: list[list[int]] = []
@@ -127,7 +133,7 @@ def compile_context(fst, symtab, entities, cfg: BoostCompileConfig, id: str,
         _check_words(labels)
         todo.append(labels)
     if todo:
-        arcs, status = _compile(csr_arrays(fst), todo, cfg.max_epsilon_depth,
+        arcs, status = _compile(arrays, todo, cfg.max_epsilon_depth,
                                 threads or (os.cpu_count() or 1))
         stats.compiled = int((status == 1).sum())
         stats.unmatched = int((status == 0).sum())
@@ -135,3 +141,71 @@ def compile_context(fst, symtab, entities, cfg: BoostCompileConfig, id: str,
         arcs = np.zeros(0, dtype=np.int64)
     stats.empty = not len(arcs)
     return BiasingContext(id=id, arc_indices=arcs, discount=cfg.discount, stats=stats)
+
+
+@dataclass
+class EntityList:
+    """Ordered word sequences to boost (reference biasing.py:31-57)."""
+
+    entries: list[list[str]]
+    source: str = ""
+
+    def __post_init__(self) -> None:
+        for entry in self.entries:
+            if not entry:
+                raise BiasingCompileError(f"empty entity in {self.source or 'entity list'}")
+
+    @classmethod
+    def parse_text(cls, text: str, source: str = "") -> "EntityList":
+        """One entity per line, words space-separated; '#' lines are comments."""
+        entries = []
+        for raw in text.splitlines():
+            line = raw.strip()
+            if not line or line.startswith("#"):
+                continue
+            entries.append(line.split())
+        return cls(entries=entries, source=source)
+
+    @classmethod
+    def from_file(cls, path) -> "EntityList":
+        path = Path(path)
+        return cls.parse_text(path.read_text(encoding="utf-8"), source=str(path))
+
+
+def _graph_fingerprint(fst) -> str:
+    fp = getattr(fst, "fingerprint", "")
+    return fp() if callable(fp) else fp
+
+
+def load_registry(fst, symtab, manifest: Iterable[tuple[str, str]], cfg: BoostCompileConfig,
+                  threads: int = 0) -> ContextRegistry:
+    """Compile every manifest entry before decoding (reference
+    biasing.py:352-372): duplicate ids and unreadable entity files raise
+    BiasingCompileError; the registry carries the graph fingerprint."""
+    contexts: dict[str, BiasingContext] = {}
+    arrays = None
+    for context_id, path in manifest:
+        if context_id in contexts:
+            raise BiasingCompileError(f"duplicate context id {context_id!r} in manifest")
+        try:
+            entities = EntityList.from_file(path)
+        except OSError as exc:
+            raise BiasingCompileError(f"cannot read entity file {path}: {exc}") from None
+        if arrays is None:
+            arrays = csr_arrays(fst)
+        contexts[context_id] = _compile_context_arrays(arrays, symtab, entities, cfg, context_id, threads)
+    return ContextRegistry(contexts=contexts, graph_fingerprint=_graph_fingerprint(fst))
+
+
+def read_context_manifest(text: str) -> list[tuple[str, str]]:
+    """TSV lines ``id<TAB>entity-file-path`` (reference biasing.py:375-389)."""
+    rows: list[tuple[str, str]] = []
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split("\t")
+        if len(parts) != 2:
+            raise BiasingCompileError(f"manifest line {lineno}: expected 'id<TAB>path', got {raw!r}")
+        rows.append((parts[0], parts[1]))
+    return rows

@@ -19,6 +19,7 @@
 #include "context_compiler.h"
 #include "graph_ingest.h"
 #include "score_ingest.h"
+#include "scoring.h"
 #include "decode_kernel.cuh"
 
 using namespace ab;
@@ -1491,6 +1492,36 @@ extern "C" int ab_compile_context(int32_t num_states, int64_t num_arcs, const in
   if (out_arcs)
     std::copy(all.begin(), all.begin() + std::min<int64_t>((int64_t)all.size(), std::max<int64_t>(out_cap, 0)),
               out_arcs);
+  return AB_OK;
+}
+
+extern "C" int ab_align(const int32_t *ref, int64_t nr, const int32_t *hyp, int64_t nh, int8_t *kind,
+                        int32_t *ref_pos, int32_t *hyp_pos, int64_t cap, int64_t *n_ops) {
+  if (nr < 0 || nh < 0 || (nr && !ref) || (nh && !hyp) || !n_ops) return fail(AB_ERR_INVALID, "invalid arguments");
+  if (nr >= INT32_MAX || nh >= INT32_MAX) return fail(AB_ERR_INVALID, "sequence too long");
+  std::vector<uint32_t> D;
+  std::vector<int8_t> k;
+  std::vector<int32_t> rp, hp;
+  ab::edit_table(ref, nr, hyp, nh, D);
+  ab::backtrace(ref, nr, hyp, nh, D, k, rp, hp);
+  *n_ops = (int64_t)k.size();
+  const size_t m = (size_t)std::min<int64_t>((int64_t)k.size(), std::max<int64_t>(cap, 0));
+  if (m && (!kind || !ref_pos || !hyp_pos)) return fail(AB_ERR_INVALID, "null output");
+  std::copy(k.begin(), k.begin() + m, kind);
+  std::copy(rp.begin(), rp.begin() + m, ref_pos);
+  std::copy(hp.begin(), hp.begin() + m, hyp_pos);
+  return AB_OK;
+}
+
+extern "C" int ab_edit_distances(int64_t n, const int64_t *ref_off, const int32_t *ref, const int64_t *hyp_off,
+                                 const int32_t *hyp, int32_t num_threads, int64_t *dist) {
+  if (n < 0 || (n && (!ref_off || !hyp_off || !dist))) return fail(AB_ERR_INVALID, "invalid arguments");
+  for (int64_t p = 0; p < n; ++p)
+    if (ref_off[p + 1] < ref_off[p] || hyp_off[p + 1] < hyp_off[p]) return fail(AB_ERR_INVALID, "offsets decrease");
+  if (n && ((ref_off[n] > ref_off[0] && !ref) || (hyp_off[n] > hyp_off[0] && !hyp)))
+    return fail(AB_ERR_INVALID, "null word array");
+  const int32_t threads = num_threads > 0 ? num_threads : (int32_t)std::max(1u, std::thread::hardware_concurrency());
+  ab::edit_distances(n, ref_off, ref, hyp_off, hyp, threads, dist);
   return AB_OK;
 }
 

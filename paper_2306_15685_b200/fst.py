@@ -280,3 +280,81 @@ def load_fst(path, num_states_hint: int | None = None, cache: bool = True,
     csr = _native_fst(h)
     csr.cache_hit = bool(hit.value)
     return csr
+
+
+class SymbolTableError(ValueError):
+    """Invalid symbol table (reference fst.py:32)."""
+
+
+class SymbolTable:
+    """Bijective word <-> label-id map, id 0 is epsilon (reference
+    fst.py:334-373); the harness maps hypothesis labels back to words."""
+
+    def __init__(self, word_to_id: dict[str, int]):
+        if 0 not in word_to_id.values():
+            raise SymbolTableError("missing epsilon entry at id 0")
+        self._word_to_id = dict(word_to_id)
+        self._id_to_word: dict[int, str] = {}
+        for word, label in self._word_to_id.items():
+            if label in self._id_to_word:
+                raise SymbolTableError(f"duplicate id {label} ({self._id_to_word[label]!r} vs {word!r})")
+            self._id_to_word[label] = word
+
+    def __len__(self) -> int:
+        return len(self._word_to_id)
+
+    def __contains__(self, word: str) -> bool:
+        return word in self._word_to_id
+
+    def id_of(self, word: str) -> int:
+        try:
+            return self._word_to_id[word]
+        except KeyError:
+            raise SymbolTableError(f"unknown word {word!r}") from None
+
+    def get_id(self, word: str) -> int | None:
+        return self._word_to_id.get(word)
+
+    def word_of(self, label: int) -> str:
+        try:
+            return self._id_to_word[label]
+        except KeyError:
+            raise SymbolTableError(f"unknown label id {label}") from None
+
+    def words(self):
+        return iter(self._word_to_id)
+
+    @property
+    def epsilon_word(self) -> str:
+        return self._id_to_word[EPSILON]
+
+
+def parse_symbol_table(text) -> SymbolTable:
+    """``word id`` lines (reference fst.py:376-400): blank and ``#`` lines
+    skipped, duplicate words or ids rejected, the reference's messages."""
+    if hasattr(text, "read"):
+        text = text.read()
+    lines = text.splitlines() if isinstance(text, str) else list(text)
+    word_to_id: dict[str, int] = {}
+    seen_ids: dict[int, str] = {}
+    for lineno, raw in enumerate(lines, start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        fields = line.split()
+        if len(fields) != 2:
+            raise FstParseError(f"line {lineno}: expected 'word id', got {raw!r}")
+        word = fields[0]
+        try:
+            label = int(fields[1])
+        except ValueError:
+            raise FstParseError(f"line {lineno}: bad id {fields[1]!r}") from None
+        if label < 0:
+            raise FstParseError(f"line {lineno}: negative id {label}")
+        if word in word_to_id:
+            raise SymbolTableError(f"duplicate word {word!r}")
+        if label in seen_ids:
+            raise SymbolTableError(f"duplicate id {label} ({seen_ids[label]!r} vs {word!r})")
+        word_to_id[word] = label
+        seen_ids[label] = word
+    return SymbolTable(word_to_id)
