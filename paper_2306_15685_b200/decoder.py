@@ -135,7 +135,7 @@ class Channel:
 
 # ------------------------------------------------------------ host mirror sync
 
-def _bind(ch: Channel, csr) -> tuple[BatchDecoder, int]:
+def _bind(ch: Channel, csr, prefer: BatchDecoder | None = None) -> tuple[BatchDecoder, int]:
     dg = device_graph(csr)
     if ch._graph is dg:
         return ch._page, ch._slot
@@ -143,7 +143,7 @@ def _bind(ch: Channel, csr) -> tuple[BatchDecoder, int]:
         if not ch._fresh:
             raise DecodeError(f"channel {ch.id!r}: cannot move to another graph mid-utterance")
         ch._page.free_slot(ch._slot)
-    page, slot = dg.bind_slot()
+    page, slot = dg.bind_slot(prefer)
     ch._graph, ch._page, ch._slot = dg, page, slot
     ch._last_words = []
     weakref.finalize(ch, page.free_slot, slot)
@@ -354,10 +354,11 @@ def decode_batch(channels: Sequence[tuple[Channel, ScoreMatrix]], csr,
     dg = device_graph(csr)
     _check_eps_cap(cfg)
     pending: list[tuple[int, Channel, ScoreMatrix]] = []
+    page = dg.reserve(len({id(ch) for ch, _ in channels if ch._graph is not dg}))
     for i, (ch, scores) in enumerate(channels):
         try:
             ctx = _prepare(ch, scores, csr, registry, dg)
-            _bind(ch, csr)
+            _bind(ch, csr, page)
             ch._ctx_handle = dg.context_handle(ctx)
             pending.append((i, ch, scores))
         except Exception as exc:  # per-channel isolation (decoder.py:516-521)
@@ -380,15 +381,21 @@ def _launch_stream(items, dg: DeviceGraph, cfg, results) -> None:
     page = items[0][1]._page
     L = dg.num_emitting_labels
     mats = [s.costs for _, _, s in items]
-    f32 = all(m.dtype == np.float32 or
-              (m.size == 0 or np.array_equal(m.astype(np.float32).astype(np.float64), m))
-              for m in mats)
-    dt = np.float32 if f32 else np.float64
+    # f32 on the device when every cost is exactly an f32 (half the H2D bytes)
+    m32 = []
+    f32 = True
+    for m in mats:
+        if f32:
+            x = m if m.dtype == np.float32 else m.astype(np.float32)
+            f32 = x is m or np.array_equal(x, m)
+            m32.append(x)
+    src = m32 if f32 else [m.astype(np.float64, copy=False) for m in mats]
     frames = np.array([m.shape[0] for m in mats], dtype=np.int32)
     offs = np.zeros(len(mats), dtype=np.int64)
     if len(mats) > 1:
         np.cumsum(frames[:-1].astype(np.int64) * L, out=offs[1:])
-    rows = [m.astype(dt, copy=False).reshape(-1) for m in mats if m.size]
+    rows = [m.reshape(-1) for m in src if m.size]
+    dt = np.float32 if f32 else np.float64
     packed = np.ascontiguousarray(np.concatenate(rows)) if rows else np.zeros(1, dtype=dt)
     for _, ch, _ in items:
         _push(ch)

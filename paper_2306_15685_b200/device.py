@@ -107,7 +107,24 @@ class DeviceGraph:
                 pass
 
     # -- channel slots -------------------------------------------------
-    def bind_slot(self) -> tuple["BatchDecoder", int]:
+    def reserve(self, n: int) -> "BatchDecoder | None":
+        """A page with room for n more channels (a new one if none has it), so
+        a batch binding many channels at once decodes in one launch instead of
+        one per geometrically grown page."""
+        if n <= 0:
+            return None
+        for p in self._pages:
+            if len(p._free) >= n:
+                return p
+        p = BatchDecoder(self, min(1024, max(n, 8 << len(self._pages))))
+        self._pages.append(p)
+        return p
+
+    def bind_slot(self, prefer: "BatchDecoder | None" = None) -> tuple["BatchDecoder", int]:
+        if prefer is not None:
+            s = prefer.alloc_slot()
+            if s is not None:
+                return prefer, s
         for p in self._pages:
             s = p.alloc_slot()
             if s is not None:
