@@ -70,6 +70,7 @@ struct ab_graph {
   std::vector<int32_t> olabels; // host copy for context classification
   std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
   uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
+  unsigned char *deg = nullptr;              // per state arc counts (DecodeParams::deg)
   void *e_arcs = nullptr, *x_arcs = nullptr;
   double *final_cost = nullptr;
   size_t bytes = 0;
@@ -218,15 +219,21 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     return fail(AB_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
   }
   // build the split arc arrays (arc order inside each state preserved).
-  // Fmt16: a state's block of up to four 16-B records never straddles a
-  // 64-byte DRAM atom (it is moved to the next atom if it would), longer
-  // blocks start on an atom: one random block read is as few atoms as its
-  // size allows.
+  // A state with at most SLOT_E emitting (SLOT_X epsilon) arcs keeps them in
+  // its fixed slot at s * SLOT_E (s * SLOT_X), so the kernel finds them from
+  // the state id and a 1-byte count that stays in L2, without a dependent
+  // read of the range array; bigger states go to an overflow area after the
+  // slots and are found through the ranges.  (Slots are skipped when they
+  // would cost more than 8 GB.)  Overflow blocks, Fmt16: a block of up to
+  // four 16-B records never straddles a 64-byte DRAM atom, longer blocks
+  // start on an atom.
   const bool f16 = g->fmt16;
   size_t esz = f16 ? sizeof(EArc16) : sizeof(EArc24);
   size_t xsz = f16 ? sizeof(XArc16) : sizeof(XArc24);
+  const bool slots = (uint64_t)num_states * (SLOT_E * esz + SLOT_X * xsz) <= (8ull << 30);
   std::vector<u32> e_beg(num_states), x_beg(num_states);
-  uint64_t e_tot = 0, x_tot = 0;
+  std::vector<unsigned char> deg(num_states);
+  uint64_t e_tot = slots ? (uint64_t)num_states * SLOT_E : 0, x_tot = slots ? (uint64_t)num_states * SLOT_X : 0;
   auto place = [&](uint64_t &cur, u32 cnt) -> u32 {
     if (f16 && cnt) {
       constexpr uint64_t ATOM = 4; // records per 64-byte atom
@@ -237,8 +244,21 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     return b;
   };
   for (int s = 0; s < num_states; ++s) {
-    e_beg[s] = place(e_tot, e_cnt[s + 1] - e_cnt[s]);
-    x_beg[s] = place(x_tot, x_cnt[s + 1] - x_cnt[s]);
+    const u32 ec = e_cnt[s + 1] - e_cnt[s], xc = x_cnt[s + 1] - x_cnt[s];
+    u32 de = DEG_OVF, dx = DEG_OVF;
+    if (slots && ec <= SLOT_E) {
+      e_beg[s] = (u32)s * SLOT_E;
+      de = ec;
+    } else {
+      e_beg[s] = place(e_tot, ec);
+    }
+    if (slots && xc <= SLOT_X) {
+      x_beg[s] = (u32)s * SLOT_X;
+      dx = xc;
+    } else {
+      x_beg[s] = place(x_tot, xc);
+    }
+    deg[s] = (unsigned char)(de | (dx << 4));
   }
   if (e_tot >= 0xFFFFFFFFull || x_tot >= 0xFFFFFFFFull) {
     delete g;
@@ -283,7 +303,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   if (dmalloc(&g->e_rng, num_states, acc) || dmalloc(&g->x_rng, num_states, acc) ||
       dmalloc(&de, eh.size(), acc) || dmalloc(&dx, xh.size(), acc) ||
-      dmalloc(&g->final_cost, num_states, acc)) {
+      dmalloc(&g->final_cost, num_states, acc) || dmalloc(&g->deg, num_states, acc)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "device allocation for the graph failed (%zu bytes)", acc);
   }
@@ -295,7 +315,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       cudaMemcpy(g->x_rng, xrng.data(), num_states * sizeof(uint2), cudaMemcpyHostToDevice) ||
       cudaMemcpy(de, eh.data(), eh.size(), cudaMemcpyHostToDevice) ||
       cudaMemcpy(dx, xh.data(), xh.size(), cudaMemcpyHostToDevice) ||
-      cudaMemcpy(g->final_cost, fin.data(), num_states * sizeof(double), cudaMemcpyHostToDevice)) {
+      cudaMemcpy(g->final_cost, fin.data(), num_states * sizeof(double), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->deg, deg.data(), num_states, cudaMemcpyHostToDevice)) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "graph upload failed: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -313,6 +334,7 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   cudaFree(g->d_ctxs);
   cudaFree(g->e_rng);
   cudaFree(g->x_rng);
+  cudaFree(g->deg);
   cudaFree(g->e_arcs);
   cudaFree(g->x_arcs);
   cudaFree(g->final_cost);
@@ -812,6 +834,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   ab_graph *g = d->g;
   memset(&P, 0, sizeof(P));
   P.e_rng = g->e_rng;
+  P.deg = g->deg;
   P.e_arcs = g->e_arcs;
   P.x_rng = g->x_rng;
   P.x_arcs = g->x_arcs;

@@ -72,6 +72,8 @@ __device__ __forceinline__ u32 aux_src(u32 src, u32 rflags, u32 g) {
 }
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
+constexpr u32 SLOT_E = 4, SLOT_X = 2;         // arc records per state slot (emitting / epsilon)
+constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the overflow area
 #ifndef AB_EXP_Q
 #define AB_EXP_Q 2
 #endif
@@ -202,6 +204,11 @@ struct DecodeParams {
   const void *e_arcs;
   const uint2 *x_rng; // per state {begin, end} of its epsilon arcs
   const void *x_arcs;
+  // per state: emitting arc count (low nibble), epsilon arc count (high
+  // nibble); DEG_OVF = more than a slot holds, use the ranges.  A state with
+  // at most SLOT_E emitting (SLOT_X epsilon) arcs has them at s * SLOT_E
+  // (s * SLOT_X): no range lookup.  1 byte per state stays L2-resident.
+  const unsigned char *deg;
   const double *final_cost; // NaN = not final
   int start;
   int num_states;
@@ -804,6 +811,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   double *t_cost = C.t_cost;
   const int tid = threadIdx.x;
   const uint2 *rng = EMIT ? P.e_rng : P.x_rng;
+  constexpr u32 SLOT = EMIT ? SLOT_E : SLOT_X;
   const void *arcs = EMIT ? P.e_arcs : P.x_arcs;
   RelaxAcc acc;
   acc.min_ck = ~0ull;
@@ -846,9 +854,17 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       a0[q] = 0;
       cnt[q] = 0;
       if (EMIT ? (idx[q] != 0xFFFFFFFFu) : !(st[q] & ROW_DISP)) {
-        const uint2 r = __ldg(&rng[EMIT ? st[q] : (st[q] & ROW_STATE)]);
-        a0[q] = r.x;
-        cnt[q] = r.y - r.x;
+        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
+        const u32 dg = __ldg(&P.deg[s]);
+        const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
+        if (c == DEG_OVF) {
+          const uint2 r = __ldg(&rng[s]);
+          a0[q] = r.x;
+          cnt[q] = r.y - r.x;
+        } else {
+          a0[q] = s * SLOT;
+          cnt[q] = c;
+        }
       }
     }
     u32 tsum = 0;
