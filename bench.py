@@ -215,7 +215,8 @@ def hbm_peak():
 
 # ------------------------------------------------------------------ workload
 
-def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense=None, kind="words"):
+def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense=None, kind="words",
+                 host_scores=True):
     from paper_2306_15685_b200 import synth
 
     t0 = time.time()
@@ -232,9 +233,11 @@ def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense
             pool = synth.unigram_contexts(csr, 20, range(1000, 1000 + n_pool), num_labels=L)
     t1 = time.time()
     C, T = W["channels"], W["frames"]
-    scores = np.empty((C, T, L), dtype=np.float32)
-    for c in range(C):
-        scores[c] = synth.channel_scores(seed_base, channel_base + c, T, L)
+    scores = None
+    if host_scores:  # else the GPU arm generates them in HBM (synth.device_channel_scores)
+        scores = np.empty((C, T, L), dtype=np.float32)
+        for c in range(C):
+            scores[c] = synth.channel_scores(seed_base, channel_base + c, T, L)
     return csr, pool, scores, {"graph_s": t1 - t0, "scores_s": time.time() - t1}
 
 
@@ -278,7 +281,7 @@ def run_b200(args, W, world, rank, local):
     import torch
 
     import paper_2306_15685_b200 as ab
-    from paper_2306_15685_b200 import _lib
+    from paper_2306_15685_b200 import _lib, synth
     from paper_2306_15685_b200.device import BatchDecoder, Capacity, DeviceGraph
 
     torch.cuda.set_device(local)
@@ -287,8 +290,8 @@ def run_b200(args, W, world, rank, local):
     Tseg = T // S
     assert Tseg * S == T
     dense = args.density if args.workload == "c4" else None
-    csr, pool, scores_np, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense,
-                                              kind=args.c4_kind)
+    csr, pool, _, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense,
+                                      kind=args.c4_kind, host_scores=False)
     cfg = ab.DecoderConfig(beam=13.0, max_active=7000, max_epsilon_expansion=20,
                            partial_every=W["partial_every"])
     t0 = time.time()
@@ -302,8 +305,16 @@ def run_b200(args, W, world, rank, local):
     cap = Capacity(arena_records=(1 << 20) if big else (1 << 19))
     dec = BatchDecoder(dg, C, cap)
     prep["upload_s"] = time.time() - t0
-    scores_dev = torch.from_numpy(scores_np).to(dev)
-    scores_host = torch.from_numpy(scores_np).pin_memory()
+    # the same numpy streams, generated in HBM (ab_scores_generate, bit-identical
+    # to synth.channel_scores); the pinned host copy feeds the e2e leg and the
+    # CPU baseline
+    t0 = time.time()
+    scores_dev = synth.device_channel_scores(7, range(rank * C, rank * C + C), T, L, device=local)
+    torch.cuda.synchronize(dev)
+    prep["scores_s"] = time.time() - t0
+    scores_host = torch.empty(scores_dev.shape, dtype=scores_dev.dtype, pin_memory=True)
+    scores_host.copy_(scores_dev)
+    scores_np = scores_host.numpy()
     stream = torch.cuda.Stream(device=dev)
     slots = np.arange(C, dtype=np.int32)
 
@@ -404,7 +415,7 @@ def run_b200(args, W, world, rank, local):
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 accumulate (f32 weights/scores)",
-        "data": "synthetic (benchmark_graph seed 421; scores U[0,6) default_rng([7, c]))",
+        "data": "synthetic (benchmark_graph seed 421; scores U[0,6) default_rng([7, c]), generated in HBM bit-identically by ab_scores_generate)",
         "config": {"workload": f"{args.workload}: G {W['states']} states x 4 arcs, L={L}, "
                                f"{C} channels/GPU x {T} frames, {S} segments with context switch, "
                                f"partial_every {W['partial_every']}, beam 13, max_active 7000",

@@ -240,6 +240,16 @@ int ab_align(const int32_t *ref, int64_t nr, const int32_t *hyp, int64_t nh, int
 int ab_edit_distances(int64_t n, const int64_t *ref_off, const int32_t *ref, const int64_t *hyp_off,
                       const int32_t *hyp, int32_t num_threads, int64_t *dist);
 
+/* Synthetic scores on the device (synth.py:69-75, 156-195; the benchmark's
+   default_rng([seed, channel]).uniform streams): n_streams numpy PCG64
+   streams, streams[4*s..4*s+3] = {state >> 64, state & (2^64-1), inc >> 64,
+   inc & (2^64-1)} as numpy's bit_generator.state reports them; writes
+   out[s * values_per_stream + k] = offset + (low + (high - low) * u_k), u_k the
+   k-th next_double of stream s, bit-identical to numpy, as f32 (AB_F32,
+   rounded to nearest) or f64, into device memory.  Synchronous on stream. */
+int ab_scores_generate(int32_t device, const uint64_t *streams, int32_t n_streams, int64_t values_per_stream,
+                       double low, double high, double offset, int32_t dtype, void *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

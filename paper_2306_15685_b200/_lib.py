@@ -152,6 +152,7 @@ SIGNATURES = {
                                   C.POINTER(_I64), _P]),
     "ab_align": (_I32, [_P, _I64, _P, _I64, _P, _P, _P, _I64, C.POINTER(_I64)]),
     "ab_edit_distances": (_I32, [_I64, _P, _P, _P, _P, _I32, _P]),
+    "ab_scores_generate": (_I32, [_I32, _P, _I32, _I64, C.c_double, C.c_double, C.c_double, _I32, _P, _P]),
 }
 
 _lib = None

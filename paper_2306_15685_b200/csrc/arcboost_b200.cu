@@ -20,6 +20,7 @@
 #include "graph_ingest.h"
 #include "score_ingest.h"
 #include "scoring.h"
+#include "score_gen.cuh"
 #include "decode_kernel.cuh"
 
 using namespace ab;
@@ -1545,6 +1546,37 @@ extern "C" int ab_edit_distances(int64_t n, const int64_t *ref_off, const int32_
     return fail(AB_ERR_INVALID, "null word array");
   const int32_t threads = num_threads > 0 ? num_threads : (int32_t)std::max(1u, std::thread::hardware_concurrency());
   ab::edit_distances(n, ref_off, ref, hyp_off, hyp, threads, dist);
+  return AB_OK;
+}
+
+extern "C" int ab_scores_generate(int32_t device, const uint64_t *streams, int32_t n_streams,
+                                  int64_t values_per_stream, double low, double high, double offset,
+                                  int32_t dtype, void *out, void *stream) {
+  if (n_streams < 0 || values_per_stream < 0 || (n_streams && (!streams || !out)))
+    return fail(AB_ERR_INVALID, "invalid arguments");
+  if (dtype != AB_F32 && dtype != AB_F64) return fail(AB_ERR_INVALID, "dtype must be AB_F32 or AB_F64");
+  if (!n_streams || !values_per_stream) return AB_OK;
+  CK(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *d_streams = nullptr;
+  CK(cudaMalloc(&d_streams, (size_t)n_streams * 4 * sizeof(unsigned long long)));
+  cudaError_t e = cudaMemcpyAsync(d_streams, streams, (size_t)n_streams * 4 * sizeof(unsigned long long),
+                                  cudaMemcpyHostToDevice, st);
+  const long long chunks = (values_per_stream + ab::GEN_CHUNK - 1) / ab::GEN_CHUNK;
+  const long long threads = chunks * n_streams;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  if (e == cudaSuccess) {
+    if (dtype == AB_F32)
+      ab::uniform_kernel<float><<<blocks, 256, 0, st>>>(d_streams, n_streams, values_per_stream, low, high - low,
+                                                        offset, (float *)out);
+    else
+      ab::uniform_kernel<double><<<blocks, 256, 0, st>>>(d_streams, n_streams, values_per_stream, low, high - low,
+                                                         offset, (double *)out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_streams);
+  if (e != cudaSuccess) return fail(AB_ERR_CUDA, "score generation: %s", cudaGetErrorString(e));
   return AB_OK;
 }
 

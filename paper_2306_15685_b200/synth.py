@@ -142,3 +142,49 @@ def dense_context(csr, fraction: float, ctx_seed: int, *, discount: float = -2.0
     k = int(round(fraction * n))
     idx = np.sort(rng.choice(n, size=k, replace=False)).astype(np.int64)
     return BiasingContext(id=ctx_id or f"dense{ctx_seed}", arc_indices=idx, discount=discount)
+
+
+def pcg64_streams(seeds) -> np.ndarray:
+    """[n, 4] uint64 {state hi, state lo, inc hi, inc lo} of
+    ``np.random.default_rng(seed)`` for each seed (numpy's PCG64 state)."""
+    out = np.zeros((len(seeds), 4), dtype=np.uint64)
+    m = (1 << 64) - 1
+    for i, seed in enumerate(seeds):
+        st = np.random.default_rng(seed).bit_generator.state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        out[i] = (s >> 64, s & m, inc >> 64, inc & m)
+    return out
+
+
+def device_uniform(seeds, n: int, low: float, high: float, *, offset: float = 0.0,
+                   dtype="float32", out=None, device: int = 0):
+    """``offset + default_rng(seed).uniform(low, high, n)`` for every seed,
+    generated on the GPU bit-identically to numpy (``ab_scores_generate``):
+    a [len(seeds), n] torch tensor in device memory."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    tdt = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
+    if out is None:
+        out = torch.empty((len(seeds), n), dtype=tdt, device=torch.device("cuda", device))
+    if not (out.is_cuda and out.is_contiguous() and out.dtype == tdt and out.numel() == len(seeds) * n):
+        raise ValueError("out must be a contiguous CUDA tensor of len(seeds) * n values")
+    st = np.ascontiguousarray(pcg64_streams(seeds))
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    _lib.check(_lib.load().ab_scores_generate(
+        out.device.index, st.ctypes.data, len(seeds), int(n), float(low), float(high), float(offset),
+        _lib.AB_F32 if tdt == torch.float32 else _lib.AB_F64, C.c_void_p(out.data_ptr()),
+        C.c_void_p(stream)))
+    return out
+
+
+def device_channel_scores(seed: int, channels, frames: int, width: int, *, out=None, device: int = 0):
+    """``channel_scores(seed, c, frames, width)`` for every c in channels,
+    stacked [C, frames, width] f32, generated in device memory."""
+    chans = list(channels)
+    t = device_uniform([[seed, c] for c in chans], frames * width, 0.0, 6.0,
+                       out=None if out is None else out.view(len(chans), frames * width), device=device)
+    return t.view(len(chans), frames, width)
