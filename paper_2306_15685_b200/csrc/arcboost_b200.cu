@@ -931,11 +931,16 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
 template <typename F, typename S>
 static cudaError_t launch_decode_b(int block, const DecodeParams &P, int grid, size_t smem,
                                    cudaStream_t st) {
+#ifdef AB_ONLY_256 // experiment builds whose tiles do not fit the larger CTAs
+  (void)block;
+  return launch_decode<256, F, S>(P, grid, smem, st);
+#else
   switch (block) {
   case 512: return launch_decode<512, F, S>(P, grid, smem, st);
   case 1024: return launch_decode<1024, F, S>(P, grid, smem, st);
   default: return launch_decode<256, F, S>(P, grid, smem, st);
   }
+#endif
 }
 
 template <int BLOCK, typename F, typename S>

@@ -77,10 +77,15 @@ constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the
 #ifndef AB_EXP_Q
 #define AB_EXP_Q 2
 #endif
+#ifndef AB_EXP_Q256
+#define AB_EXP_Q256 3 // 256-thread CTAs (many channels): larger tiles, fewer tile barriers
+#endif
 #ifndef AB_EXP_U
 #define AB_EXP_U 1
 #endif
-constexpr int EXP_Q = AB_EXP_Q; // inputs per thread per expansion tile (CSR range loads in flight)
+// inputs per thread per expansion tile (the tile arrays are static shared
+// memory: 20 bytes per input, under the 48 KB static limit at 1024 threads)
+template <int BLOCK> __host__ __device__ constexpr int exp_q() { return BLOCK <= 256 ? AB_EXP_Q256 : AB_EXP_Q; }
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
 #ifndef AB_PRUNE_Q
 #define AB_PRUNE_Q 4
@@ -1042,7 +1047,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       sh.cnt_tok += n_front; // token expansions of the reference's round
     }
     __syncthreads();
-    expand<BLOCK, EXP_Q, EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, (u32)rounds);
+    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, (u32)rounds);
     __syncthreads();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
@@ -1176,7 +1181,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   constexpr int QP = PRUNE_Q;
   constexpr u32 TILE = BLOCK * QP;
   // digit histograms of the split-bucket selection live in the expansion tile
-  constexpr int DB = (BLOCK * EXP_Q >= 2048) ? 11 : (BLOCK * EXP_Q >= 1024) ? 10 : (BLOCK * EXP_Q >= 512) ? 9 : 8;
+  constexpr int DB = (BLOCK * exp_q<BLOCK>() >= 2048) ? 11 : (BLOCK * exp_q<BLOCK>() >= 1024) ? 10 : (BLOCK * exp_q<BLOCK>() >= 512) ? 9 : 8;
   const int tid = threadIdx.x;
   const u32 n_rows = sh.flog_n;
   const u64 best_ck = sh.min_ck;
@@ -1538,7 +1543,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   next_epoch<BLOCK>(P, C, sh);
-  expand<BLOCK, EXP_Q, EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
+  expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
   __syncthreads();
   apply_kills<BLOCK>(P, C, sh);
   PROF_MARK(sh, PF_EMIT_X);
@@ -1812,10 +1817,10 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   __shared__ Shared sh;
   __shared__ Chan<F, S> C;
-  __shared__ double tile_cost[BLOCK * EXP_Q];
-  __shared__ u32 tile_a0[BLOCK * EXP_Q];
-  __shared__ u32 tile_pref[BLOCK * EXP_Q + 1];
-  __shared__ u32 tile_src[BLOCK * EXP_Q];
+  __shared__ double tile_cost[BLOCK * exp_q<BLOCK>()];
+  __shared__ u32 tile_a0[BLOCK * exp_q<BLOCK>()];
+  __shared__ u32 tile_pref[BLOCK * exp_q<BLOCK>() + 1];
+  __shared__ u32 tile_src[BLOCK * exp_q<BLOCK>()];
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
