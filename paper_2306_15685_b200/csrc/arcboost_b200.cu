@@ -22,6 +22,10 @@
 #include "scoring.h"
 #include "score_gen.cuh"
 #include "decode_kernel.cuh"
+#include "decode_instances.h"
+
+// compiled in csrc/kernels/*.cu
+AB_DECODE_ALL(AB_DECODE_EXTERN)
 
 using namespace ab;
 

@@ -1,0 +1,26 @@
+// The decode kernel's instantiations, one group per translation unit
+// (csrc/kernels/*.cu): each unit compiles only its group, so the hot C3
+// kernel (256 threads, 16-byte records, direct table, f32 scores) is
+// optimised on its own, and the units build in parallel.  The host ABI
+// (arcboost_b200.cu) declares them extern and launches them.
+#pragma once
+
+#define AB_DECODE_HOT(X) X(256, Fmt16<false>, float)
+#define AB_DECODE_F16D(X)                                                                               \
+  X(512, Fmt16<false>, float) X(1024, Fmt16<false>, float) X(256, Fmt16<false>, double)               \
+  X(512, Fmt16<false>, double) X(1024, Fmt16<false>, double)
+#define AB_DECODE_F16H(X)                                                                               \
+  X(256, Fmt16<true>, float) X(512, Fmt16<true>, float) X(1024, Fmt16<true>, float)                   \
+  X(256, Fmt16<true>, double) X(512, Fmt16<true>, double) X(1024, Fmt16<true>, double)
+#define AB_DECODE_F24D(X)                                                                               \
+  X(256, Fmt24<false>, float) X(512, Fmt24<false>, float) X(1024, Fmt24<false>, float)                \
+  X(256, Fmt24<false>, double) X(512, Fmt24<false>, double) X(1024, Fmt24<false>, double)
+#define AB_DECODE_F24H(X)                                                                               \
+  X(256, Fmt24<true>, float) X(512, Fmt24<true>, float) X(1024, Fmt24<true>, float)                   \
+  X(256, Fmt24<true>, double) X(512, Fmt24<true>, double) X(1024, Fmt24<true>, double)
+#define AB_DECODE_ALL(X) AB_DECODE_HOT(X) AB_DECODE_F16D(X) AB_DECODE_F16H(X) AB_DECODE_F24D(X) AB_DECODE_F24H(X)
+
+#define AB_DECODE_EXTERN(B, F, S) \
+  extern template __global__ void ab::decode_kernel<B, ab::F, S>(const __grid_constant__ ab::DecodeParams);
+#define AB_DECODE_INSTANCE(B, F, S) \
+  template __global__ void ab::decode_kernel<B, ab::F, S>(const __grid_constant__ ab::DecodeParams);
