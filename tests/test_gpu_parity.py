@@ -363,3 +363,47 @@ def test_extreme_beams_and_caps(beam, max_active):
     assert rc == 0
     _same(res.hypotheses, want, f"beam {beam} max_active {max_active}")
     assert len(ch.store) == info["store_len"]
+
+
+def test_full_size_launch_shapes_agree(monkeypatch):
+    """Race check at C3 scale (5M-state graph, 256 biased channels): 256-,
+    512- and 1024-thread CTAs and a short grid (several channels per CTA, in
+    a different order) give bit-identical hypotheses — the CAS recombination,
+    warp-aggregated row reservation and kill queues leave no trace of
+    scheduling — and two channels match the CPU oracle."""
+    import gc
+
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(5_000_000, 4, 2000, seed=421, f32_weights=True)
+    pool = synth.unigram_contexts(csr, 20, range(1000, 1008), num_labels=2000)
+    reg = ab.ContextRegistry({c.id: c for c in pool}, graph_fingerprint="")
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
+    n, T = 256, 24
+    mats = [ab.ScoreMatrix(synth.channel_scores(7, c, T, 2000)) for c in range(n)]
+
+    def run():
+        chans = [ab.init_channel(f"f{c}", reg, pool[c % 8].id, cfg) for c in range(n)]
+        res = ab.decode_batch(list(zip(chans, mats)), csr, reg, cfg)
+        out = [[(h.words, h.cost, h.frame, h.kind, h.hits) for h in r.hypotheses] for r in res]
+        assert all(r.error is None for r in res)
+        del chans, res
+        gc.collect()
+        return out
+
+    shapes = [("256", None), ("512", None), ("1024", None), ("256", "37")]
+    outs = []
+    for block, grid in shapes:
+        monkeypatch.setenv("AB_BLOCK", block)
+        if grid:
+            monkeypatch.setenv("AB_GRID", grid)
+        else:
+            monkeypatch.delenv("AB_GRID", raising=False)
+        outs.append(run())
+    for (block, grid), o in zip(shapes[1:], outs[1:]):
+        assert o == outs[0], (block, grid)
+    for c in (0, 131):
+        want, rc, _ = _oracle(csr, mats[c].costs, pool[c % 8], cfg)
+        assert rc == 0
+        assert [(h.words, h.cost, h.frame, h.kind, h.hits) for h in want] == outs[0][c], c
