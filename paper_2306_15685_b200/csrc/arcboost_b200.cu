@@ -838,6 +838,12 @@ static int ensure_batch(ab_decoder *d, size_t n) {
 static void fill_params(ab_decoder *d, DecodeParams &P) {
   ab_graph *g = d->g;
   memset(&P, 0, sizeof(P));
+#ifdef AB_PROFILE
+  static unsigned long long *prof = nullptr;
+  if (!prof && cudaMalloc(&prof, PF_N * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(prof, 0, PF_N * sizeof(unsigned long long));
+  P.prof = prof;
+#endif
   P.e_rng = g->e_rng;
   P.deg = g->deg;
   P.e_arcs = g->e_arcs;
@@ -1256,14 +1262,13 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
 #ifdef AB_PROFILE
   {
     unsigned long long pr[PF_N];
-    cudaMemcpyFromSymbol(pr, g_prof, sizeof(pr));
+    cudaMemcpy(pr, P.prof, sizeof(pr), cudaMemcpyDeviceToHost);
     static const char *names[PF_N] = {"start", "row", "emit_x", "emit_s", "eps_x", "eps_s",
                                       "prune_scan", "prune_sel", "prune_out", "hyp", "gc", "rounds"};
     fprintf(stderr, "AB_PROFILE");
     for (int q = 0; q < 12; ++q) fprintf(stderr, " %s=%llu", names[q], pr[q]);
     fprintf(stderr, "\n");
-    unsigned long long z[PF_N] = {};
-    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    cudaMemset(P.prof, 0, sizeof(pr));
   }
 #endif
   return AB_OK;

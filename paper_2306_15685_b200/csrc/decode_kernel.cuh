@@ -217,6 +217,7 @@ struct DecodeParams {
   const double *final_cost; // NaN = not final
   int start;
   int num_states;
+  unsigned long long *prof; // phase cycle counters (AB_PROFILE builds only)
   int L;
   const CtxDesc *ctxs;
   int num_ctxs;
@@ -420,11 +421,10 @@ __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
 
 // ------------------------------------------------------------ phase profile
 // Built with -DAB_PROFILE only (scripts/, never the shipped library): thread 0
-// accumulates SM clock cycles per phase; the kernel adds them to g_prof.
+// accumulates SM clock cycles per phase; the kernel adds them to P.prof.
 enum { PF_START = 0, PF_ROW, PF_EMIT_X, PF_EMIT_S, PF_EPS_X, PF_EPS_S, PF_PRUNE_SCAN, PF_PRUNE_SEL,
        PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_N = 16 };
 #ifdef AB_PROFILE
-__device__ unsigned long long g_prof[PF_N];
 #define PROF_MARK(sh, id)                                                                          \
   do {                                                                                             \
     if (threadIdx.x == 0) {                                                                        \
@@ -1903,7 +1903,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       P.errors[b] = sh.error;
       P.frames_done[b] = t;
 #ifdef AB_PROFILE
-      for (int q = 0; q < PF_N; ++q) atomicAdd(&g_prof[q], sh.prof[q]);
+      for (int q = 0; q < PF_N; ++q) atomicAdd(&P.prof[q], sh.prof[q]);
 #endif
     }
   }
