@@ -917,12 +917,16 @@ static int pick_block(int n) {
 template <int BLOCK, typename F, typename S>
 static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cudaStream_t st) {
   static int per_sm = -1, sms = 0;
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    // static tiles + dynamic (context, score row[, token table]) exceed the 48 KB default
+    const size_t want = std::max(dyn_smem_max(), smem);
+    cudaFuncSetAttribute(decode_kernel<BLOCK, F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    attr_set = want;
+  }
   if (per_sm < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    // static tiles + dynamic (context, score row) exceed the 48 KB default
-    cudaFuncSetAttribute(decode_kernel<BLOCK, F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)dyn_smem_max());
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<BLOCK, F, S>, BLOCK,
                                                       smem) != cudaSuccess || per_sm < 1)
@@ -936,6 +940,28 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   const int grid = (n + waves - 1) / waves;
   decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
   return cudaGetLastError();
+}
+
+// Whether a channel's direct token table (table_cap 16-byte values) fits in
+// shared memory next to the 1024-thread kernel's static tiles and the dynamic
+// context / score-row area (`smem`): then the table's loads and CAS-128s stay
+// on the SM (small graphs: C1 / C2's 10k states = 160 KB).
+template <typename S> static bool smem_table_fits(size_t smem, size_t table_cap) {
+  static int optin = -1;
+  static size_t stat = 0;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, decode_kernel<1024, Fmt16S, S>) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      optin = 0;
+    }
+    stat = fa.sharedSizeBytes;
+  }
+  if (getenv("AB_NO_SMEM_TABLE")) return false;
+  return stat + smem + table_cap * 16 <= (size_t)optin;
 }
 
 template <typename F, typename S>
@@ -997,7 +1023,7 @@ __global__ void pack_kernel(int n, const int *n_hyps, const long long *wused, co
 
 static size_t dyn_smem(int L, bool s64) {
   size_t row = (size_t)L * (s64 ? 8 : 4);
-  if (row > (size_t)SCORE_SMEM_MAX_BYTES) row = 0;
+  row = row > (size_t)SCORE_SMEM_MAX_BYTES ? 0 : (row + 15) / 16 * 16; // a shared-memory table follows
   return CTX_SMEM_WORDS * sizeof(u32) + row;
 }
 
@@ -1180,8 +1206,12 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       else le = s64 ? launch_decode_b<Fmt24<true>, double>(block, P, m, smem, st)
                     : launch_decode_b<Fmt24<true>, float>(block, P, m, smem, st);
     } else {
-      if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<false>, double>(block, P, m, smem, st)
-                             : launch_decode_b<Fmt16<false>, float>(block, P, m, smem, st);
+      if (g->fmt16 && block == 1024 && (s64 ? smem_table_fits<double>(smem, P.table_cap)
+                                            : smem_table_fits<float>(smem, P.table_cap)))
+        le = s64 ? launch_decode<1024, Fmt16S, double>(P, m, smem + (size_t)P.table_cap * 16, st)
+                 : launch_decode<1024, Fmt16S, float>(P, m, smem + (size_t)P.table_cap * 16, st);
+      else if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<false>, double>(block, P, m, smem, st)
+                                  : launch_decode_b<Fmt16<false>, float>(block, P, m, smem, st);
       else le = s64 ? launch_decode_b<Fmt24<false>, double>(block, P, m, smem, st)
                     : launch_decode_b<Fmt24<false>, float>(block, P, m, smem, st);
     }

@@ -136,8 +136,9 @@ struct __align__(16) XArc16 { u32 ns, g; float w; u32 ol; };
 struct __align__(8) EArc24 { u32 ns, g, il, ol; double w; };
 struct __align__(8) XArc24 { u32 ns, g, ol, pad; double w; };
 
-template <bool H> struct Fmt16 {
+template <bool H, bool SMT = false> struct Fmt16 {
   static constexpr bool hashed = H; // token table: hashed (true) or identity-mapped
+  static constexpr bool smem_table = SMT; // identity-mapped table in shared memory (small graphs)
   typedef EArc16 E;
   typedef XArc16 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -160,6 +161,7 @@ template <bool H> struct Fmt16 {
 };
 template <bool H> struct Fmt24 {
   static constexpr bool hashed = H;
+  static constexpr bool smem_table = false;
   typedef EArc24 E;
   typedef XArc24 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -184,6 +186,8 @@ template <bool H> struct Fmt24 {
     w = __ldg(&p->w);
   }
 };
+
+typedef Fmt16<false, true> Fmt16S; // direct table in shared memory (one macro argument)
 
 struct ChanState {
   ab_channel_info info; // info.store_len = records appended this utterance (reference len(store))
@@ -288,41 +292,53 @@ __device__ __forceinline__ void ld_cg_head(const Entry *e, u64 &key, u32 &flog) 
   key = a;
   flog = (u32)b;
 }
-__device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
+// Value accessors; SM = the table lives in shared memory (Fmt::smem_table).
+template <bool SM = false> __device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
   u64 a, b;
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v));
+  if (SM) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(v);
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(sa) : "memory");
+  } else {
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v));
+  }
   ck = a;
   g = (u32)b;
   info = (u32)(b >> 32);
 }
+// CAS-128 that only issues: the old value comes back in (r0, r1); the caller
+// compares, so several can be in flight per thread.
+template <bool SM = false>
+__device__ __forceinline__ void cas128(u64 *addr, u64 e0, u64 e1, u64 d0, u64 d1, u64 &r0, u64 &r1) {
+  if (SM) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(addr);
+    asm volatile(
+        "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
+        " atom.shared.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
+        : "=l"(r0), "=l"(r1)
+        : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "r"(sa)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
+        " atom.global.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
+        : "=l"(r0), "=l"(r1)
+        : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(addr)
+        : "memory");
+  }
+}
+
 // 128-bit compare-and-swap on the value half of an entry (ATOMG.E.CAS.128).
-__device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng,
-                                          u32 ninfo) {
+template <bool SM = false>
+__device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng, u32 ninfo) {
   u64 e0 = ck, e1 = ((u64)info << 32) | g;
   u64 d0 = nck, d1 = ((u64)ninfo << 32) | ng;
   u64 r0, r1;
-  asm volatile(
-      "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
-      " atom.global.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
-      : "=l"(r0), "=l"(r1)
-      : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(v)
-      : "memory");
+  cas128<SM>(v, e0, e1, d0, d1, r0, r1);
   bool ok = (r0 == e0) && (r1 == e1);
   ck = r0;
   g = (u32)r1;
   info = (u32)(r1 >> 32);
   return ok;
-}
-
-// CAS-128 that only issues: the old value comes back in (r0, r1); the caller
-// compares, so several can be in flight per thread.
-__device__ __forceinline__ void cas128(u64 *addr, u64 e0, u64 e1, u64 d0, u64 d1, u64 &r0, u64 &r1) {
-  asm volatile(
-      "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
-      " atom.global.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
-      : "=l"(r0), "=l"(r1)
-      : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(addr)
-      : "memory");
 }
 
 // L2 prefetch: memory-level parallelism that costs no registers
@@ -396,6 +412,18 @@ __device__ __forceinline__ void block_argmin(u64 &key, u32 &state, int &idx, u64
 // the lanes that are converged here (one shared atomic per group): the
 // entries of a warp are contiguous, so its stores to them coalesce.
 __device__ __forceinline__ u32 agg_reserve(u32 *counter, u32 n) {
+  // one request per lane (the usual case): ballot + popc, one atomic per warp
+  // (the cooperative-groups path below finds lanes in software)
+  const u32 act = __activemask();
+  if (__all_sync(act, n <= 1u)) {
+    const u32 m = __ballot_sync(act, n != 0);
+    if (!m) return 0;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    u32 base = 0;
+    if (lane == leader) base = atomicAdd(counter, (u32)__popc(m));
+    base = __shfl_sync(act, base, leader);
+    return base + (u32)__popc(m & ((1u << lane) - 1u));
+  }
   namespace cg = cooperative_groups;
   cg::coalesced_group grp = cg::coalesced_threads();
   const u32 excl = cg::exclusive_scan(grp, n, cg::plus<u32>());
@@ -490,6 +518,7 @@ template <typename F, typename S> struct Chan {
   ChanState *cs;
   Entry *table;
   u64 *vals;
+  u64 *gvals; // the channel's global direct table (wiped with a shared-memory table)
   u32 *tok_state;
   double *tok_cost;
   TokInfo *tok_info;
@@ -639,7 +668,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
     }
     const u32 old_info = vinfo;
     const u64 old_ck = vck;
-    if (cas_value(v, vck, vg, vinfo, ck, g, info)) {
+    if (cas_value<F::smem_table>(v, vck, vg, vinfo, ck, g, info)) {
       installed(P, C, sh, acc, round, etag, old_info, old_ck, ck);
       return;
     }
@@ -719,7 +748,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
         u32 fl;
         ld_cg_head(&C.table[slot[u]], key[u], fl);
       }
-      ld_cg_value(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
+      ld_cg_value<F::smem_table>(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
     }
   }
   bool fast[U];
@@ -783,7 +812,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (want[u])
-      cas128(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u], ((u64)ninfo[u] << 32) | g[u],
+      cas128<F::smem_table>(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u], ((u64)ninfo[u] << 32) | g[u],
              r0[u], r1[u]);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -1405,6 +1434,10 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     } else {
       uint4 *v = reinterpret_cast<uint4 *>(C.vals);
       for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) v[i] = make_uint4(0, 0, 0, 0);
+      if (F::smem_table && C.gvals) { // keep the global table's tags consistent for later launches
+        uint4 *gv = reinterpret_cast<uint4 *>(C.gvals);
+        for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) gv[i] = make_uint4(0, 0, 0, 0);
+      }
     }
     e += 1;
   }
@@ -1745,6 +1778,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     const size_t s = (size_t)slot;
     C.table = P.table ? P.table + s * P.table_cap : nullptr;
     C.vals = P.vals ? P.vals + 2 * s * P.table_cap : nullptr;
+    C.gvals = C.vals;
     C.tok_state = P.tok_state + s * P.tok_cap;
     C.tok_cost = P.tok_cost + s * P.tok_cap;
     C.tok_info = P.tok_info + (2 * s + (C.cs->tok_half & 1u)) * P.tok_cap;
@@ -1824,10 +1858,18 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
+  // small graphs: the channel's direct token table in shared memory, after
+  // the context words and the score row (host: smem_table_bytes)
+  uint4 *sh_table = reinterpret_cast<uint4 *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32) +
+                                              (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
   for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
     setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src);
     ChanState *cs = C.cs;
+    if (F::smem_table) { // a fresh table per channel: zero tags are never current
+      for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) sh_table[i] = make_uint4(0, 0, 0, 0);
+    }
     if (threadIdx.x == 0) {
+      if (F::smem_table) C.vals = reinterpret_cast<u64 *>(sh_table);
       sh.error = 0;
       sh.rec_n = cs->rec_phys;
       sh.rec_logical = (unsigned long long)cs->info.store_len;
