@@ -974,10 +974,19 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     }
     __syncthreads();
   }
-  if (acc.min_ck != ~0ull) atomicMin(&sh.min_ck, acc.min_ck);
-  if (acc.n_rec) atomicAdd(&sh.n_rec_frame, acc.n_rec);
-  if (acc.n_app) atomicAdd(&sh.n_app, acc.n_app);
-  if (acc.n_new && atomicAdd(&sh.n_new, acc.n_new) + acc.n_new > P.tok_cap) set_error(sh, E_CAP);
+  // per-warp totals first: one shared atomic per warp and counter
+  u64 mck = acc.min_ck;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mck = min(mck, __shfl_xor_sync(0xFFFFFFFFu, mck, o));
+  const int n_rec = __reduce_add_sync(0xFFFFFFFFu, acc.n_rec);
+  const u32 n_app = __reduce_add_sync(0xFFFFFFFFu, acc.n_app);
+  const u32 n_new = __reduce_add_sync(0xFFFFFFFFu, acc.n_new);
+  if ((tid & 31) == 0) {
+    if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
+    if (n_rec) atomicAdd(&sh.n_rec_frame, n_rec);
+    if (n_app) atomicAdd(&sh.n_app, n_app);
+    if (n_new && atomicAdd(&sh.n_new, n_new) + n_new > P.tok_cap) set_error(sh, E_CAP);
+  }
   if (tid == 0) {
     sh.n_cand += arcs_seen;
     if (EMIT) sh.cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
@@ -991,16 +1000,19 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 template <int BLOCK, typename F, typename S>
 __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const u32 n = min(sh.n_kill, P.flog_cap);
+  u32 unrec = 0;
   for (u32 i = threadIdx.x; i < n; i += BLOCK) {
     const u32 v = C.app_list[i];
     const u32 row = v & VROW_MASK;
     const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
     if (v & KILL_DISP) { // a displaced row is no application (no record) and leaves the epsilon frontier
-      if (old & ROW_HASOL) atomicSub(&sh.n_rec_frame, 1);
+      if (old & ROW_HASOL) unrec++;
       const u32 ep = C.flog_aux[row].y;
       if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
     }
   }
+  unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
+  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&sh.n_rec_frame, unrec);
   __syncthreads();
   if (threadIdx.x == 0) sh.n_kill = 0;
   __syncthreads();
@@ -1112,7 +1124,8 @@ __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared
     C.tok_info_alt[i] = t;
     if ((int)r == best_row) sh.best_last_il = t.last_il;
   }
-  atomicMax(&sh.max_depth, md);
+  md = __reduce_max_sync(0xFFFFFFFFu, md);
+  if ((threadIdx.x & 31) == 0) atomicMax(&sh.max_depth, md);
   __syncthreads();
   if (threadIdx.x == 0) {
     C.cs->max_depth = sh.max_depth;
@@ -1398,7 +1411,8 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
     const u32 i = i0 + threadIdx.x;
     const u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
     const bool live = !(st & (ROW_DEAD | ROW_DISP));
-    if ((st & (ROW_DISP | ROW_HASOL)) == ROW_HASOL) atomicAdd(&sh.rec_logical, 1ull);
+    const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, (st & (ROW_DISP | ROW_HASOL)) == ROW_HASOL));
+    if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&sh.rec_logical, (unsigned long long)nrec);
     u32 total;
     const u32 p = n_tok + block_excl_scan<BLOCK>(live ? 1u : 0u, total, sh.scan);
     if (live) {
