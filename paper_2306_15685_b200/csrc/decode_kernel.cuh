@@ -77,6 +77,9 @@ constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the
 #ifndef AB_EXP_Q
 #define AB_EXP_Q 2
 #endif
+#ifndef AB_WARP_TILES_MIN_BLOCK
+#define AB_WARP_TILES_MIN_BLOCK 1024
+#endif
 #ifndef AB_EXP_Q256
 #define AB_EXP_Q256 3 // 256-thread CTAs (many channels): larger tiles, fewer tile barriers
 #endif
@@ -839,6 +842,10 @@ template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const uint4 *list, u32 n_in,
                        u32 round) {
   constexpr u32 TILE = BLOCK * Q;
+  // 1024-thread CTAs (one channel alone on its SM, C1 / C2): warp-private
+  // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
+  // with other channels, which hide the tile barrier (CTA-wide tiles)
+  constexpr bool WARP_TILES = AB_WARP_TILES_MIN_BLOCK > 0 && BLOCK >= AB_WARP_TILES_MIN_BLOCK;
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
   u32 *t_src = C.t_src;
@@ -853,6 +860,142 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   acc.n_app = 0;
   acc.n_rec = 0;
   u32 arcs_seen = 0;
+  if constexpr (WARP_TILES) {
+  // Each warp works through its own sub-tiles (32 * Q inputs; smaller when
+  // the input is short, so every warp gets some): a warp-level scan of the
+  // out-degrees, then its 32 lanes walk the sub-tile's arcs.  No block
+  // barrier inside the pass, so a warp never waits for the slowest warp of
+  // the CTA between tiles.
+  constexpr u32 NW = BLOCK / 32;
+  constexpr u32 WT = 32 * Q;
+  const u32 lane = (u32)tid & 31u, wid = (u32)tid >> 5;
+  u32 *w_a0 = t_a0 + wid * WT;
+  u32 *w_pref = t_pref + wid * WT;
+  u32 *w_src = t_src + wid * WT;
+  double *w_cost = t_cost + wid * WT;
+  const u32 per = n_in >= NW * WT ? WT : max(1u, (n_in + NW - 1) / NW);
+  for (u32 base = wid * per; base < n_in; base += NW * per) {
+    const u32 ne = min(per, n_in - base);
+    u32 idx[Q], st[Q], a0[Q], cnt[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const u32 j = lane * Q + q;
+      idx[q] = 0xFFFFFFFFu;
+      st[q] = ROW_DISP;
+      if (j < ne) {
+        if (EMIT) {
+          idx[q] = base + j;
+          st[q] = C.tok_state[idx[q]];
+          w_cost[j] = C.tok_cost[idx[q]];
+        } else { // epsilon-frontier entries carry the row's state, flags and cost
+          const uint4 e = list[base + j];
+          idx[q] = e.x;
+          st[q] = e.y;
+          w_cost[j] = key_cost(((u64)e.w << 32) | e.z);
+        }
+        w_src[j] = idx[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      a0[q] = 0;
+      cnt[q] = 0;
+      if (EMIT ? (idx[q] != 0xFFFFFFFFu) : !(st[q] & ROW_DISP)) {
+        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
+        const u32 dg = __ldg(&P.deg[s]);
+        const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
+        if (c == DEG_OVF) {
+          const uint2 r = __ldg(&rng[s]);
+          a0[q] = r.x;
+          cnt[q] = r.y - r.x;
+        } else {
+          a0[q] = s * SLOT;
+          cnt[q] = c;
+        }
+      }
+    }
+    u32 tsum = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) tsum += cnt[q];
+    u32 incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (u32)o) incl += y;
+    }
+    const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    u32 run = incl - tsum;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const u32 j = lane * Q + q;
+      if (j < ne) {
+        w_a0[j] = a0[q];
+        w_pref[j] = run;
+      }
+      run += cnt[q];
+    }
+    __syncwarp();
+    arcs_seen += total;
+    for (u32 k0 = lane; k0 < total; k0 += 32 * U) {
+      bool on[U];
+      u32 a[U], src[U];
+      double cj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const u32 k = k0 + u * 32;
+        on[u] = k < total;
+        a[u] = 0;
+        src[u] = 0;
+        cj[u] = 0.0;
+        if (on[u]) {
+          u32 lo = 0, hi = ne - 1; // largest j with w_pref[j] <= k (its range holds k)
+          while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (w_pref[mid] <= k) lo = mid;
+            else hi = mid - 1;
+          }
+          a[u] = w_a0[lo] + (k - w_pref[lo]);
+          src[u] = w_src[lo];
+          cj[u] = w_cost[lo];
+        }
+      }
+      u32 d[U], g[U], il[U], ol[U];
+      double w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        d[u] = g[u] = il[u] = ol[u] = 0;
+        w[u] = 0.0;
+        if (on[u]) {
+          if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
+          else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
+        }
+      }
+      u64 ck[U];
+      u32 rflags[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ck[u] = 0;
+        rflags[u] = 0;
+        if (on[u]) {
+          // _effective_weights (decoder.py:234-240): boost fused into the cost add
+          const bool bst = is_boosted(C, g[u] & G_MASK, ol[u]);
+          const double we = bst ? w[u] + C.discount : w[u];
+          double cand;
+          if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
+          else cand = cj[u] + we;                                    // decoder.py:268
+          ck[u] = cost_key(cand);
+          rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
+        }
+      }
+      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && arcs_seen) {
+    atomicAdd(&sh.n_cand, arcs_seen);
+    atomicAdd(EMIT ? &sh.cnt_emit : &sh.cnt_eps, (unsigned long long)arcs_seen);
+  }
+  } else {
   for (u32 base = 0; base < n_in; base += TILE) {
     const u32 i0 = base + (u32)tid * Q;
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
@@ -974,6 +1117,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     }
     __syncthreads();
   }
+  }
   // per-warp totals first: one shared atomic per warp and counter
   u64 mck = acc.min_ck;
 #pragma unroll
@@ -988,10 +1132,12 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     if (n_new && atomicAdd(&sh.n_new, n_new) + n_new > P.tok_cap) set_error(sh, E_CAP);
   }
   if (tid == 0) {
-    sh.n_cand += arcs_seen;
     if (EMIT) sh.cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
-    if (EMIT) sh.cnt_emit += arcs_seen;
-    else sh.cnt_eps += arcs_seen;
+    if (!WARP_TILES) {
+      sh.n_cand += arcs_seen;
+      if (EMIT) sh.cnt_emit += arcs_seen;
+      else sh.cnt_eps += arcs_seen;
+    }
   }
 }
 
