@@ -935,7 +935,6 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   int resident = std::max(1, per_sm * sms);
   const char *env = getenv("AB_GRID");
   if (env && atoi(env) > 0) resident = atoi(env);
-  if (const char *l2 = getenv("AB_L2FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
   const int waves = (n + resident - 1) / resident;
   const int grid = (n + waves - 1) / waves;
   decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
