@@ -289,11 +289,15 @@ __device__ __forceinline__ double key_cost(u64 k) {
   return __longlong_as_double((long long)b);
 }
 
-__device__ __forceinline__ void ld_cg_head(const Entry *e, u64 &key, u32 &flog) {
-  u64 a, b;
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(&e->key));
+// whole 32-byte hashed entry in one request (key and value)
+__device__ __forceinline__ void ld_cg_entry(const Entry *e, u64 &key, u64 &ck, u32 &g, u32 &info) {
+  u64 a, b, c, d;
+  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(e));
+  (void)b; // the entry's row field is not needed here
   key = a;
-  flog = (u32)b;
+  ck = c;
+  g = (u32)d;
+  info = (u32)(d >> 32);
 }
 // Value accessors; SM = the table lives in shared memory (Fmt::smem_table).
 template <bool SM = false> __device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
@@ -700,9 +704,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
       set_error(sh, E_CAP);
       return;
     }
-    u32 fl;
-    ld_cg_head(&C.table[slot], key, fl);
-    ld_cg_value(val_at(C, slot), vck, vg, vinfo);
+    ld_cg_entry(&C.table[slot], key, vck, vg, vinfo);
   }
   if (!value_better(ck, g, round, C.etag, vck, vg, vinfo)) return;
   const u32 row = atomicAdd(&sh.flog_n, 1u);
@@ -747,11 +749,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     vg[u] = 0;
     vinfo[u] = 0;
     if (on[u]) {
-      if (F::hashed) {
-        u32 fl;
-        ld_cg_head(&C.table[slot[u]], key[u], fl);
-      }
-      ld_cg_value<F::smem_table>(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
+      if (F::hashed) ld_cg_entry(&C.table[slot[u]], key[u], vck[u], vg[u], vinfo[u]);
+      else ld_cg_value<F::smem_table>(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
     }
   }
   bool fast[U];
