@@ -293,7 +293,7 @@ __device__ __forceinline__ double key_cost(u64 k) {
 __device__ __forceinline__ void ld_cg_entry(const Entry *e, u64 &key, u64 &ck, u32 &g, u32 &info) {
   u64 a, b, c, d;
   asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(e));
-  (void)b; // the entry's row field is not needed here
+  asm volatile("" ::"l"(b)); // the entry's row field is not needed here
   key = a;
   ck = c;
   g = (u32)d;
