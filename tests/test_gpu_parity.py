@@ -407,3 +407,46 @@ def test_full_size_launch_shapes_agree(monkeypatch):
         want, rc, _ = _oracle(csr, mats[c].costs, pool[c % 8], cfg)
         assert rc == 0
         assert [(h.words, h.cost, h.frame, h.kind, h.hits) for h in want] == outs[0][c], c
+
+
+def test_smem_token_table_matches_global(monkeypatch):
+    """Small graphs at 1024 threads keep the token table in shared memory.
+    It must give the same hypotheses as the HBM table, and alternating the
+    two across calls on the same channels (epoch tags wrapping every 127
+    frames in between) must not let a stale tag of either table alias."""
+    import gc
+
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    pool = synth.unigram_contexts(csr, 20, range(1000, 1004), num_labels=2000)
+    reg = ab.ContextRegistry({c.id: c for c in pool}, graph_fingerprint="")
+    cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
+    n, T = 4, 140
+    utts = [[ab.ScoreMatrix(synth.channel_scores(30 + u, c, T, 2000)) for c in range(n)] for u in range(3)]
+
+    def run(modes):
+        chans = [ab.init_channel(f"s{c}", reg, pool[c].id, cfg) for c in range(n)]
+        out = []
+        for u, smem in enumerate(modes):
+            if smem:
+                monkeypatch.delenv("AB_NO_SMEM_TABLE", raising=False)
+            else:
+                monkeypatch.setenv("AB_NO_SMEM_TABLE", "1")
+            res = ab.decode_batch(list(zip(chans, utts[u])), csr, reg, cfg)
+            assert all(r.error is None for r in res)
+            out.append([[(h.words, h.cost, h.frame, h.kind, h.hits) for h in r.hypotheses] for r in res])
+        del chans
+        gc.collect()
+        return out
+
+    monkeypatch.setenv("AB_BLOCK", "1024")
+    ref = run([False, False, False])
+    assert run([True, True, True]) == ref
+    assert run([True, False, True]) == ref
+    assert run([False, True, False]) == ref
+    for c in range(2):
+        want, rc, _ = _oracle(csr, utts[0][c].costs, pool[c], cfg)
+        assert rc == 0
+        assert [(h.words, h.cost, h.frame, h.kind, h.hits) for h in want] == ref[0][c]
