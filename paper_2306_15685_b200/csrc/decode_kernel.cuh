@@ -80,6 +80,14 @@ constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the
 #ifndef AB_WARP_TILES_MIN_BLOCK
 #define AB_WARP_TILES_MIN_BLOCK 1024
 #endif
+// Frontier rows and epsilon entries are read back only after the rest of the
+// pass: with many channels per SM (256-thread CTAs, DRAM-bound) they are
+// stored evict-first so L2 keeps the token-table lines between load and CAS;
+// a 1024-thread CTA (few channels, L2-resident working set) stores normally.
+template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T v) {
+  if (BLOCK <= 256) __stcs(p, v);
+  else *p = v;
+}
 #ifndef AB_EXP_Q256
 #define AB_EXP_Q256 3 // 256-thread CTAs (many channels): larger tiles, fewer tile barriers
 #endif
@@ -731,7 +739,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
 // is issued for all U candidates before any result is consumed: loads of the
 // slots, key claims (hashed tables), row writes, value CAS-128s.  Lost races
 // and probe chains fall back to the sequential path.
-template <int U, typename F, typename S>
+template <int BLOCK, int U, typename F, typename S>
 __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
                                             const bool (&on)[U], const u32 (&d)[U], const u64 (&ck)[U],
                                             const u32 (&g)[U], const u32 (&src)[U], const u32 (&rflags)[U],
@@ -801,11 +809,11 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     rows[u] = row++;
     if (rflags[u] & ROW_EPS) { // next round's epsilon frontier
       eps_pos[u] = ep_at++;
-      C.eps_list[eps_pos[u]] = make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32));
+      st_row<BLOCK>(&C.eps_list[eps_pos[u]], make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32)));
     }
-    C.flog_state[rows[u]] = d[u] | rflags[u];
-    C.flog_ck[rows[u]] = ck[u];
-    C.flog_aux[rows[u]] = make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]);
+    st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | rflags[u]);
+    st_row<BLOCK>(&C.flog_ck[rows[u]], (unsigned long long)ck[u]);
+    st_row<BLOCK>(&C.flog_aux[rows[u]], make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]));
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
     acc.n_rec += (rflags[u] & ROW_HASOL) ? 1 : 0;
     ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
@@ -986,7 +994,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
     }
     __syncwarp();
   }
@@ -1112,7 +1120,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
     }
     __syncthreads();
   }
