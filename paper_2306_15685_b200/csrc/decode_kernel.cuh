@@ -84,6 +84,11 @@ constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the
 // pass: with many channels per SM (256-thread CTAs, DRAM-bound) they are
 // stored evict-first so L2 keeps the token-table lines between load and CAS;
 // a 1024-thread CTA (few channels, L2-resident working set) stores normally.
+// How a displaced row leaves the next round's epsilon frontier: 1024-thread
+// CTAs (L2-resident rows) check the row's DISP flag when the round lists its
+// entries; smaller CTAs (rows evicted to DRAM by then) mark the entry when the
+// kill is applied, so listing needs no second read.
+template <int BLOCK> __host__ __device__ constexpr bool disp_at_listing() { return BLOCK >= 1024; }
 template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T v) {
   if (BLOCK <= 256) __stcs(p, v);
   else *p = v;
@@ -668,7 +673,7 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
 
 // CAS retry loop after a lost race; the candidate's row is `row`.  A
 // candidate that stops being better marks its own row displaced.
-template <typename F, typename S>
+template <bool MARK_EPS, typename F, typename S>
 __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
                             u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row,
                             u32 eps_pos, bool hasol) {
@@ -676,7 +681,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
   while (true) {
     if (!value_better(ck, g, round, etag, vck, vg, vinfo)) {
       atomicOr(&C.flog_state[row], ROW_DISP);
-      if (eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
+      if (MARK_EPS && eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
       atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
       acc.n_rec -= hasol ? 1 : 0;
       return;
@@ -731,7 +736,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
   acc.n_rec += (rflags & ROW_HASOL) ? 1 : 0;
   const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
-  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos,
+  relax_retry<true>(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos,
               (rflags & ROW_HASOL) != 0);
 }
 
@@ -830,7 +835,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u]))
       installed(P, C, sh, acc, round, etag, vinfo[u], vck[u], ck[u]);
     else
-      relax_retry(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
+      relax_retry<!disp_at_listing<BLOCK>()>(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
                   (u32)(r1[u] >> 32), rows[u], eps_pos[u], (rflags[u] & ROW_HASOL) != 0);
   }
 }
@@ -853,6 +858,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
   // with other channels, which hide the tile barrier (CTA-wide tiles)
   constexpr bool WARP_TILES = AB_WARP_TILES_MIN_BLOCK > 0 && BLOCK >= AB_WARP_TILES_MIN_BLOCK;
+  constexpr bool DISP_AT_LISTING = disp_at_listing<BLOCK>();
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
   u32 *t_src = C.t_src;
@@ -897,7 +903,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         } else { // epsilon-frontier entries carry the row's state, flags and cost
           const uint4 e = list[base + j];
           idx[q] = e.x;
-          st[q] = e.y;
+          st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
           w_cost[j] = key_cost(((u64)e.w << 32) | e.z);
         }
         w_src[j] = idx[q];
@@ -907,7 +913,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     for (int q = 0; q < Q; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (EMIT ? (idx[q] != 0xFFFFFFFFu) : !(st[q] & ROW_DISP)) {
+      // (with the DISP check at listing, the degree load does not wait for it)
+      if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
         const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
         const u32 dg = __ldg(&P.deg[s]);
         const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
@@ -919,6 +926,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           a0[q] = s * SLOT;
           cnt[q] = c;
         }
+        if (!EMIT && (st[q] & ROW_DISP)) cnt[q] = 0; // displaced: not expanded
       }
     }
     u32 tsum = 0;
@@ -1027,7 +1035,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         if (i0 + q < n_in) {
           const uint4 e = list[i0 + q];
           idx[q] = e.x;
-          st[q] = e.y;
+          st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
           t_cost[j] = key_cost(((u64)e.w << 32) | e.z);
         }
         t_src[j] = idx[q];
@@ -1037,7 +1045,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     for (int q = 0; q < Q; ++q) {
       a0[q] = 0;
       cnt[q] = 0;
-      if (EMIT ? (idx[q] != 0xFFFFFFFFu) : !(st[q] & ROW_DISP)) {
+      // (with the DISP check at listing, the degree load does not wait for it)
+      if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
         const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
         const u32 dg = __ldg(&P.deg[s]);
         const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
@@ -1049,6 +1058,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           a0[q] = s * SLOT;
           cnt[q] = c;
         }
+        if (!EMIT && (st[q] & ROW_DISP)) cnt[q] = 0; // displaced: not expanded
       }
     }
     u32 tsum = 0;
@@ -1160,8 +1170,10 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
     const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
     if (v & KILL_DISP) { // a displaced row is no application (no record) and leaves the epsilon frontier
       if (old & ROW_HASOL) unrec++;
-      const u32 ep = C.flog_aux[row].y;
-      if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
+      if (!disp_at_listing<BLOCK>()) {
+        const u32 ep = C.flog_aux[row].y;
+        if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
+      }
     }
   }
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
