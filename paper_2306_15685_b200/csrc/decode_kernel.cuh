@@ -93,6 +93,9 @@ template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T 
   if (BLOCK <= 256) __stcs(p, v);
   else *p = v;
 }
+#ifndef AB_EXP_Q1024
+#define AB_EXP_Q1024 1 // 1024-thread CTAs: 32-input warp sub-tiles
+#endif
 #ifndef AB_EXP_Q256
 #define AB_EXP_Q256 3 // 256-thread CTAs (many channels): larger tiles, fewer tile barriers
 #endif
@@ -101,7 +104,9 @@ template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T 
 #endif
 // inputs per thread per expansion tile (the tile arrays are static shared
 // memory: 20 bytes per input, under the 48 KB static limit at 1024 threads)
-template <int BLOCK> __host__ __device__ constexpr int exp_q() { return BLOCK <= 256 ? AB_EXP_Q256 : AB_EXP_Q; }
+template <int BLOCK> __host__ __device__ constexpr int exp_q() {
+  return BLOCK <= 256 ? AB_EXP_Q256 : (BLOCK >= 1024 ? AB_EXP_Q1024 : AB_EXP_Q);
+}
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
 #ifndef AB_PRUNE_Q
 #define AB_PRUNE_Q 4
