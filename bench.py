@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-overhead", action="store_true", help="skip the unbiased / zero-discount runs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--parity-channels", type=int, default=16,
+                   help="channels whose every segment is checked against the oracle")
     p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
     p.add_argument("--c4-kind", choices=["words", "arcs"], default="words",
                    help="c4 contexts: unigram word sets (density x L words) or uniform random arcs")
@@ -89,6 +91,10 @@ def workload(args):
 # ----------------------------------------------------------------- distributed
 
 def dist_setup(args):
+    """One process per GPU (torchrun env).  The GPU is LOCAL_RANK modulo the
+    visible devices, so a world larger than the box (e.g. 2 ranks on one GPU)
+    still runs: its control plane is gloo then (NCCL rejects two ranks on one
+    device); the data path has no collective either way."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -96,9 +102,14 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
 
+        backend = "gloo"
         if args.impl == "b200":
+            n_dev = max(1, torch.cuda.device_count())
+            local = local % n_dev
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+            backend = "nccl" if local_world <= n_dev else "gloo"
+        dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -109,26 +120,28 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(x: float, world: int, device) -> float:
+def _reduce(x: float, world: int, device, op) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
+    dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    import torch.distributed as dist
+
+    return _reduce(x, world, device, dist.ReduceOp.MAX) if world > 1 else x
 
 
 def sum_over_ranks(x: float, world: int, device) -> float:
-    if world == 1:
-        return x
-    import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, world, device, dist.ReduceOp.SUM) if world > 1 else x
 
 
 # ---------------------------------------------------------------------- clocks
@@ -245,15 +258,31 @@ def ctx_index(c: int, seg: int, n_pool: int) -> int:
     return (c * 131 + seg * 17) % n_pool
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def oracle_decode_sample(csr, pool, scores, W, cfg, budget_s: float, threads: int = 1,
-                         channels=None):
-    """CPU oracle over channels' first segment until the time budget is spent."""
+                         channels=None, og=None):
+    """CPU oracle over whole channels - every segment, with the workload's
+    context switch at each segment boundary, on one persistent oracle channel
+    (the GPU's schedule) - until the time budget is spent.  Returns
+    {channel: [(hyps, rc) per segment]}, frames decoded, seconds."""
     from concurrent.futures import ThreadPoolExecutor
 
-    from oracle.oracle import OracleGraph, decode_stream
+    from oracle.oracle import OracleChannel, OracleGraph, decode_stream
 
-    og = OracleGraph.from_csr(csr)
-    Tseg = W["frames"] // W["segments"]
+    og = og or OracleGraph.from_csr(csr)
+    S = W["segments"]
+    Tseg = W["frames"] // S
     C = W["channels"]
     order = list(channels) if channels is not None else list(range(C))
     results = {}
@@ -261,18 +290,22 @@ def oracle_decode_sample(csr, pool, scores, W, cfg, budget_s: float, threads: in
     t0 = time.perf_counter()
 
     def one(c):
-        ctx = pool[ctx_index(c, 0, len(pool))] if pool else None
-        hyps, rc = decode_stream(og, scores[c, :Tseg].astype(np.float64), ctx, cfg)
-        return c, hyps, rc
+        ch = OracleChannel(og)
+        segs = []
+        for seg in range(S):
+            ctx = pool[ctx_index(c, seg, len(pool))] if pool else None
+            segs.append(decode_stream(og, scores[c, seg * Tseg:(seg + 1) * Tseg].astype(np.float64),
+                                      ctx, cfg, channel=ch))
+        return c, segs
 
     i = 0
     with ThreadPoolExecutor(max_workers=threads) as ex:
         while i < len(order) and (time.perf_counter() - t0 < budget_s or frames_done == 0):
             batch = order[i:i + threads]
             i += len(batch)
-            for c, hyps, rc in ex.map(one, batch):
-                results[c] = (hyps, rc)
-                frames_done += Tseg
+            for c, segs in ex.map(one, batch):
+                results[c] = segs
+                frames_done += Tseg * S
     dt = time.perf_counter() - t0
     return results, frames_done, dt
 
@@ -345,8 +378,8 @@ def run_b200(args, W, world, rank, local):
                 raise RuntimeError(f"device errors in segment {seg}: {np.unique(er)}")
             kernel_ms += dec.last_kernel_ms()
             launches += dec.last_launch_count()
-            if collect and seg == 0:
-                out["seg0"] = (nh.copy(), hyps, stride, words.copy())
+            if collect:
+                out.setdefault("segs", []).append((nh.copy(), hyps, stride, words.copy()))
             out["d2h_bytes"] = out.get("d2h_bytes", 0) + int(nh.sum()) * 48 + int(words.nbytes)
         infos = dec.get_many(slots)
         out["counters"] = (sum(i.tok_expansions for i in infos), sum(i.emit_arcs for i in infos),
@@ -445,22 +478,38 @@ def run_b200(args, W, world, rank, local):
                          "d2h_bytes_per_step": int(eouts[-1]["d2h_bytes"]),
                          "path": "C ABI ab_decode with pinned host scores (BatchDecoder.decode)"}
     if rank == 0 and not args.no_cpu:
-        # CPU oracle on a bounded sample of the same workload + parity on that sample
-        res, nfr, dt = oracle_decode_sample(csr, pool, scores_np, W, cfg, args.cpu_seconds, 1)
-        nh, hyps, stride, words = first["seg0"]
-        ok = True
-        for c, (oh, rc) in res.items():
-            last, got = [], []
-            for q in range(int(nh[c])):
-                x = hyps[c * stride + q]
-                w = last[:x.shared] + words[x.words_off:x.words_off + x.n_words - x.shared].tolist()
-                last = w if x.kind == 0 else []
-                got.append((w, x.cost, x.hits))
-            ok &= rc == 0 and got == [(h.words, h.cost, h.hits) for h in oh]
+        from oracle.oracle import OracleGraph
+
+        og = OracleGraph.from_csr(csr)
+        # CPU oracle timed on a bounded sample of the same workload (whole
+        # channels: every segment and context switch), 1 thread
+        res, nfr, dt = oracle_decode_sample(csr, pool, scores_np, W, cfg, args.cpu_seconds, 1, og=og)
+        # parity: the first channels, all segments, every hypothesis, against
+        # the oracle run with every host thread (not timed)
+        n_par = min(C, args.parity_channels)
+        par, _, _ = oracle_decode_sample(csr, pool, scores_np, W, cfg, 0.0, os.cpu_count() or 1,
+                                         channels=range(n_par), og=og)
+        ok, n_hyp = True, 0
+        for c in range(n_par):
+            for seg, (nh, hyps, stride, words) in enumerate(first["segs"]):
+                oh, rc = par[c][seg]
+                last, got = [], []
+                for q in range(int(nh[c])):
+                    x = hyps[c * stride + q]
+                    w = last[:x.shared] + words[x.words_off:x.words_off + x.n_words - x.shared].tolist()
+                    last = w if x.kind == 0 else []
+                    got.append((w, x.cost, x.hits, x.frame))
+                ok &= rc == 0 and got == [(h.words, h.cost, h.hits, h.frame) for h in oh]
+                n_hyp += len(oh)
         result["cpu_baseline"] = {"value": nfr / dt, "unit": "frames/s", "cores": 1, "kind": "port",
-                                  "sample": f"{len(res)} channel(s) x {T // S} frames (segment 0) "
-                                            f"of the same workload, C oracle, 1 thread",
-                                  "parity_with_gpu": bool(ok)}
+                                  "cpu": cpu_model(), "host_threads": os.cpu_count(),
+                                  "sample": f"{len(res)} whole channel(s) x {T} frames ({S} segments "
+                                            f"with context switches) of the same workload, C oracle "
+                                            f"(restatement of decoder.py), 1 thread",
+                                  "parity_with_gpu": bool(ok),
+                                  "parity_sample": f"channels 0..{n_par - 1}, all {S} segments, "
+                                                   f"{n_hyp} hypotheses (words, f64 cost bit-exact, "
+                                                   f"hits, frame) vs the oracle"}
     return result
 
 
@@ -492,8 +541,11 @@ def run_reference(args, W, world, rank):
         "config": {"workload": f"{args.workload} (bounded CPU sample)", "threads": threads},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{W['channels']} channels x {W['frames'] // W['segments']} "
-                                   "frames per step, C oracle (restatement of the reference "
+                         "cpu": cpu_model(),
+                         "sample": f"whole channels of the workload ({W['frames']} frames, "
+                                   f"{W['segments']} context-switched segments each; up to "
+                                   f"{W['channels']}) until a {budget / args.steps:.1f} s budget "
+                                   "per step is spent, C oracle (restatement of the reference "
                                    "decoder), one channel per thread"},
         "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -52,8 +52,10 @@ enum {
            chosen by AUTO) when the context is exactly the set of arcs whose
            olabel lies in some label set, e.g. single-word entities */
 enum { AB_CTX_AUTO = 0, AB_CTX_LIST = 1, AB_CTX_BITSET = 2, AB_CTX_LABELS = 3 };
-/* device limits: distinct tokens per channel-frame, hashed-table slots, epsilon rounds */
-enum { AB_MAX_TOKENS = 131072, AB_MAX_HASH_SLOTS = 4194304, AB_MAX_EPSILON_ROUNDS = 63 };
+/* device limits: distinct tokens per channel-frame, hashed-table slots; the
+   epsilon-round cap is not limited (any int32, negative = no rounds, as
+   decoder.py:263 `rounds < max_epsilon_expansion`) */
+enum { AB_MAX_TOKENS = 131072, AB_MAX_HASH_SLOTS = 4194304, AB_MAX_EPSILON_ROUNDS = 2147483647 };
 
 typedef struct ab_graph ab_graph;
 typedef struct ab_fst ab_fst; /* a parsed graph on the host (state-major CSR) */
@@ -172,9 +174,11 @@ int ab_channels_init(ab_decoder *d, int32_t n, const int32_t *slots, const int32
 int ab_channels_set_context(ab_decoder *d, int32_t n, const int32_t *slots,
                             const int32_t *contexts);
 int ab_channels_get(ab_decoder *d, int32_t n, const int32_t *slots, ab_channel_info *infos);
-/* Active token table: states/costs/hits (any pointer may be NULL). Returns count in *n. */
+/* Active token table: states / costs / hits / backpointers (device emission-record
+   id of the token's newest word, -1 = none); any pointer may be NULL.  Returns
+   the count in *n.  (Token fields, decoder.py:58-62.) */
 int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, double *costs, int32_t *hits,
-                      int32_t cap, int32_t *n);
+                      int32_t *backpointers, int32_t cap, int32_t *n);
 
 /* advance_frame × T / _decode_one for a batch; results stay on the device. */
 int ab_decode(ab_decoder *d, const ab_decode_args *args);

@@ -32,7 +32,7 @@ AB_PARTIAL, AB_FINAL = 0, 1
 AB_F32, AB_F64 = 0, 1
 AB_MODE_ADVANCE, AB_MODE_STREAM = 0, 1
 AB_CTX_AUTO, AB_CTX_LIST, AB_CTX_BITSET, AB_CTX_LABELS = 0, 1, 2, 3
-AB_MAX_TOKENS, AB_MAX_HASH_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 4194304, 63
+AB_MAX_TOKENS, AB_MAX_HASH_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 4194304, 2147483647
 
 
 class ab_config(C.Structure):
@@ -127,7 +127,7 @@ SIGNATURES = {
     "ab_channel_set_context": (_I32, [_P, _I32, _I32]),
     "ab_channel_get": (_I32, [_P, _I32, C.POINTER(ab_channel_info)]),
     "ab_channel_put": (_I32, [_P, _I32, C.POINTER(ab_channel_info)]),
-    "ab_channel_tokens": (_I32, [_P, _I32, _P, _P, _P, _I32, C.POINTER(_I32)]),
+    "ab_channel_tokens": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, C.POINTER(_I32)]),
     "ab_decode": (_I32, [_P, C.POINTER(ab_decode_args)]),
     "ab_read_results": (_I32, [_P, _P, _P, _P, _I32, _P, _I64, C.POINTER(_I64)]),
     "ab_partial": (_I32, [_P, _I32, C.POINTER(ab_hyp), _P, _I32]),

@@ -772,7 +772,7 @@ extern "C" int ab_channels_set_context(ab_decoder *d, int32_t n, const int32_t *
 }
 
 extern "C" int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, double *costs,
-                                 int32_t *hits, int32_t cap, int32_t *n) {
+                                 int32_t *hits, int32_t *bps, int32_t cap, int32_t *n) {
   int rc;
   if ((rc = check_slot(d, ch))) return rc;
   ab_channel_info info;
@@ -783,13 +783,16 @@ extern "C" int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, dou
   const size_t base = (size_t)ch * d->tok_cap;
   if (states) CK(cudaMemcpy(states, d->tok_state + base, m * sizeof(u32), cudaMemcpyDeviceToHost));
   if (costs) CK(cudaMemcpy(costs, d->tok_cost + base, m * sizeof(double), cudaMemcpyDeviceToHost));
-  if (hits) {
+  if (hits || bps) {
     ChanState cs;
     CK(cudaMemcpy(&cs, d->chans + ch, sizeof(ChanState), cudaMemcpyDeviceToHost));
     const size_t tbase = (2 * (size_t)ch + (cs.tok_half & 1u)) * d->tok_cap;
     std::vector<TokInfo> ti(m);
     CK(cudaMemcpy(ti.data(), d->tok_info + tbase, m * sizeof(TokInfo), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < m; ++i) hits[i] = ti[i].hits;
+    for (int i = 0; i < m; ++i) {
+      if (hits) hits[i] = ti[i].hits;
+      if (bps) bps[i] = ti[i].bp;
+    }
   }
   return AB_OK;
 }
@@ -1047,8 +1050,8 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   if (!(cf.beam > 0)) return fail(AB_ERR_INVALID, "beam must be positive");
   if (cf.max_active < 1) return fail(AB_ERR_INVALID, "max_active must be >= 1");
   if (cf.partial_every < 1) return fail(AB_ERR_INVALID, "partial_every must be >= 1");
-  if (cf.max_epsilon_expansion < 0 || cf.max_epsilon_expansion > MAX_EPS_ROUNDS)
-    return fail(AB_ERR_INVALID, "max_epsilon_expansion must be in [0, %d]", MAX_EPS_ROUNDS);
+  // max_epsilon_expansion: any value (a round without applications ends the
+  // closure; negative = no rounds, decoder.py:263)
   std::vector<int> slots(a->channels, a->channels + n), frames(a->frames, a->frames + n);
   std::vector<long long> soff(a->score_offsets, a->score_offsets + n);
   int64_t maxT = 0, rows = 0;

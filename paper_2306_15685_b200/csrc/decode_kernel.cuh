@@ -36,10 +36,13 @@ typedef unsigned long long u64;
 typedef uint32_t u32;
 
 constexpr u64 KEY_EPOCH_MASK = 0x7FFFFFFF00000000ull;
-// value.info = round(6) | epoch tag(7) | frontier row of the winner(19)
-constexpr int ROUND_SHIFT = 26;
+// value.info = epoch tag(13) | frontier row of the winner(19).  Rows are
+// allocated in round order inside a frame, so the row also tells the round:
+// a value whose row is below the current round's first row is from an earlier
+// round (no round field, so the tag is wide: the table is wiped once per 8191
+// epochs).
 constexpr int TAG_SHIFT = 19;
-constexpr u32 TAG_MASK = 0x7Fu;
+constexpr u32 TAG_MASK = 0x1FFFu;
 constexpr u32 VROW_MASK = (1u << TAG_SHIFT) - 1;
 constexpr u32 MAX_ROWS = 1u << TAG_SHIFT;  // frontier rows per channel-frame
 constexpr u32 KILL_DISP = 0x80000000u;     // kill-queue entry: the row was displaced
@@ -51,7 +54,6 @@ constexpr u32 G_MASK = 0x7FFFFFFFu;
 constexpr u32 G_START = 0xFFFFFFFFu; // frontier row of the utterance-start token
 constexpr u32 MAX_TOKENS = 1u << 17;            // distinct tokens per channel-frame
 constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per channel
-constexpr int MAX_EPS_ROUNDS = 63;
 // frontier row word: state | flags
 constexpr u32 ROW_DEAD = 0x80000000u;  // superseded by a later round (an application, not a token)
 constexpr u32 ROW_DISP = 0x40000000u;  // displaced in its own round (not an application)
@@ -129,7 +131,7 @@ struct __align__(16) TokInfo {
 // value per graph state (slot = state, no key, no probing) plus a u32 row
 // array.  The value (16 B, the CAS-128 target) = ordered cost key, global arc
 // id, info.  A value whose epoch tag differs from the channel's current tag is
-// empty; the table is wiped when the 8-bit tag wraps (every 255 epochs).
+// empty; the table is wiped when the 13-bit tag wraps (every 8191 epochs).
 struct __align__(32) Entry {
   u64 key;
   u32 flog; // frontier-log row of the latest application in this frame
@@ -366,6 +368,30 @@ __device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u6
   return ok;
 }
 
+// Degree byte of a state (a 5 MB array read for every expanded state): loaded
+// with an L2 evict_last policy so it stays resident next to the streams of
+// per-channel rows and token-table lines that flow through L2.
+#ifndef AB_DEG_KEEP
+#define AB_DEG_KEEP 1
+#endif
+__device__ __forceinline__ u64 l2_keep_policy() {
+  u64 pol = 0;
+#if AB_DEG_KEEP
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ u32 ld_deg(const unsigned char *p, u64 pol) {
+#if AB_DEG_KEEP
+  u32 v;
+  asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+
 // L2 prefetch: memory-level parallelism that costs no registers
 __device__ __forceinline__ void prefetch_l2(const void *p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -396,6 +422,45 @@ template <int BLOCK> __device__ __forceinline__ u32 block_excl_scan(u32 v, u32 &
   total = sh[NW - 1];
   __syncthreads();
   return base + x - v;
+}
+
+// Exclusive scan of Q values per thread in q-major order (element (q, t) at
+// position q * BLOCK + t): the order of coalesced loads i = base + q * BLOCK +
+// tid.  One barrier round like block_excl_scan; sh needs Q * BLOCK / 32 words.
+template <int BLOCK, int Q>
+__device__ __forceinline__ void block_excl_scan_q(const u32 (&v)[Q], u32 (&ex)[Q], u32 &total, u32 *sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = BLOCK / 32;
+  static_assert(Q * NW <= 32, "scan scratch");
+  u32 x[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    x[q] = v[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x[q], o);
+      if (lane >= o) x[q] += y;
+    }
+    if (lane == 31) sh[q * NW + wid] = x[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = lane < Q * NW ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < Q * NW) sh[lane] = w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k = q * NW + wid;
+    ex[q] = (k ? sh[k - 1] : 0u) + x[q] - v[q];
+  }
+  total = sh[Q * NW - 1];
+  __syncthreads();
 }
 
 // (key, state) lexicographic argmin over a block; returns the winner's idx.
@@ -634,11 +699,11 @@ template <typename F, typename S> __device__ __forceinline__ u64 *val_at(const C
 // as superseded (an application, no longer a token).  The queue is applied
 // after the round's barrier, so the rows of a round are final without a
 // second pass over the table.
-__device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 round, u32 etag, u64 vck, u32 vg,
+__device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 row0, u32 etag, u64 vck, u32 vg,
                                              u32 vinfo) {
   const bool valid = ((vinfo >> TAG_SHIFT) & TAG_MASK) == etag;
-  const u32 cround = vinfo >> ROUND_SHIFT;
-  return !valid || ((cround < round) ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
+  const bool earlier = (vinfo & VROW_MASK) < row0; // installed in an earlier round of the frame
+  return !valid || (earlier ? (ck < vck) : (ck < vck || (ck == vck && g < vg)));
 }
 
 struct RelaxAcc {
@@ -659,7 +724,7 @@ __device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, 
 // Outcome of a successful CAS that replaced old_info.
 template <typename F, typename S>
 __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
-                                          u32 round, u32 etag, u32 old_info, u64 old_ck, u64 ck) {
+                                          u32 row0, u32 etag, u32 old_info, u64 old_ck, u64 ck) {
   acc.min_ck = min(acc.min_ck, ck);
   if (((old_info >> TAG_SHIFT) & TAG_MASK) != etag) {
     acc.n_new++;
@@ -668,7 +733,7 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
   }
   // the replaced winner's row leaves the live rows (its cost is the CAS's expected key)
   atomicSub(&sh.fhist[hbucket(sh, key_cost(old_ck))], 1u);
-  if ((old_info >> ROUND_SHIFT) < round) {
+  if ((old_info & VROW_MASK) < row0) {
     acc.n_app++;
     queue_kill(P, C, sh, old_info & VROW_MASK);
   } else {
@@ -680,11 +745,11 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
 // candidate that stops being better marks its own row displaced.
 template <bool MARK_EPS, typename F, typename S>
 __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
-                            u64 ck, u32 g, u32 info, u32 round, u64 vck, u32 vg, u32 vinfo, u32 row,
+                            u64 ck, u32 g, u32 info, u32 row0, u64 vck, u32 vg, u32 vinfo, u32 row,
                             u32 eps_pos, bool hasol) {
   const u32 etag = C.etag;
   while (true) {
-    if (!value_better(ck, g, round, etag, vck, vg, vinfo)) {
+    if (!value_better(ck, g, row0, etag, vck, vg, vinfo)) {
       atomicOr(&C.flog_state[row], ROW_DISP);
       if (MARK_EPS && eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
       atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
@@ -694,7 +759,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
     const u32 old_info = vinfo;
     const u64 old_ck = vck;
     if (cas_value<F::smem_table>(v, vck, vg, vinfo, ck, g, info)) {
-      installed(P, C, sh, acc, round, etag, old_info, old_ck, ck);
+      installed(P, C, sh, acc, row0, etag, old_info, old_ck, ck);
       return;
     }
   }
@@ -705,7 +770,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
 template <typename F, typename S>
 __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
                                          u32 d, u64 ck, u32 g, u32 src, u32 rflags, u32 lab_ol, u32 lab_il,
-                                         u32 round, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
+                                         u32 row0, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
   const u64 ep = (u64)C.epoch << 32;
   u32 probes = 0;
   while (true) {
@@ -724,7 +789,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     }
     ld_cg_entry(&C.table[slot], key, vck, vg, vinfo);
   }
-  if (!value_better(ck, g, round, C.etag, vck, vg, vinfo)) return;
+  if (!value_better(ck, g, row0, C.etag, vck, vg, vinfo)) return;
   const u32 row = atomicAdd(&sh.flog_n, 1u);
   if (row >= P.flog_cap) {
     set_error(sh, E_CAP);
@@ -740,8 +805,8 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   C.flog_aux[row] = make_uint4(aux_src(src, rflags, g), epos, lab_ol, lab_il);
   atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
   acc.n_rec += (rflags & ROW_HASOL) ? 1 : 0;
-  const u32 info = (round << ROUND_SHIFT) | (C.etag << TAG_SHIFT) | row;
-  relax_retry<true>(P, C, sh, acc, val_at(C, slot), ck, g, info, round, vck, vg, vinfo, row, epos,
+  const u32 info = (C.etag << TAG_SHIFT) | row;
+  relax_retry<true>(P, C, sh, acc, val_at(C, slot), ck, g, info, row0, vck, vg, vinfo, row, epos,
               (rflags & ROW_HASOL) != 0);
 }
 
@@ -753,7 +818,7 @@ template <int BLOCK, int U, typename F, typename S>
 __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
                                             const bool (&on)[U], const u32 (&d)[U], const u64 (&ck)[U],
                                             const u32 (&g)[U], const u32 (&src)[U], const u32 (&rflags)[U],
-                                            const u32 (&ol)[U], const u32 (&il)[U], u32 round) {
+                                            const u32 (&ol)[U], const u32 (&il)[U], u32 row0) {
   const u32 etag = C.etag;
   const u64 ep = (u64)C.epoch << 32;
   u32 slot[U];
@@ -786,7 +851,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (on[u] && !fast[u])
-        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], ol[u], il[u], round, slot[u],
+        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], ol[u], il[u], row0, slot[u],
                           key[u], vck[u], vg[u], vinfo[u]);
   } else {
 #pragma unroll
@@ -796,7 +861,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   u32 nw = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    want[u] = fast[u] && value_better(ck[u], g[u], round, etag, vck[u], vg[u], vinfo[u]);
+    want[u] = fast[u] && value_better(ck[u], g[u], row0, etag, vck[u], vg[u], vinfo[u]);
     nw += want[u] ? 1u : 0u;
   }
   if (!nw) return;
@@ -826,7 +891,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     st_row<BLOCK>(&C.flog_aux[rows[u]], make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]));
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
     acc.n_rec += (rflags[u] & ROW_HASOL) ? 1 : 0;
-    ninfo[u] = (round << ROUND_SHIFT) | (etag << TAG_SHIFT) | rows[u];
+    ninfo[u] = (etag << TAG_SHIFT) | rows[u];
   }
   u64 r0[U], r1[U];
 #pragma unroll
@@ -838,9 +903,9 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   for (int u = 0; u < U; ++u) {
     if (!want[u]) continue;
     if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u]))
-      installed(P, C, sh, acc, round, etag, vinfo[u], vck[u], ck[u]);
+      installed(P, C, sh, acc, row0, etag, vinfo[u], vck[u], ck[u]);
     else
-      relax_retry<!disp_at_listing<BLOCK>()>(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], round, r0[u], (u32)r1[u],
+      relax_retry<!disp_at_listing<BLOCK>()>(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], row0, r0[u], (u32)r1[u],
                   (u32)(r1[u] >> 32), rows[u], eps_pos[u], (rflags[u] & ROW_HASOL) != 0);
   }
 }
@@ -857,7 +922,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 //      into the cost add), one batched relaxation.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const uint4 *list, u32 n_in,
-                       u32 round) {
+                       u32 row0) {
   constexpr u32 TILE = BLOCK * Q;
   // 1024-thread CTAs (one channel alone on its SM, C1 / C2): warp-private
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
@@ -878,6 +943,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   acc.n_app = 0;
   acc.n_rec = 0;
   u32 arcs_seen = 0;
+  const u64 deg_pol = l2_keep_policy();
   if constexpr (WARP_TILES) {
   // Each warp works through its own sub-tiles (32 * Q inputs; smaller when
   // the input is short, so every warp gets some): a warp-level scan of the
@@ -921,7 +987,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       // (with the DISP check at listing, the degree load does not wait for it)
       if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
         const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
-        const u32 dg = __ldg(&P.deg[s]);
+        const u32 dg = ld_deg(&P.deg[s], deg_pol);
         const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
         if (c == DEG_OVF) {
           const uint2 r = __ldg(&rng[s]);
@@ -1007,7 +1073,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
     }
     __syncwarp();
   }
@@ -1016,17 +1082,21 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     atomicAdd(EMIT ? &sh.cnt_emit : &sh.cnt_eps, (unsigned long long)arcs_seen);
   }
   } else {
+  // tile position j = q * BLOCK + tid: input base + j, so every load of the
+  // tile's inputs is warp-coalesced (the degree scan runs in the same order)
   for (u32 base = 0; base < n_in; base += TILE) {
-    const u32 i0 = base + (u32)tid * Q;
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
     if (EMIT) {
 #pragma unroll
-      for (int q = 0; q < Q; ++q) idx[q] = i0 + q < n_in ? i0 + q : 0xFFFFFFFFu;
+      for (int q = 0; q < Q; ++q) {
+        const u32 i = base + (u32)q * BLOCK + (u32)tid;
+        idx[q] = i < n_in ? i : 0xFFFFFFFFu;
+      }
 #pragma unroll
       for (int q = 0; q < Q; ++q) st[q] = idx[q] == 0xFFFFFFFFu ? ROW_DISP : C.tok_state[idx[q]];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const u32 j = (u32)tid * Q + q;
+        const u32 j = (u32)q * BLOCK + (u32)tid;
         t_src[j] = idx[q];
         if (idx[q] != 0xFFFFFFFFu) t_cost[j] = C.tok_cost[idx[q]];
       }
@@ -1034,11 +1104,11 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       // epsilon-frontier entries carry the row's state, flags and cost
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const u32 j = (u32)tid * Q + q;
+        const u32 j = (u32)q * BLOCK + (u32)tid;
         idx[q] = 0xFFFFFFFFu;
         st[q] = ROW_DISP;
-        if (i0 + q < n_in) {
-          const uint4 e = list[i0 + q];
+        if (base + j < n_in) {
+          const uint4 e = list[base + j];
           idx[q] = e.x;
           st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
           t_cost[j] = key_cost(((u64)e.w << 32) | e.z);
@@ -1053,7 +1123,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       // (with the DISP check at listing, the degree load does not wait for it)
       if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
         const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
-        const u32 dg = __ldg(&P.deg[s]);
+        const u32 dg = ld_deg(&P.deg[s], deg_pol);
         const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
         if (c == DEG_OVF) {
           const uint2 r = __ldg(&rng[s]);
@@ -1066,17 +1136,13 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         if (!EMIT && (st[q] & ROW_DISP)) cnt[q] = 0; // displaced: not expanded
       }
     }
-    u32 tsum = 0;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) tsum += cnt[q];
-    u32 total;
-    u32 run = block_excl_scan<BLOCK>(tsum, total, sh.scan);
+    u32 total, pref[Q];
+    block_excl_scan_q<BLOCK, Q>(cnt, pref, total, sh.scan);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const u32 j = (u32)tid * Q + q;
+      const u32 j = (u32)q * BLOCK + (u32)tid;
       t_a0[j] = a0[q];
-      t_pref[j] = run;
-      run += cnt[q];
+      t_pref[j] = pref[q];
     }
     if (tid == 0) t_pref[TILE] = total;
     __syncthreads();
@@ -1135,7 +1201,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
         }
       }
-      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, round);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
     }
     __syncthreads();
   }
@@ -1251,6 +1317,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       break;
     }
     rounds++;
+    const u32 row0 = sh.flog_n; // rows below were written by earlier rounds of this frame
     __syncthreads();
     if (threadIdx.x == 0) {
       sh.n_app = 0;
@@ -1258,7 +1325,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       sh.cnt_tok += n_front; // token expansions of the reference's round
     }
     __syncthreads();
-    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, (u32)rounds);
+    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
     __syncthreads();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
@@ -1441,13 +1508,19 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   u32 n_tok = 0, n_mem = 0;
   u32 *mem_row = C.scr_row + P.flog_cap; // set-aside rows grow down from the top of scr_row
   for (u32 base = 0; base < n_rows; base += TILE) {
-    const u32 i0 = base + (u32)tid * QP;
+    // rows base + q * BLOCK + tid: warp-coalesced loads
     u32 st[QP], bq[QP];
     u64 ck[QP];
 #pragma unroll
-    for (int q = 0; q < QP; ++q) st[q] = i0 + q < n_rows ? C.flog_state[i0 + q] : ROW_DISP;
+    for (int q = 0; q < QP; ++q) {
+      const u32 i = base + (u32)q * BLOCK + (u32)tid;
+      st[q] = i < n_rows ? C.flog_state[i] : ROW_DISP;
+    }
 #pragma unroll
-    for (int q = 0; q < QP; ++q) ck[q] = i0 + q < n_rows ? C.flog_ck[i0 + q] : ~0ull;
+    for (int q = 0; q < QP; ++q) {
+      const u32 i = base + (u32)q * BLOCK + (u32)tid;
+      ck[q] = i < n_rows ? C.flog_ck[i] : ~0ull;
+    }
     u32 ns = 0, nm = 0;
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
@@ -1463,16 +1536,17 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     for (int q = 0; q < QP; ++q) {
       if (bq[q] > split || (bq[q] == split && ck[q] > thr_ck)) continue;
       const u32 s = st[q] & ROW_STATE;
-      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)(i0 + q);
+      const u32 i = base + (u32)q * BLOCK + (u32)tid;
+      if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)i;
       if (bq[q] < split) {
         C.tok_state[ps] = s;
         C.tok_cost[ps] = key_cost(ck[q]);
-        C.scr_row[ps] = i0 + q;
+        C.scr_row[ps] = i;
         ++ps;
       } else {
         C.scr_key[pm] = ck[q];
         scr_state[pm] = s;
-        *(mem_row - 1 - pm) = i0 + q;
+        *(mem_row - 1 - pm) = i;
         ++pm;
       }
     }
@@ -1599,7 +1673,7 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
 }
 
 // Moves the channel to a fresh table epoch; the table is wiped when the
-// 7-bit epoch tag would wrap, so a tag is never reused while stale values
+// 13-bit epoch tag would wrap, so a tag is never reused while stale values
 // carrying it can still be in the table.  Also opens the frame's cost
 // histogram: buckets of beam / HIST_PER_BEAM from one beam below the previous
 // frame's best cost (values outside clamp into the end buckets).
@@ -2076,9 +2150,12 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
     int t = 0;
     for (; t < T; ++t) {
       if (P.mode == AB_MODE_STREAM) {
-        // a frame adds at most 1 + max_eps words to any path and emits at most two
-        // hypotheses; pause (the host relaunches) if they might not fit
-        const long long bound = (long long)(cs->info.fresh ? 0 : cs->max_depth) + 2 + P.max_eps;
+        // a frame adds at most 1 + max_eps words to any path (a fresh channel's
+        // start closure up to max_eps more) and emits at most two hypotheses of
+        // at most path_cap words; pause (the host relaunches) if they might not fit
+        const long long E = min((long long)max(P.max_eps, 0), (long long)P.path_cap);
+        const long long bound =
+            min((long long)(cs->info.fresh ? E : cs->max_depth) + 2 + E, (long long)P.path_cap);
         if (P.words_used[b] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
           if (t == 0 && threadIdx.x == 0) set_error(sh, E_CAP); // no progress possible
           break;

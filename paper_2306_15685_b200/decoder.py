@@ -67,9 +67,14 @@ _CODE_TO_STATUS = {v: k for k, v in _STATUS_TO_CODE.items()}
 
 @dataclass
 class Token:
+    """decoder.py:58-62 (state, cost, backpointer).  ``backpointer`` is the
+    device emission-record id of the token's newest word (-1 = none); record
+    ids are the device arena's, not the reference store's positions (the words
+    they lead to are the same).  ``hits`` (boosted arcs on the path) is extra."""
     state: int
     cost: float
-    hits: int
+    backpointer: int = -1
+    hits: int = 0
 
 
 @dataclass
@@ -111,6 +116,7 @@ class Channel:
     _ctx_handle: int = field(default=-1, repr=False, compare=False)
     _last_words: list = field(default_factory=list, repr=False, compare=False)
     _work: tuple = field(default=(0, 0, 0), repr=False, compare=False)
+    _slot_finalizer: object = field(default=None, repr=False, compare=False)
 
     @property
     def store(self) -> _StoreView:
@@ -123,9 +129,9 @@ class Channel:
     def active_tokens(self) -> list[Token]:
         if self._page is None or self._num_active == 0:
             return []
-        st, co, hi = self._page.tokens(self._slot)
+        st, co, hi, bp = self._page.tokens(self._slot)
         order = np.lexsort((co, st))
-        return [Token(int(st[i]), float(co[i]), int(hi[i])) for i in order]
+        return [Token(int(st[i]), float(co[i]), int(bp[i]), int(hi[i])) for i in order]
 
     @property
     def work_counters(self) -> tuple:
@@ -142,11 +148,14 @@ def _bind(ch: Channel, csr, prefer: BatchDecoder | None = None) -> tuple[BatchDe
     if ch._graph is not None:
         if not ch._fresh:
             raise DecodeError(f"channel {ch.id!r}: cannot move to another graph mid-utterance")
-        ch._page.free_slot(ch._slot)
+        # the old slot goes back now; its finalizer must not free it again later
+        # (another channel may own it by then)
+        if ch._slot_finalizer is not None:
+            ch._slot_finalizer()
     page, slot = dg.bind_slot(prefer)
     ch._graph, ch._page, ch._slot = dg, page, slot
     ch._last_words = []
-    weakref.finalize(ch, page.free_slot, slot)
+    ch._slot_finalizer = weakref.finalize(ch, page.free_slot, slot)
     return page, slot
 
 
@@ -211,9 +220,11 @@ def _width_error(width, L) -> DecodeError:
 
 
 def _check_eps_cap(cfg) -> None:
-    if not 0 <= cfg.max_epsilon_expansion <= _lib.AB_MAX_EPSILON_ROUNDS:
-        raise DecodeError(
-            f"max_epsilon_expansion must be in [0, {_lib.AB_MAX_EPSILON_ROUNDS}] on the device")
+    """Any integer cap is accepted, as in the reference (decoder.py:263); the
+    device field is int32, so larger caps saturate (same rounds: a closure
+    ends long before 2**31 rounds, every round with applications takes a
+    frontier row)."""
+    int(cfg.max_epsilon_expansion)
 
 
 # ------------------------------------------------------------------- public API

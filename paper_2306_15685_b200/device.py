@@ -24,13 +24,39 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
+def default_device() -> int:
+    """The GPU a graph goes to when the caller names none.  In order:
+    ``ARCBOOST_DEVICE``; torch's current device when torch has initialised
+    CUDA in this process (a rank that called ``torch.cuda.set_device``);
+    ``LOCAL_RANK`` modulo the device count (one process per GPU under
+    torchrun, SPEC.md:343,365); else 0."""
+    env = os.environ.get("ARCBOOST_DEVICE")
+    if env is not None:
+        return int(env)
+    import sys
+
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    local = os.environ.get("LOCAL_RANK")
+    if local is not None:
+        n = C.c_int32()
+        if _lib.load().ab_device_count(C.byref(n)) == 0 and n.value > 0:
+            return int(local) % n.value
+    return 0
+
+
 class DeviceGraph:
     """Device CSR split into emitting / epsilon SoA (fst.py:165-191)."""
 
     def __init__(self, csr, device: int | None = None):
         lib = _lib.load()
         if device is None:
-            device = int(os.environ.get("ARCBOOST_DEVICE", "0"))
+            device = default_device()
         self.device = device
         ro = np.ascontiguousarray(csr.row_offsets, dtype=np.int64)
         il = np.ascontiguousarray(csr.ilabels, dtype=np.int32)
@@ -62,7 +88,7 @@ class DeviceGraph:
         self.num_emitting_labels = L.value
         self.weights_f32 = bool(w32.value)
         self.device_bytes = nbytes.value
-        self._ctx: dict[int, tuple[weakref.ref, int]] = {}
+        self._ctx: dict[int, tuple[weakref.ref, int, tuple]] = {}
         self._pages: list[BatchDecoder] = []
         # decoders built on this graph must be destroyed before it
         self._decoder_finalizers: list = []
@@ -90,11 +116,16 @@ class DeviceGraph:
         if ctx is None:
             return -1
         key = id(ctx)
+        # the reference reads the live object every frame (decoder.py:234-240):
+        # a changed discount or a reassigned index array is a new device context
+        arcs = ctx.arc_indices
+        n = len(arcs)
+        stamp = (float(ctx.discount), id(arcs), n, int(arcs[0]) if n else -1, int(arcs[-1]) if n else -1)
         hit = self._ctx.get(key)
-        if hit is not None and hit[0]() is ctx:
+        if hit is not None and hit[0]() is ctx and hit[2] == stamp:
             return hit[1]
-        h = self.register_context(ctx.arc_indices, ctx.discount)
-        self._ctx[key] = (weakref.ref(ctx, lambda _r, k=key, hh=h: self._drop_ctx(k, hh)), h)
+        h = self.register_context(arcs, ctx.discount)
+        self._ctx[key] = (weakref.ref(ctx, lambda _r, k=key, hh=h: self._drop_ctx(k, hh)), h, stamp)
         return h
 
     def _drop_ctx(self, key: int, h: int) -> None:
@@ -207,14 +238,15 @@ class BatchDecoder:
 
     def tokens(self, slot: int):
         n = C.c_int32()
-        check(_lib.load().ab_channel_tokens(self.handle, int(slot), None, None, None, 0,
+        check(_lib.load().ab_channel_tokens(self.handle, int(slot), None, None, None, None, 0,
                                             C.byref(n)))
         st = np.zeros(max(n.value, 1), dtype=np.int32)
         co = np.zeros(max(n.value, 1), dtype=np.float64)
         hi = np.zeros(max(n.value, 1), dtype=np.int32)
+        bp = np.zeros(max(n.value, 1), dtype=np.int32)
         check(_lib.load().ab_channel_tokens(self.handle, int(slot), _ptr(st), _ptr(co), _ptr(hi),
-                                            n.value, C.byref(n)))
-        return st[:n.value], co[:n.value], hi[:n.value]
+                                            _ptr(bp), n.value, C.byref(n)))
+        return st[:n.value], co[:n.value], hi[:n.value], bp[:n.value]
 
     def decode(self, slots, frames, score_offsets, scores, width: int, cfg, mode: int,
                scores_on_device: bool = False, scores_dtype: int | None = None,
@@ -295,7 +327,9 @@ class BatchDecoder:
 
 
 def make_config(cfg) -> _lib.ab_config:
-    return _lib.ab_config(float(cfg.beam), int(cfg.max_active), int(cfg.max_epsilon_expansion),
+    # the epsilon cap saturates to int32 (same rounds, see decoder._check_eps_cap)
+    eps = max(-(1 << 31), min(int(cfg.max_epsilon_expansion), _lib.AB_MAX_EPSILON_ROUNDS))
+    return _lib.ab_config(float(cfg.beam), int(cfg.max_active), eps,
                           int(cfg.partial_every), int(cfg.endpoint_silence_frames),
                           int(cfg.silence_ilabel), 0)
 
