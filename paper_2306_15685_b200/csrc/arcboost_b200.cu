@@ -61,7 +61,8 @@ struct HostCtx {
   int abi_mode = AB_CTX_LIST;
   u32 words = 0;
   u32 *d_list = nullptr;
-  u32 *d_bits = nullptr;
+  u32 *d_bits = nullptr;   // CTX_BITSET: emitting record positions; CTX_LABELS: olabel bitmap
+  u32 *d_bits_x = nullptr; // CTX_BITSET: epsilon record positions
 };
 
 struct ab_graph {
@@ -74,6 +75,11 @@ struct ab_graph {
   bool fmt16 = true; // f32 weights and 16-bit labels: 16-byte arc records
   std::vector<int32_t> olabels; // host copy for context classification
   std::vector<u32> ol_count;    // arcs per output label (empty if labels are huge)
+  // device record position of every arc (bit 31 = epsilon array): BITSET
+  // contexts are stored by record position, so the kernel's boost lookup is
+  // addressed before the arc record arrives (issued next to the record load)
+  std::vector<u32> arc_pos;
+  uint64_t e_tot = 0, x_tot = 0; // records in the emitting / epsilon arrays
   uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
   unsigned char *deg = nullptr;              // per state arc counts (DecodeParams::deg)
   void *e_arcs = nullptr, *x_arcs = nullptr;
@@ -270,6 +276,9 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     return fail(AB_ERR_INVALID, "too many arcs after block alignment");
   }
   std::vector<unsigned char> eh(std::max<size_t>(e_tot, 1) * esz, 0), xh(std::max<size_t>(x_tot, 1) * xsz, 0);
+  g->e_tot = e_tot;
+  g->x_tot = x_tot;
+  g->arc_pos.resize(num_arcs);
   for (int s = 0; s < num_states; ++s) {
     u32 pe = e_beg[s], px = x_beg[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
@@ -285,6 +294,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
           EArc24 r{(u32)next_states[a], ga, (u32)ilabels[a], (u32)olabels[a], weights[a]};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         }
+        g->arc_pos[a] = pe;
         pe++;
       } else {
         const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
@@ -295,6 +305,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
           XArc24 r{(u32)next_states[a], ga, (u32)olabels[a], 0u, weights[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         }
+        g->arc_pos[a] = px | 0x80000000u;
         px++;
       }
     }
@@ -335,6 +346,7 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   for (auto &c : g->ctxs) {
     cudaFree(c.d_list);
     cudaFree(c.d_bits);
+    cudaFree(c.d_bits_x);
   }
   cudaFree(g->d_ctxs);
   cudaFree(g->e_rng);
@@ -369,6 +381,7 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].pad = 0;
     h[i].list = c.d_list;
     h[i].bits = c.d_bits;
+    h[i].bits_x = c.d_bits_x;
   }
   if (h.size() > g->d_ctxs_cap) {
     cudaFree(g->d_ctxs);
@@ -428,11 +441,19 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
   if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
   if (mode == AB_CTX_BITSET) {
-    size_t words = ((size_t)g->num_arcs + 31) / 32 + 1;
-    std::vector<u32> bits(words, 0);
-    for (u32 a : list) bits[a >> 5] |= 1u << (a & 31);
-    CK(cudaMalloc(&c.d_bits, words * sizeof(u32)));
-    CK(cudaMemcpy(c.d_bits, bits.data(), words * sizeof(u32), cudaMemcpyHostToDevice));
+    // one bit per record position of each arc array (biasing.py:108-117 by
+    // position instead of arc id: the same set, addressed without the record)
+    const size_t we = (size_t)(g->e_tot + 31) / 32 + 1, wx = (size_t)(g->x_tot + 31) / 32 + 1;
+    std::vector<u32> be(we, 0), bx(wx, 0);
+    for (u32 a : list) {
+      const u32 p = g->arc_pos[a];
+      if (p & 0x80000000u) bx[(p & 0x7FFFFFFFu) >> 5] |= 1u << (p & 31);
+      else be[p >> 5] |= 1u << (p & 31);
+    }
+    CK(cudaMalloc(&c.d_bits, we * sizeof(u32)));
+    CK(cudaMemcpy(c.d_bits, be.data(), we * sizeof(u32), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c.d_bits_x, wx * sizeof(u32)));
+    CK(cudaMemcpy(c.d_bits_x, bx.data(), wx * sizeof(u32), cudaMemcpyHostToDevice));
   } else if (mode == AB_CTX_LABELS) {
     c.words = (u32)lbits.size();
     CK(cudaMalloc(&c.d_bits, lbits.size() * sizeof(u32)));
@@ -470,6 +491,7 @@ extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
   HostCtx &c = g->ctxs[handle];
   cudaFree(c.d_list);
   cudaFree(c.d_bits);
+  cudaFree(c.d_bits_x);
   c = HostCtx();
   return sync_ctx_table(g);
 }

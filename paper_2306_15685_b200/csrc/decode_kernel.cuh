@@ -148,7 +148,8 @@ struct CtxDesc {
   u32 words; // CTX_LABELS: bitmap words
   u32 pad;
   const u32 *list; // sorted arc ids
-  const u32 *bits; // CTX_BITSET: arc bitmap, CTX_LABELS: olabel bitmap
+  const u32 *bits;   // CTX_BITSET: bit per emitting record position, CTX_LABELS: olabel bitmap
+  const u32 *bits_x; // CTX_BITSET: bit per epsilon record position
 };
 
 // Arc record formats.  Fmt16: f32 weight, 16-bit labels (one 16 B load).
@@ -633,6 +634,7 @@ template <typename F, typename S> struct Chan {
   const u32 *ctx_list;
   u32 ctx_k;
   const u32 *ctx_bits;
+  const u32 *ctx_bits_x;
   u32 ctx_words;
   u32 epoch;
   u32 etag;
@@ -652,14 +654,21 @@ __device__ __forceinline__ u32 hbucket(const Shared &sh, double c) {
   return !(x > 0.0) ? 0u : (x >= (double)(NB_HIST - 1) ? NB_HIST - 1 : (u32)x);
 }
 
+// Bitset word of a BITSET context for the arc record at position a: addressed
+// by position, so it is loaded next to the record, not after it.
+template <bool EMIT, typename F, typename S>
+__device__ __forceinline__ u32 boost_word(const Chan<F, S> &C, u32 a) {
+  return C.ctx_mode == CTX_BITSET ? __ldg(&(EMIT ? C.ctx_bits : C.ctx_bits_x)[a >> 5]) : 0u;
+}
+
 // BiasingContext.boosted_mask (biasing.py:108-117) in the representation the
-// context store chose for this context.
+// context store chose for this context; bw = boost_word of the record.
 template <typename F, typename S>
-__device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 g, u32 ol) {
+__device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 a, u32 bw, u32 g, u32 ol) {
   switch (C.ctx_mode) {
   case CTX_NONE: return false;
   case CTX_LABELS: return ol < C.ctx_words * 32u && ((C.ctx_bits[ol >> 5] >> (ol & 31)) & 1u);
-  case CTX_BITSET: return (__ldg(&C.ctx_bits[g >> 5]) >> (g & 31)) & 1u;
+  case CTX_BITSET: return (bw >> (a & 31)) & 1u;
   default: {
     const u32 *a = C.ctx_list;
     u32 lo = 0, hi = C.ctx_k;
@@ -1045,13 +1054,15 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = w_cost[lo];
         }
       }
-      u32 d[U], g[U], il[U], ol[U];
+      u32 d[U], g[U], il[U], ol[U], bw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         d[u] = g[u] = il[u] = ol[u] = 0;
         w[u] = 0.0;
+        bw[u] = 0;
         if (on[u]) {
+          bw[u] = boost_word<EMIT>(C, a[u]);
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
@@ -1064,7 +1075,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         rflags[u] = 0;
         if (on[u]) {
           // _effective_weights (decoder.py:234-240): boost fused into the cost add
-          const bool bst = is_boosted(C, g[u] & G_MASK, ol[u]);
+          const bool bst = is_boosted(C, a[u], bw[u], g[u] & G_MASK, ol[u]);
           const double we = bst ? w[u] + C.discount : w[u];
           double cand;
           if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
@@ -1173,13 +1184,15 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = t_cost[lo];
         }
       }
-      u32 d[U], g[U], il[U], ol[U];
+      u32 d[U], g[U], il[U], ol[U], bw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         d[u] = g[u] = il[u] = ol[u] = 0;
         w[u] = 0.0;
+        bw[u] = 0;
         if (on[u]) {
+          bw[u] = boost_word<EMIT>(C, a[u]);
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
@@ -1192,7 +1205,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         rflags[u] = 0;
         if (on[u]) {
           // _effective_weights (decoder.py:234-240): boost fused into the cost add
-          const bool bst = is_boosted(C, g[u] & G_MASK, ol[u]);
+          const bool bst = is_boosted(C, a[u], bw[u], g[u] & G_MASK, ol[u]);
           const double we = bst ? w[u] + C.discount : w[u];
           double cand;
           if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
@@ -2063,6 +2076,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.ctx_words = 0;
     C.ctx_list = nullptr;
     C.ctx_bits = nullptr;
+    C.ctx_bits_x = nullptr;
     C.t_a0 = t_a0;
     C.t_pref = t_pref;
     C.t_cost = t_cost;
@@ -2091,6 +2105,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
       C.ctx_mode = mode;
       C.ctx_words = d.words;
       C.ctx_bits = mode == CTX_LABELS ? sh_ctx : d.bits;
+      C.ctx_bits_x = d.bits_x;
       C.ctx_list = mode == CTX_SLIST ? sh_ctx : d.list;
     }
   }

@@ -190,28 +190,40 @@ def _pull(ch: Channel) -> None:
     ch._work = (info.tok_expansions, info.emit_arcs, info.eps_arcs)
 
 
-def _hyp(ch: Channel, h, words: np.ndarray) -> Hypothesis:
+def hyp_from_device(h, words: np.ndarray, prev: list) -> tuple[Hypothesis, list]:
+    """A device hypothesis row -> Hypothesis.  The device shares path prefixes:
+    ``h.shared`` leading words equal the previous hypothesis of the same channel
+    (``prev``); the rest are at ``words[h.words_off:]``.  Returns the hypothesis
+    and the prefix the channel's next row refers to (empty after a final)."""
     s, n = h.shared, h.n_words
     suffix = words[h.words_off:h.words_off + (n - s)].tolist() if n > s else []
-    w = ch._last_words[:s] + suffix
-    ch._last_words = w
+    w = prev[:s] + suffix
     kind = "final" if h.kind == _lib.AB_FINAL else "partial"
-    if kind == "final":
-        ch._last_words = []
-    return Hypothesis(words=list(w), cost=float(h.cost), frame=int(h.frame), kind=kind,
-                      fallback=bool(h.fallback), hits=int(h.hits))
+    return (Hypothesis(words=list(w), cost=float(h.cost), frame=int(h.frame), kind=kind,
+                       fallback=bool(h.fallback), hits=int(h.hits)),
+            [] if kind == "final" else w)
+
+
+def _hyp(ch: Channel, h, words: np.ndarray) -> Hypothesis:
+    hyp, ch._last_words = hyp_from_device(h, words, ch._last_words)
+    return hyp
+
+
+def device_error(channel_id: str, status: str, code: int, what: str = "finalize") -> DecodeError:
+    """The reference's DecodeError for a device error code (decoder.py:422, 437-441, 459)."""
+    if code == _lib.AB_ERR_DEAD:
+        return DecodeError(f"channel {channel_id!r}: decode failure, no active tokens")
+    if code == _lib.AB_ERR_STATUS:
+        return DecodeError(f"channel {channel_id!r}: cannot {what} in status {status}")
+    if code == _lib.AB_ERR_CAPACITY:
+        return DecodeError(
+            f"channel {channel_id!r}: device capacity exceeded (token table, frontier log, emission "
+            "arena or hypothesis path); raise paper_2306_15685_b200.device.DEFAULT_CAPACITY")
+    return DecodeError(f"channel {channel_id!r}: device error {code}")
 
 
 def _device_error(ch: Channel, code: int, what: str = "finalize") -> DecodeError:
-    if code == _lib.AB_ERR_DEAD:
-        return DecodeError(f"channel {ch.id!r}: decode failure, no active tokens")
-    if code == _lib.AB_ERR_STATUS:
-        return DecodeError(f"channel {ch.id!r}: cannot {what} in status {ch.status.value}")
-    if code == _lib.AB_ERR_CAPACITY:
-        return DecodeError(
-            f"channel {ch.id!r}: device capacity exceeded (token table, frontier log, emission "
-            "arena or hypothesis path); raise paper_2306_15685_b200.device.DEFAULT_CAPACITY")
-    return DecodeError(f"channel {ch.id!r}: device error {code}")
+    return device_error(ch.id, ch.status.value, code, what)
 
 
 def _width_error(width, L) -> DecodeError:
@@ -388,11 +400,10 @@ def decode_batch(channels: Sequence[tuple[Channel, ScoreMatrix]], csr,
     return results  # type: ignore[return-value]
 
 
-def _launch_stream(items, dg: DeviceGraph, cfg, results) -> None:
-    page = items[0][1]._page
-    L = dg.num_emitting_labels
-    mats = [s.costs for _, _, s in items]
-    # f32 on the device when every cost is exactly an f32 (half the H2D bytes)
+def pack_streams(mats, L: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Score matrices of one launch -> (packed rows, frames per stream, row
+    offsets).  f32 when every cost is exactly an f32 (half the H2D bytes, same
+    f64 arithmetic on the device), else f64."""
     m32 = []
     f32 = True
     for m in mats:
@@ -408,6 +419,13 @@ def _launch_stream(items, dg: DeviceGraph, cfg, results) -> None:
     rows = [m.reshape(-1) for m in src if m.size]
     dt = np.float32 if f32 else np.float64
     packed = np.ascontiguousarray(np.concatenate(rows)) if rows else np.zeros(1, dtype=dt)
+    return packed, frames, offs
+
+
+def _launch_stream(items, dg: DeviceGraph, cfg, results) -> None:
+    page = items[0][1]._page
+    L = dg.num_emitting_labels
+    packed, frames, offs = pack_streams([s.costs for _, _, s in items], L)
     for _, ch, _ in items:
         _push(ch)
     page.decode([ch._slot for _, ch, _ in items], frames, offs, packed, L, cfg,
