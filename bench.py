@@ -26,6 +26,7 @@ Multi-GPU: launched under torchrun, each rank decodes its own 1024 channels
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -62,6 +63,10 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-overhead", action="store_true", help="skip the unbiased / zero-discount runs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--exact", action="store_true",
+                   help="relax every candidate (exact_counters): no expansion-time cutoff")
+    p.add_argument("--table-slots", type=int, default=0,
+                   help="token-table slots per channel (0 = direct table when it fits)")
     p.add_argument("--parity-channels", type=int, default=16,
                    help="channels whose every segment is checked against the oracle")
     p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
@@ -335,7 +340,7 @@ def run_b200(args, W, world, rank, local):
     # emission arena: ~16 frames of appends (~45k records per channel-frame on
     # G_large); the in-kernel copying GC reclaims records of pruned paths
     big = W["states"] > 1_000_000
-    cap = Capacity(arena_records=(1 << 20) if big else (1 << 19))
+    cap = Capacity(table_slots=args.table_slots, arena_records=(1 << 20) if big else (1 << 19))
     dec = BatchDecoder(dg, C, cap)
     prep["upload_s"] = time.time() - t0
     # the same numpy streams, generated in HBM (ab_scores_generate, bit-identical
@@ -357,7 +362,12 @@ def run_b200(args, W, world, rank, local):
         hs = handles0 if variant == "zero" else handles
         return np.array([hs[ctx_index(c, seg, len(hs))] for c in range(C)], dtype=np.int32)
 
-    def step(on_device=True, variant="biased", collect=False):
+    cfg_exact = dataclasses.replace(cfg, exact_counters=True)
+    if args.exact:
+        cfg = cfg_exact
+
+    def step(on_device=True, variant="biased", collect=False, c=None):
+        c = c or cfg
         kernel_ms = 0.0
         launches = 0
         out = {}
@@ -367,11 +377,11 @@ def run_b200(args, W, world, rank, local):
                 dec.set_contexts(slots, ctxs(seg, variant))
             offs = np.arange(C, dtype=np.int64) * (T * L) + seg * Tseg * L
             if on_device:
-                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_dev.data_ptr(), L, cfg,
+                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_dev.data_ptr(), L, c,
                            _lib.AB_MODE_STREAM, scores_on_device=True, scores_dtype=_lib.AB_F32,
                            stream=stream.cuda_stream)
             else:
-                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_host.numpy(), L, cfg,
+                dec.decode(slots, np.full(C, Tseg, np.int32), offs, scores_host.numpy(), L, c,
                            _lib.AB_MODE_STREAM, stream=stream.cuda_stream)
             nh, er, hyps, stride, words = dec.results(C)
             if er.any():
@@ -384,6 +394,7 @@ def run_b200(args, W, world, rank, local):
         infos = dec.get_many(slots)
         out["counters"] = (sum(i.tok_expansions for i in infos), sum(i.emit_arcs for i in infos),
                            sum(i.eps_arcs for i in infos))
+        out["redos"] = sum(i.cut_redos for i in infos)
         out["kernel_ms"] = kernel_ms
         out["launches"] = launches
         return out
@@ -423,13 +434,20 @@ def run_b200(args, W, world, rank, local):
     ms_max = max_over_ranks(ms, world, dev)
     frames_total = C * T * args.steps * world
     value = frames_total / (ms_max / 1000.0)
-    n_tok, a_e, a_x = outs[-1]["counters"]
+    # algorithmic bytes count the reference's work: every token
+    # expansion and arc of the reference algorithm, including the candidates
+    # the expansion-time cutoff drops.  They are the work counters of the same
+    # step decoded with exact_counters (every candidate relaxed; untimed).
+    ref_work = outs[-1]["counters"] if args.exact else step(c=cfg_exact)["counters"]
+    n_tok, a_e, a_x = ref_work
     alg_bytes = 16 * n_tok + 16 * a_e + 12 * a_x
+    xn, xe, xx = outs[-1]["counters"]
     kms = outs[-1]["kernel_ms"]
     peak, peak_kind = hbm_peak()
     achieved = alg_bytes / (kms / 1000.0) / 1e9
-    # measured DRAM traffic (ncu, per channel-frame) scaled to one decode launch
-    # (one segment of all channels), and the random-sector view of the same run
+    # measured DRAM traffic (ncu --set full of one steady-state launch: segment
+    # 2, after two context switches; per channel-frame) scaled to one decode
+    # launch (one segment of all channels), and the random-sector view
     pref = profile_ref()
     traffic = None
     random_access = None
@@ -456,13 +474,25 @@ def run_b200(args, W, world, rank, local):
                    "parallelism": f"channels sharded, {world} GPU(s), no collective",
                    "l2": "inputs (4 GB scores + 0.36 GB graph) exceed L2"},
         "gpu_launches": outs[-1]["launches"] * args.steps,
+        "cutoff": {"mode": "exact_counters" if args.exact else "expansion-time cutoff (verified per frame)",
+                   "frames_redone_per_step": outs[-1]["redos"],
+                   "frames_per_step": C * T},
         "clocks": clk,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "decode_kernel (whole frame loop; expand + epsilon + prune fused)",
+                     "per": "launch (one segment of every channel: the unit the ncu capture measures)",
+                     "alg_bytes_per_launch": alg_bytes / S,
+                     "traffic_over_alg": (traffic / (alg_bytes / S)) if traffic else None,
+                     "launches_per_step": S, "kernel_ms_per_launch": kms / S,
                      "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": kms,
                      "per_channel_frame": {"N": n_tok / (C * T), "A_e": a_e / (C * T),
                                            "A_eps": a_x / (C * T)},
+                     "expanded_per_channel_frame": {"N": xn / (C * T), "A_e": xe / (C * T),
+                                                    "A_eps": xx / (C * T),
+                                                    "note": "what the timed run expanded (the "
+                                                            "cutoff drops candidates that cannot "
+                                                            "survive; alg bytes use the reference's work)"},
                      "random_access": random_access},
         "prep_s": prep,
     }

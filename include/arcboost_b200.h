@@ -70,8 +70,15 @@ typedef struct ab_config {
   int32_t partial_every;
   int32_t endpoint_silence_frames;
   int32_t silence_ilabel;
-  int32_t pad_;
+  /* AB_CFG_EXACT: relax every candidate, as the reference does, so len(store)
+     and eps_truncations count the applications of candidates that cannot
+     survive the frame too.  Default (0): candidates provably outside the
+     frame's survivors are dropped at expansion (same surviving tokens, costs,
+     hypotheses; those two counters then count relaxed candidates only). */
+  int32_t flags;
 } ab_config;
+
+#define AB_CFG_EXACT 1
 
 /* Device capacities per channel; 0 selects a default derived from the graph. */
 typedef struct ab_capacity {
@@ -97,7 +104,8 @@ typedef struct ab_channel_info {
   int32_t num_active;  /* len(_states) */
   int64_t store_len;   /* len(store) */
   int32_t error;       /* last device error code for this channel */
-  int32_t pad_;
+  int32_t cut_redos;   /* frames redone without the expansion-time cutoff (its hint was
+                          below the frame's cutoff; see ab_config.flags) */
   /* work counters accumulated by the device: token expansions,
      emitting arcs, epsilon arcs */
   uint64_t tok_expansions;
@@ -139,6 +147,10 @@ typedef struct ab_decode_args {
 const char *ab_last_error(void);
 int ab_device_count(int32_t *count);
 
+/* Re-reads the environment knobs (AB_CUT_HINT_MIN, AB_CUT_HINT_EXTRA: the
+   expansion-time cutoff's hint margin, see ab_config.flags). */
+void ab_reload_env(void);
+
 /* build_csr (fst.py:165-191) → device CSR split into emitting / epsilon SoA. */
 int ab_graph_create(int32_t device, int32_t start, int32_t num_states, int64_t num_arcs,
                     const int64_t *row_offsets, const int32_t *ilabels, const int32_t *olabels,
@@ -148,6 +160,13 @@ void ab_graph_destroy(ab_graph *g);
 /* num_emitting_labels (fst.py:141-145) and storage facts. */
 int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels, int32_t *weights_f32,
                    int64_t *device_bytes);
+
+/* The expansion-time cutoff's epsilon slack of a context (handle -1: the
+   unbiased graph): the most an epsilon path lowers a token's cost under its
+   weighting, and the number of set bits in the Bloom filter of the states it
+   applies to (negated when the slack bounds paths of at most 64 epsilon arcs
+   only: a negative epsilon cycle or a longer chain). */
+int ab_context_slack(const ab_graph *g, int32_t handle, double *slack, int32_t *neg_states);
 
 /* BiasingContext (biasing.py:86-117) → device context store entry.  arc_indices
    must be strictly increasing and non-negative (indices >= num_arcs never match). */

@@ -31,6 +31,7 @@ AB_IDLE, AB_DECODING, AB_ENDPOINTED, AB_FINISHED = 0, 1, 2, 3
 AB_PARTIAL, AB_FINAL = 0, 1
 AB_F32, AB_F64 = 0, 1
 AB_MODE_ADVANCE, AB_MODE_STREAM = 0, 1
+AB_CFG_EXACT = 1
 AB_CTX_AUTO, AB_CTX_LIST, AB_CTX_BITSET, AB_CTX_LABELS = 0, 1, 2, 3
 AB_MAX_TOKENS, AB_MAX_HASH_SLOTS, AB_MAX_EPSILON_ROUNDS = 131072, 4194304, 2147483647
 
@@ -43,7 +44,7 @@ class ab_config(C.Structure):
         ("partial_every", C.c_int32),
         ("endpoint_silence_frames", C.c_int32),
         ("silence_ilabel", C.c_int32),
-        ("pad_", C.c_int32),
+        ("flags", C.c_int32),
     ]
 
 
@@ -69,7 +70,7 @@ class ab_channel_info(C.Structure):
         ("num_active", C.c_int32),
         ("store_len", C.c_int64),
         ("error", C.c_int32),
-        ("pad_", C.c_int32),
+        ("cut_redos", C.c_int32),
         ("tok_expansions", C.c_uint64),
         ("emit_arcs", C.c_uint64),
         ("eps_arcs", C.c_uint64),
@@ -113,6 +114,7 @@ _I64 = C.c_int64
 SIGNATURES = {
     "ab_last_error": (C.c_char_p, []),
     "ab_device_count": (_I32, [C.POINTER(_I32)]),
+    "ab_reload_env": (None, []),
     "ab_graph_create": (_I32, [_I32, _I32, _I32, _I64, _P, _P, _P, _P, _P, _I32, _P, _P,
                                C.POINTER(_P)]),
     "ab_graph_destroy": (None, [_P]),
@@ -120,6 +122,7 @@ SIGNATURES = {
     "ab_context_register": (_I32, [_P, _P, _I64, C.c_double, _I32, C.POINTER(_I32)]),
     "ab_context_release": (_I32, [_P, _I32]),
     "ab_context_mode": (_I32, [_P, _I32, C.POINTER(_I32)]),
+    "ab_context_slack": (_I32, [_P, _I32, C.POINTER(C.c_double), C.POINTER(_I32)]),
     "ab_decoder_create": (_I32, [_P, C.POINTER(ab_capacity), _I32, C.POINTER(_P)]),
     "ab_decoder_destroy": (None, [_P]),
     "ab_decoder_query": (_I32, [_P, C.POINTER(ab_capacity), C.POINTER(_I64)]),

@@ -63,6 +63,9 @@ struct HostCtx {
   u32 *d_list = nullptr;
   u32 *d_bits = nullptr;   // CTX_BITSET: emitting record positions; CTX_LABELS: olabel bitmap
   u32 *d_bits_x = nullptr; // CTX_BITSET: epsilon record positions
+  double slack = 0.0;      // eps_slack of the context's weighting
+  int slack_rounds = 0;
+  u32 *d_neg = nullptr;    // its neg bitmap (NEG_WORDS)
 };
 
 struct ab_graph {
@@ -80,6 +83,15 @@ struct ab_graph {
   // addressed before the arc record arrives (issued next to the record load)
   std::vector<u32> arc_pos;
   uint64_t e_tot = 0, x_tot = 0; // records in the emitting / epsilon arrays
+  // epsilon subgraph on the host (arc ids increasing; reverse adjacency by
+  // destination) for the epsilon slack of a weighting (eps_slack)
+  std::vector<u32> xe_g, xe_src, xe_dst, xr_off, xr_arc;
+  std::vector<u32> xe_neg; // epsilon arcs with a negative graph weight
+  std::vector<double> xe_w;
+  std::vector<double> h_buf; // eps_slack scratch, one value per state
+  double slack0 = 0.0;       // slack of the unbiased graph
+  int slack0_rounds = 0;
+  u32 *d_neg0 = nullptr;     // its neg bitmap (NEG_WORDS)
   uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
   unsigned char *deg = nullptr;              // per state arc counts (DecodeParams::deg)
   void *e_arcs = nullptr, *x_arcs = nullptr;
@@ -95,6 +107,7 @@ struct ab_decoder {
   ab_graph *g = nullptr;
   int device = 0;
   int max_ch = 0;
+  std::vector<int32_t> slot_ctx; // context handle of every slot (host mirror: sizes shared memory)
   ab_capacity cap{};
   u32 table_cap = 0;
   int hashed = 0;
@@ -159,6 +172,9 @@ extern "C" int ab_device_count(int32_t *count) {
 }
 
 // ------------------------------------------------------------------ graph
+
+static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
+                        std::vector<u32> *neg_bits, int *rounds_ok);
 
 extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states,
                                int64_t num_arcs, const int64_t *row_offsets,
@@ -310,6 +326,25 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       }
     }
   }
+  for (int s = 0; s < num_states; ++s)
+    for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a)
+      if (ilabels[a] == 0) {
+        g->xe_g.push_back((u32)a);
+        g->xe_src.push_back((u32)s);
+        g->xe_dst.push_back((u32)next_states[a]);
+        if (weights[a] < 0.0) g->xe_neg.push_back((u32)g->xe_w.size());
+        g->xe_w.push_back(weights[a]);
+      }
+  g->xr_off.assign((size_t)num_states + 1, 0);
+  for (u32 d : g->xe_dst) g->xr_off[d + 1]++;
+  for (int s = 0; s < num_states; ++s) g->xr_off[s + 1] += g->xr_off[s];
+  g->xr_arc.resize(g->xe_g.size());
+  {
+    std::vector<u32> fill(g->xr_off.begin(), g->xr_off.end() - 1);
+    for (size_t i = 0; i < g->xe_g.size(); ++i) g->xr_arc[fill[g->xe_dst[i]]++] = (u32)i;
+  }
+  std::vector<u32> neg0;
+  g->slack0 = eps_slack(g, {}, 0.0, &neg0, &g->slack0_rounds);
   size_t acc = 0;
   unsigned char *de = nullptr, *dx = nullptr;
   std::vector<uint2> erng(num_states), xrng(num_states);
@@ -325,6 +360,11 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   g->e_arcs = de;
   g->x_arcs = dx;
+  if (dmalloc(&g->d_neg0, NEG_WORDS, acc) ||
+      cudaMemcpy(g->d_neg0, neg0.data(), NEG_WORDS * sizeof(u32), cudaMemcpyHostToDevice) != cudaSuccess) {
+    ab_graph_destroy(g);
+    return fail(AB_ERR_CUDA, "device allocation for the graph failed");
+  }
   g->bytes = acc;
   if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMemcpy(g->e_rng, erng.data(), num_states * sizeof(uint2), cudaMemcpyHostToDevice) ||
@@ -347,6 +387,7 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
     cudaFree(c.d_list);
     cudaFree(c.d_bits);
     cudaFree(c.d_bits_x);
+    cudaFree(c.d_neg);
   }
   cudaFree(g->d_ctxs);
   cudaFree(g->e_rng);
@@ -355,6 +396,7 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   cudaFree(g->e_arcs);
   cudaFree(g->x_arcs);
   cudaFree(g->final_cost);
+  cudaFree(g->d_neg0);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -370,6 +412,75 @@ extern "C" int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels,
 
 // ---------------------------------------------------------------- contexts
 
+// Epsilon slack of a weighting of the graph (the kernel's expansion-time
+// cutoff, decode_kernel.cuh advance()): S = -min over states s of h(s), where
+// h(s) = min(0, cheapest epsilon path leaving s) under the effective weights
+// w + discount on boosted arcs (biasing.py:166-171).  An epsilon path lowers a
+// token's cost by at most S.  Computed backwards from the negative epsilon arcs
+// (Bellman-Ford over reverse epsilon arcs, only states whose h drops below 0
+// are visited).  When h has not settled after 64 rounds (a negative epsilon
+// cycle, or a longer negative chain) the result bounds paths of at most 64
+// arcs only: *rounds_ok = 64 (the kernel then uses it for max_epsilon_expansion
+// <= 64 only), else INT_MAX.  neg_bits: Bloom filter of the states with
+// h < 0 (decode_kernel.cuh neg_test).  `boosted` = sorted arc ids.
+static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
+                        std::vector<u32> *neg_bits, int *rounds_ok) {
+  if (!boosted.empty() && discount >= 0.0 && g->xe_neg.size() == 0) {
+    // boosting only raises weights: no negative epsilon arc anywhere
+    neg_bits->assign(NEG_WORDS, 0u);
+    *rounds_ok = INT32_MAX;
+    return 0.0;
+  }
+  auto is_boosted = [&](u32 gid) { return std::binary_search(boosted.begin(), boosted.end(), gid); };
+  auto weff = [&](u32 i) { return is_boosted(g->xe_g[i]) ? g->xe_w[i] + discount : g->xe_w[i]; };
+  if (g->h_buf.empty()) g->h_buf.assign((size_t)g->num_states, 0.0);
+  std::vector<double> &h = g->h_buf;
+  std::vector<u32> front, next, touched;
+  auto lower = [&](u32 s, double c, std::vector<u32> &out) {
+    if (c < h[s]) {
+      if (h[s] == 0.0) touched.push_back(s);
+      h[s] = c;
+      out.push_back(s);
+    }
+  };
+  // negative epsilon arcs: the graph's own (not boosted) and boosted ones below 0
+  for (u32 i : g->xe_neg)
+    if (weff(i) < 0.0) lower(g->xe_src[i], weff(i), front);
+  if (discount < 0.0)
+    for (u32 gid : boosted) {
+      auto it = std::lower_bound(g->xe_g.begin(), g->xe_g.end(), gid);
+      if (it == g->xe_g.end() || *it != gid) continue; // not an epsilon arc
+      const u32 i = (u32)(it - g->xe_g.begin());
+      if (g->xe_w[i] >= 0.0 && g->xe_w[i] + discount < 0.0) lower(g->xe_src[i], g->xe_w[i] + discount, front);
+    }
+  int rounds = 0;
+  while (!front.empty() && rounds < 64) {
+    std::sort(front.begin(), front.end());
+    front.erase(std::unique(front.begin(), front.end()), front.end());
+    next.clear();
+    for (u32 d : front)
+      for (u32 k = g->xr_off[d]; k < g->xr_off[d + 1]; ++k) {
+        const u32 i = g->xr_arc[k];
+        lower(g->xe_src[i], weff(i) + h[d], next);
+      }
+    front.swap(next);
+    ++rounds;
+  }
+  double lo = 0.0;
+  neg_bits->assign(NEG_WORDS, 0u);
+  for (u32 s : touched) {
+    lo = std::min(lo, h[s]);
+    if (h[s] < 0.0) {
+      (*neg_bits)[neg_h1(s) >> 5] |= 1u << (neg_h1(s) & 31);
+      (*neg_bits)[neg_h2(s) >> 5] |= 1u << (neg_h2(s) & 31);
+    }
+    h[s] = 0.0;
+  }
+  *rounds_ok = front.empty() ? INT32_MAX : 64;
+  // margin for the f64 rounding of path sums (the kernel adds its own for the hint)
+  return lo < 0.0 ? -lo * (1.0 + 1e-9) + 1e-9 : 0.0;
+}
+
 static int sync_ctx_table(ab_graph *g) {
   std::vector<CtxDesc> h(g->ctxs.size());
   for (size_t i = 0; i < g->ctxs.size(); ++i) {
@@ -382,6 +493,9 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].list = c.d_list;
     h[i].bits = c.d_bits;
     h[i].bits_x = c.d_bits_x;
+    h[i].slack = c.slack;
+    h[i].slack_rounds = c.slack_rounds;
+    h[i].neg = c.d_neg;
   }
   if (h.size() > g->d_ctxs_cap) {
     cudaFree(g->d_ctxs);
@@ -437,6 +551,10 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   if (mode != AB_CTX_LIST && mode != AB_CTX_BITSET && mode != AB_CTX_LABELS)
     return fail(AB_ERR_INVALID, "bad context mode %d", mode);
   c.abi_mode = mode;
+  std::vector<u32> negb;
+  c.slack = eps_slack(g, list, discount, &negb, &c.slack_rounds);
+  CK(cudaMalloc(&c.d_neg, NEG_WORDS * sizeof(u32)));
+  CK(cudaMemcpy(c.d_neg, negb.data(), NEG_WORDS * sizeof(u32), cudaMemcpyHostToDevice));
   c.mode = mode == AB_CTX_LABELS ? CTX_LABELS : mode == AB_CTX_BITSET ? CTX_BITSET : CTX_SLIST;
   CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
   if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
@@ -484,6 +602,27 @@ extern "C" int ab_context_mode(const ab_graph *g, int32_t handle, int32_t *mode)
   return AB_OK;
 }
 
+extern "C" int ab_context_slack(const ab_graph *g, int32_t handle, double *slack, int32_t *neg_states) {
+  if (!g) return fail(AB_ERR_INVALID, "null graph");
+  const u32 *bits = nullptr;
+  std::vector<u32> hb(NEG_WORDS);
+  if (handle < 0) {
+    *slack = g->slack0;
+    bits = g->d_neg0;
+  } else {
+    if (handle >= (int)g->ctxs.size() || !g->ctxs[handle].live)
+      return fail(AB_ERR_UNKNOWN_CTX, "unknown context handle %d", handle);
+    *slack = g->ctxs[handle].slack;
+    bits = g->ctxs[handle].d_neg;
+  }
+  CK(cudaMemcpy(hb.data(), bits, NEG_WORDS * sizeof(u32), cudaMemcpyDeviceToHost));
+  int n = 0;
+  for (u32 w : hb) n += __builtin_popcount(w);
+  if (handle < 0 ? g->slack0_rounds < INT32_MAX : g->ctxs[handle].slack_rounds < INT32_MAX) n = -n;
+  *neg_states = n;
+  return AB_OK;
+}
+
 extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
   if (!g || handle < 0 || handle >= (int)g->ctxs.size() || !g->ctxs[handle].live)
     return fail(AB_ERR_UNKNOWN_CTX, "unknown context handle %d", handle);
@@ -492,6 +631,7 @@ extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
   cudaFree(c.d_list);
   cudaFree(c.d_bits);
   cudaFree(c.d_bits_x);
+  cudaFree(c.d_neg);
   c = HostCtx();
   return sync_ctx_table(g);
 }
@@ -515,6 +655,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   d->g = g;
   d->device = g->device;
   d->max_ch = max_channels;
+  d->slot_ctx.assign((size_t)max_channels, -1);
   // Token table: direct (one value per graph state) when it fits the memory
   // budget next to the other per-channel pools, else hashed.  table_slots > 0
   // forces the choice: >= num_states gives a direct table, fewer slots a
@@ -662,6 +803,7 @@ extern "C" int ab_channel_init(ab_decoder *d, int32_t ch, int32_t context) {
   info.status = AB_IDLE;
   info.fresh = 1;
   info.context = context;
+  d->slot_ctx[ch] = context;
   // the epoch and path fields stay: epochs must never repeat within a slot
   CK(cudaMemcpy(&d->chans[ch].info, &info, sizeof(info), cudaMemcpyHostToDevice));
   int zero[4] = {0, 0, 0, 0}; // path_len, max_depth, arena_half, rec_phys
@@ -682,6 +824,7 @@ extern "C" int ab_channel_put(ab_decoder *d, int32_t ch, const ab_channel_info *
   if ((rc = check_slot(d, ch)) || (rc = check_ctx(d, info->context))) return rc;
   CK(cudaSetDevice(d->g->device));
   CK(cudaMemcpy(&d->chans[ch].info, info, sizeof(*info), cudaMemcpyHostToDevice));
+  d->slot_ctx[ch] = info->context;
   return AB_OK;
 }
 
@@ -713,6 +856,8 @@ __global__ void scatter_infos(int n, const int *slots, ChanState *chans,
       chans[slots[i]].max_depth = 0;
       chans[slots[i]].arena_half = 0;
       chans[slots[i]].rec_phys = 0;
+      chans[slots[i]].prev_cut = INFINITY;
+      chans[slots[i]].cut_rise = 0.0;
     }
   }
 }
@@ -751,6 +896,7 @@ static int put_infos(ab_decoder *d, int n, const int32_t *slots, const ab_channe
   int rc;
   CK(cudaSetDevice(d->g->device));
   if ((rc = ensure_infos(d, n))) return rc;
+  for (int i = 0; i < n; ++i) d->slot_ctx[slots[i]] = infos[i].context;
   cudaStream_t st = d->g->stream;
   CK(cudaMemcpyAsync(d->d_islots, slots, n * sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d->d_infos, infos, n * sizeof(ab_channel_info), cudaMemcpyHostToDevice, st));
@@ -860,6 +1006,25 @@ static int ensure_batch(ab_decoder *d, size_t n) {
   return AB_OK;
 }
 
+// Environment knobs read once (ab_reload_env re-reads them): the cutoff
+// hint's minimum rise per frame and extra margin (decode_kernel.cuh advance()).
+struct Knobs {
+  bool loaded = false;
+  double hint_min = 1.0, hint_extra = 0.5;
+};
+static Knobs &g_knobs() {
+  static Knobs k;
+  if (!k.loaded) {
+    const char *a = getenv("AB_CUT_HINT_MIN"), *b = getenv("AB_CUT_HINT_EXTRA");
+    k.hint_min = a ? atof(a) : 1.0;
+    k.hint_extra = b ? atof(b) : 0.5;
+    k.loaded = true;
+  }
+  return k;
+}
+
+extern "C" void ab_reload_env(void) { g_knobs().loaded = false; }
+
 static void fill_params(ab_decoder *d, DecodeParams &P) {
   ab_graph *g = d->g;
   memset(&P, 0, sizeof(P));
@@ -871,6 +1036,12 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
 #endif
   P.e_rng = g->e_rng;
   P.deg = g->deg;
+  P.exact = 1; // the expansion-time cutoff is per decode call (ab_config.flags)
+  P.slack0 = g->slack0;
+  P.slack0_rounds = g->slack0_rounds;
+  P.neg0 = g->d_neg0;
+  P.hint_min = g_knobs().hint_min;
+  P.hint_extra = g_knobs().hint_extra;
   P.e_arcs = g->e_arcs;
   P.x_rng = g->x_rng;
   P.x_arcs = g->x_arcs;
@@ -915,7 +1086,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
 #define AB_STAGE_CHUNKS 4 // host-score chunks per ab_decode call (copy/decode overlap)
 #endif
 
-static size_t dyn_smem_max() { return CTX_SMEM_WORDS * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
+static size_t dyn_smem_max() { return (CTX_SMEM_WORDS + NEG_WORDS) * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
 
 // CTA size per batch: few channels get more threads each (a channel's frame
 // is one CTA's work), many channels fill the SMs with 256-thread CTAs.
@@ -962,6 +1133,15 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   if (env && atoi(env) > 0) resident = atoi(env);
   const int waves = (n + resident - 1) / resident;
   const int grid = (n + waves - 1) / waves;
+  if (getenv("AB_VERBOSE")) {
+    static int said = 0;
+    if (said++ < 4) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, decode_kernel<BLOCK, F, S>);
+      fprintf(stderr, "[arcboost] decode_kernel<%d>: %d CTAs/SM, grid %d, static smem %zu, dynamic %zu, regs %d\n",
+              BLOCK, per_sm, grid, (size_t)fa.sharedSizeBytes, smem, fa.numRegs);
+    }
+  }
   decode_kernel<BLOCK, F, S><<<grid, BLOCK, smem, st>>>(P);
   return cudaGetLastError();
 }
@@ -1045,10 +1225,36 @@ __global__ void pack_kernel(int n, const int *n_hyps, const long long *wused, co
   }
 }
 
-static size_t dyn_smem(int L, bool s64) {
+// Dynamic shared memory of a launch: [context words | score row | neg Bloom
+// filter | (small graphs) token table].  The context area holds the largest
+// shared-memory context of the launch's channels (LABELS bitmap words or LIST
+// arcs, <= CTX_SMEM_WORDS); the Bloom filter is there only when one of them
+// (or the unbiased graph) has an epsilon slack.  Shared memory not taken is
+// L1 cache for the arc records and token lists.
+static void launch_smem_layout(ab_decoder *d, const int32_t *slots, int n, DecodeParams &P) {
+  const ab_graph *g = d->g;
+  u32 words = 0;
+  bool neg = false;
+  for (int i = 0; i < n; ++i) {
+    const int h = d->slot_ctx[slots[i]];
+    const bool live = h >= 0 && h < (int)g->ctxs.size() && g->ctxs[h].live && g->ctxs[h].k;
+    if (!live) {
+      neg |= g->slack0 > 0.0;
+      continue;
+    }
+    const HostCtx &c = g->ctxs[h];
+    if (c.mode == CTX_LABELS) words = std::max(words, c.words);
+    else if (c.mode == CTX_SLIST && c.k <= (u32)CTX_SMEM_WORDS) words = std::max(words, c.k);
+    neg |= c.slack > 0.0;
+  }
+  P.ctx_words_cap = (words + 3) & ~3u; // keeps the score row 16-byte aligned
+  P.neg_words = neg ? NEG_WORDS : 0u;
+}
+
+static size_t dyn_smem(int L, bool s64, const DecodeParams &P) {
   size_t row = (size_t)L * (s64 ? 8 : 4);
-  row = row > (size_t)SCORE_SMEM_MAX_BYTES ? 0 : (row + 15) / 16 * 16; // a shared-memory table follows
-  return CTX_SMEM_WORDS * sizeof(u32) + row;
+  row = row > (size_t)SCORE_SMEM_MAX_BYTES ? 0 : (row + 15) / 16 * 16;
+  return (size_t)P.ctx_words_cap * sizeof(u32) + row + (size_t)P.neg_words * sizeof(u32);
 }
 
 extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
@@ -1158,6 +1364,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   P.partial_every = cf.partial_every;
   P.endpoint_silence_frames = cf.endpoint_silence_frames;
   P.silence_ilabel = cf.silence_ilabel;
+  P.exact = (cf.flags & AB_CFG_EXACT) ? 1 : 0;
   P.hyps = d->d_hyps;
   P.hyp_stride = hyp_stride;
   P.n_hyps = d->d_nhyps;
@@ -1170,7 +1377,8 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   P.frames = d->d_frames;
   P.stream_frames = d->d_sframes;
   P.score_off = d->d_soff;
-  const size_t smem = dyn_smem(g->L, s64);
+  launch_smem_layout(d, slots.data(), n, P);
+  const size_t smem = dyn_smem(g->L, s64, P);
   std::vector<int> act;
   std::vector<int> remaining(n);
   std::vector<long long> cur_off(n);
@@ -1387,6 +1595,7 @@ static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *w
   P.words_used = d->d_wused;
   CK(cudaMemcpyAsync(d->d_slots, &ch, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d->d_wused, 0, sizeof(long long), st));
+  P.ctx_words_cap = CTX_SMEM_WORDS;
   const size_t smem = CTX_SMEM_WORDS * sizeof(u32);
   cudaError_t le = d->hashed ? (g->fmt16 ? launch_hyp<256, Fmt16<true>, float>(P, which, smem, st)
                                          : launch_hyp<256, Fmt24<true>, float>(P, which, smem, st))

@@ -73,6 +73,20 @@ __device__ __forceinline__ u32 aux_src(u32 src, u32 rflags, u32 g) {
          (g == G_START ? AUX_START : 0u);
 }
 constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
+// Bloom filter (two hashes, 128 Kbit = 16 KB) of the states from which an
+// epsilon path lowers a cost: the only states the cutoff's slack applies to
+// (advance()).  False positives only keep a few more candidates.
+#ifndef AB_NEG_WORDS
+#define AB_NEG_WORDS 4096
+#endif
+constexpr u32 NEG_WORDS = AB_NEG_WORDS;
+constexpr int NEG_SHIFT = 32 - 5 - __builtin_ctz(NEG_WORDS); // hashes of log2(32 * NEG_WORDS) bits
+__host__ __device__ __forceinline__ u32 neg_h1(u32 s) { return (s * 2654435761u) >> NEG_SHIFT; }
+__host__ __device__ __forceinline__ u32 neg_h2(u32 s) { return ((s ^ (s >> 16)) * 0x85EBCA6Bu) >> NEG_SHIFT; }
+__device__ __forceinline__ bool neg_test(const u32 *b, u32 s) {
+  const u32 a = neg_h1(s), c = neg_h2(s);
+  return ((b[a >> 5] >> (a & 31)) & (b[c >> 5] >> (c & 31)) & 1u) != 0;
+}
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
 constexpr u32 SLOT_E = 4, SLOT_X = 2;         // arc records per state slot (emitting / epsilon)
 constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the overflow area
@@ -150,6 +164,10 @@ struct CtxDesc {
   const u32 *list; // sorted arc ids
   const u32 *bits;   // CTX_BITSET: bit per emitting record position, CTX_LABELS: olabel bitmap
   const u32 *bits_x; // CTX_BITSET: bit per epsilon record position
+  double slack;      // -min over states of the cheapest epsilon path from them (>= 0)
+  int slack_rounds;  // slack bounds paths of at most this many epsilon arcs (INT_MAX: any)
+  int pad2;
+  const u32 *neg;    // NEG_WORDS Bloom filter of the states where that path is negative
 };
 
 // Arc record formats.  Fmt16: f32 weight, 16-bit labels (one 16 B load).
@@ -222,6 +240,8 @@ struct ChanState {
   u32 rec_phys;   // records physically in the live half
   u32 tok_half;   // which half of the channel's token-provenance buffer is current
   double prev_best; // best token cost of the previous frame (cost histogram window)
+  double prev_cut;  // the previous frame's pruning cutoff (inf: none yet), see advance()
+  double cut_rise;  // recent rise of the cutoff per frame (decaying maximum)
 };
 
 struct DevHyp {
@@ -284,6 +304,15 @@ struct DecodeParams {
   const void *scores;
   int mode;
   int final_chunk; // stream mode: the frames of this launch end the streams (finalize)
+  // expansion-time cutoff (advance()): off when exact; slack of unbiased
+  // decoding; hint = previous cutoff + max(rise, hint_min) + hint_extra
+  int exact;
+  double slack0, hint_min, hint_extra;
+  int slack0_rounds;
+  const u32 *neg0; // NEG_WORDS bitmap of the unbiased graph
+  // dynamic shared memory layout (host: launch_smem_layout)
+  u32 ctx_words_cap; // context words in shared memory (LABELS bitmap / LIST arcs)
+  u32 neg_words;     // 0 or NEG_WORDS: the neg Bloom filter after the score row
   // config (decoder.py:33-48)
   double beam;
   int max_active, max_eps, partial_every, endpoint_silence_frames, silence_ilabel;
@@ -596,6 +625,8 @@ struct Shared {
   u32 eps_n;    // entries in the channel's epsilon-frontier list this frame
   u32 emit_end; // rows below come from the emitting pass (their source is a token)
   int best_last_il;
+  double cut_hint; // this attempt's cutoff hint (inf: unfiltered), see advance()
+  int filtered;
 #ifdef AB_PROFILE
   unsigned long long prof[PF_N];
   long long prof_t;
@@ -638,6 +669,11 @@ template <typename F, typename S> struct Chan {
   u32 ctx_words;
   u32 epoch;
   u32 etag;
+  double slack; // the context's epsilon slack (CtxDesc::slack)
+  int slack_rounds;
+  double ucut0; // this attempt's candidate cutoff (candidates above it are not relaxed) ...
+  double ucut;  // ... plus the slack, for states in the neg bitmap
+  const u32 *neg; // shared-memory copy of the context's (or graph's) neg bitmap
   // expansion tile (shared memory)
   u32 *t_a0;
   u32 *t_pref;
@@ -1082,6 +1118,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           else cand = cj[u] + we;                                    // decoder.py:268
           ck[u] = cost_key(cand);
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
+          // provably outside this frame's survivors (advance())
+          on[u] = cand <= C.ucut0 || (cand <= C.ucut && neg_test(C.neg, d[u]));
         }
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
@@ -1212,6 +1250,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           else cand = cj[u] + we;                                    // decoder.py:268
           ck[u] = cost_key(cand);
           rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
+          // provably outside this frame's survivors (advance())
+          on[u] = cand <= C.ucut0 || (cand <= C.ucut && neg_test(C.neg, d[u]));
         }
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
@@ -1469,7 +1509,7 @@ __device__ u64 radix_select(Shared &sh, u32 *hist, u32 n, KeyFn keyf, u64 lo, u6
 // state) with radix selects over their keys and then their states.  Bucket
 // order is cost order, so the result is the exact top max_active.
 template <int BLOCK, typename F, typename S>
-__device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+__device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   constexpr int QP = PRUNE_Q;
   constexpr u32 TILE = BLOCK * QP;
   // digit histograms of the split-bucket selection live in the expansion tile
@@ -1480,7 +1520,6 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const double thr = key_cost(best_ck) + P.beam;
   const u64 thr_ck = cost_key(thr);
   u32 *scr_state = C.app_list; // the kill queue is free until the next frame
-  if (tid == 0 && sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
   // split bucket: the first bucket where the live rows below and in it reach
   // max_active; buckets below the threshold's bucket are entirely in the beam
   const u32 bt = hbucket(sh, thr);
@@ -1512,7 +1551,20 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   }
   const u32 split = sh.sel;
   u32 below = sh.cum; // live rows in buckets < split (when the split is below bt)
+  // The frame's cutoff C* (the max_active-th cost, at most its bucket's upper
+  // edge, or best + beam when the beam holds fewer rows): a filtered attempt
+  // is exact iff C* <= its hint (advance()); otherwise the frame is redone.
+  const double cut = split < bt ? fmin(thr, sh.hbase + ((double)split + 1.0001) / sh.hscale) : thr;
+  const bool verified = !sh.filtered || cut <= sh.cut_hint;
   __syncthreads();
+  if (!verified) return false;
+  if (tid == 0) {
+    if (sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
+    const double prev = C.cs->prev_cut;
+    const double rise = prev < INFINITY ? cut - prev : 0.0;
+    C.cs->cut_rise = fmax(rise, 0.8 * C.cs->cut_rise);
+    C.cs->prev_cut = cut;
+  }
   // pass over the rows: survivors (bucket < split) -> token list; split
   // bucket within the beam -> set aside; best (cost, state)
   u64 bk = ~0ull;
@@ -1574,7 +1626,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     if (n_tok + n_mem + need > P.flog_cap) { // survivors' rows would reach the set-aside rows
       if (tid == 0) set_error(sh, E_CAP);
       __syncthreads();
-      return;
+      return true;
     }
     // exact (cost, state) order inside the split bucket
     u64 tc = ~0ull;
@@ -1656,6 +1708,7 @@ __device__ void prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   }
   __syncthreads();
   PROF_MARK(sh, PF_PRUNE_OUT);
+  return true;
 }
 
 // Token list := every live row of the epoch (after the utterance-start
@@ -1681,7 +1734,11 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   }
   __syncthreads();
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, -1);
-  if (threadIdx.x == 0) C.cs->prev_best = key_cost(sh.min_ck);
+  if (threadIdx.x == 0) {
+    C.cs->prev_best = key_cost(sh.min_ck);
+    C.cs->prev_cut = INFINITY; // the start closure is not pruned: no cutoff to start from
+    C.cs->cut_rise = 0.0;
+  }
   __syncthreads();
 }
 
@@ -1835,6 +1892,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       return;
     }
   }
+  if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
+  __syncthreads();
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
     epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, 1u); // utterance-start closure, no prune
@@ -1846,23 +1905,67 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   PROF_MARK(sh, PF_START);
   const u32 n_tok = (u32)cs->info.num_active;
   if (threadIdx.x == 0) cs->info.status = AB_DECODING;
-  next_epoch<BLOCK>(P, C, sh);
-  expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
-  __syncthreads();
-  apply_kills<BLOCK>(P, C, sh);
-  PROF_MARK(sh, PF_EMIT_X);
-  if (sh.error) return;
-  const u32 n_app = sh.n_app;
-  if (threadIdx.x == 0) sh.emit_end = sh.flog_n;
-  __syncthreads();
-  if (n_app == 0) {
-    // no emitting arcs: every token dies (decoder.py:394-398)
-    if (threadIdx.x == 0) cs->info.num_active = 0;
-  } else {
-    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, n_app);
+  // Expansion-time cutoff.  No token whose cost exceeds the frame's cutoff C*
+  // (min(best + beam, max_active-th cost)) survives prune, and an epsilon
+  // path from a state lowers a cost by at most the context's slack S (-min
+  // over states of the cheapest epsilon path from them: 0 without negative
+  // epsilon weights).  So a candidate above U + S, for any U >= C*, is
+  // neither a survivor nor on a survivor's path: dropping it leaves the
+  // surviving tokens, their costs and their provenance exactly as the
+  // reference computes them.  U is a hint (the previous frame's cutoff plus
+  // its recent rise), verified after the closure: the filtered frame's own
+  // cutoff C*_f >= C* (its candidates are a subset), so C*_f <= U proves the
+  // frame exact; else the frame is redone unfiltered (prune returns false
+  // before it has written anything).  Emission records and epsilon-round
+  // truncations of dropped candidates are not counted (P.exact keeps every
+  // candidate and the reference's len(store) / eps_truncations).
+  const unsigned long long c_tok = sh.cnt_tok, c_emit = sh.cnt_emit, c_eps = sh.cnt_eps;
+  const long long eps_tr = cs->info.eps_truncations;
+  bool filt = !P.exact && cs->prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
+              P.max_eps <= C.slack_rounds;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double hint = filt ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra : INFINITY;
+      sh.cut_hint = hint;
+      sh.filtered = filt ? 1 : 0;
+      // (+ a margin for the f64 rounding of path sums)
+      const double m = 1e-9 * fmax(1.0, fabs(hint));
+      C.ucut0 = filt ? hint + m : INFINITY;
+      C.ucut = filt ? hint + C.slack + m : INFINITY;
+    }
+    next_epoch<BLOCK>(P, C, sh);
+    expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
+    __syncthreads();
+    apply_kills<BLOCK>(P, C, sh);
+    PROF_MARK(sh, PF_EMIT_X);
     if (sh.error) return;
-    prune<BLOCK>(P, C, sh);
+    const u32 n_app = sh.n_app;
+    if (threadIdx.x == 0) sh.emit_end = sh.flog_n;
+    __syncthreads();
+    bool ok = true;
+    if (n_app == 0) {
+      // no emitting arcs: every token dies (decoder.py:394-398); a filtered
+      // attempt proves nothing here
+      if (filt) ok = false;
+      else if (threadIdx.x == 0) cs->info.num_active = 0;
+    } else {
+      epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, n_app);
+      if (sh.error) return;
+      ok = prune<BLOCK>(P, C, sh);
+    }
+    if (ok) break;
+    __syncthreads();
+    if (threadIdx.x == 0) { // redo unfiltered: undo the attempt's counters
+      sh.cnt_tok = c_tok;
+      sh.cnt_emit = c_emit;
+      sh.cnt_eps = c_eps;
+      cs->info.eps_truncations = eps_tr;
+      cs->info.cut_redos += 1;
+    }
+    filt = false;
   }
+  if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
   __syncthreads();
   if (threadIdx.x == 0) {
     cs->info.frame_index += 1;
@@ -2025,6 +2128,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
     sh.rec_logical = 0;
     cs->path_len = 0;
     cs->max_depth = 0;
+    cs->prev_cut = INFINITY;
     cs->info.utterance_index += 1;
     cs->info.status = AB_IDLE;
   }
@@ -2037,7 +2141,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
 template <int BLOCK, typename F, typename S>
 __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh_row,
                               u32 *sh_ctx, u32 *t_a0 = nullptr, u32 *t_pref = nullptr,
-                              double *t_cost = nullptr, u32 *t_src = nullptr) {
+                              double *t_cost = nullptr, u32 *t_src = nullptr, u32 *sh_neg = nullptr) {
   const int slot = P.slots[b];
   const int h = P.chans[slot].info.context;
   __syncthreads(); // the previous channel of this CTA is done with C
@@ -2077,6 +2181,10 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.ctx_list = nullptr;
     C.ctx_bits = nullptr;
     C.ctx_bits_x = nullptr;
+    C.slack = P.slack0;
+    C.slack_rounds = P.slack0_rounds;
+    C.ucut0 = C.ucut = INFINITY;
+    C.neg = sh_neg;
     C.t_a0 = t_a0;
     C.t_pref = t_pref;
     C.t_cost = t_cost;
@@ -2093,7 +2201,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
       mode = CTX_LABELS;
     } else if (d.mode == CTX_BITSET) {
       mode = CTX_BITSET;
-    } else if (d.k <= (u32)CTX_SMEM_WORDS) {
+    } else if (d.k <= P.ctx_words_cap) {
       for (u32 i = threadIdx.x; i < d.k; i += BLOCK) sh_ctx[i] = d.list[i];
       mode = CTX_SLIST;
     } else {
@@ -2106,7 +2214,21 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
       C.ctx_words = d.words;
       C.ctx_bits = mode == CTX_LABELS ? sh_ctx : d.bits;
       C.ctx_bits_x = d.bits_x;
+      if (mode != CTX_NONE) {
+        C.slack = d.slack;
+        C.slack_rounds = d.slack_rounds;
+      }
       C.ctx_list = mode == CTX_SLIST ? sh_ctx : d.list;
+    }
+  }
+  __syncthreads();
+  if (C.slack > 0.0) { // the neg Bloom filter of the weighting in use
+    const u32 *src = P.neg0;
+    if (h >= 0 && h < P.num_ctxs && P.ctxs[h].k) src = P.ctxs[h].neg;
+    if (sh_neg && src) {
+      for (u32 i = threadIdx.x; i < NEG_WORDS; i += BLOCK) sh_neg[i] = src[i];
+    } else if (threadIdx.x == 0) {
+      C.slack = INFINITY; // no filter in this launch's layout: no cutoff for this channel
     }
   }
   __syncthreads();
@@ -2128,15 +2250,17 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   __shared__ u32 tile_a0[BLOCK * exp_q<BLOCK>()];
   __shared__ u32 tile_pref[BLOCK * exp_q<BLOCK>() + 1];
   __shared__ u32 tile_src[BLOCK * exp_q<BLOCK>()];
+  // dynamic: context words | score row | neg Bloom filter | (small graphs) the
+  // channel's direct token table (host: launch_smem_layout, dyn_smem)
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
-  S *sh_row = reinterpret_cast<S *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32));
+  S *sh_row = reinterpret_cast<S *>(dyn_smem + P.ctx_words_cap * sizeof(u32));
   const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
-  // small graphs: the channel's direct token table in shared memory, after
-  // the context words and the score row (host: smem_table_bytes)
-  uint4 *sh_table = reinterpret_cast<uint4 *>(dyn_smem + CTX_SMEM_WORDS * sizeof(u32) +
-                                              (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
+  u32 *sh_neg = reinterpret_cast<u32 *>(dyn_smem + P.ctx_words_cap * sizeof(u32) +
+                                        (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
+  uint4 *sh_table = reinterpret_cast<uint4 *>(sh_neg + P.neg_words);
   for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
-    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src);
+    setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src,
+                         P.neg_words ? sh_neg : nullptr);
     ChanState *cs = C.cs;
     if (F::smem_table) { // a fresh table per channel: zero tags are never current
       for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) sh_table[i] = make_uint4(0, 0, 0, 0);

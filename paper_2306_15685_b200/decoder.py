@@ -42,6 +42,12 @@ class DecoderConfig:
     partial_every: int = 10
     endpoint_silence_frames: int = 20
     silence_ilabel: int = 0
+    # Not in the reference (decoder.py:33-48).  False: candidates that provably
+    # cannot survive the frame are dropped at expansion (same surviving tokens,
+    # costs and hypotheses; len(store) and eps_truncations then count the
+    # relaxed candidates only).  True: every candidate is relaxed, as the
+    # reference does, so those two counters match it too.
+    exact_counters: bool = False
 
     def __post_init__(self) -> None:
         if self.beam <= 0:

@@ -108,6 +108,13 @@ class DeviceGraph:
         check(_lib.load().ab_context_mode(self.handle, int(handle), C.byref(m)))
         return m.value
 
+    def context_slack(self, handle: int) -> tuple[float, int]:
+        """(epsilon slack, states flagged in its bitmap) of a context (-1: unbiased)."""
+        v = C.c_double()
+        n = C.c_int32()
+        check(_lib.load().ab_context_slack(self.handle, int(handle), C.byref(v), C.byref(n)))
+        return v.value, n.value
+
     def release_context(self, handle: int) -> None:
         check(_lib.load().ab_context_release(self.handle, int(handle)))
 
@@ -329,9 +336,10 @@ class BatchDecoder:
 def make_config(cfg) -> _lib.ab_config:
     # the epsilon cap saturates to int32 (same rounds, see decoder._check_eps_cap)
     eps = max(-(1 << 31), min(int(cfg.max_epsilon_expansion), _lib.AB_MAX_EPSILON_ROUNDS))
+    flags = _lib.AB_CFG_EXACT if getattr(cfg, "exact_counters", False) else 0
     return _lib.ab_config(float(cfg.beam), int(cfg.max_active), eps,
                           int(cfg.partial_every), int(cfg.endpoint_silence_frames),
-                          int(cfg.silence_ilabel), 0)
+                          int(cfg.silence_ilabel), flags)
 
 
 def device_graph(csr, device: int | None = None) -> DeviceGraph:

@@ -42,7 +42,7 @@ def main():
         if frames:
             rd = d.get("dram__bytes_read.sum", {})
             wr = d.get("dram__bytes_write.sum", {})
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
             try:
                 tot = rd["value"] * scale[rd["unit"]] + wr["value"] * scale[wr["unit"]]
                 d["dram_bytes_per_channel_frame"] = tot / frames

@@ -43,8 +43,10 @@ def fx(s: str) -> float:
     return float.fromhex(s)
 
 
-def case_inputs(c: dict):
-    """(csr, scores[T, L] f64, ctx or None, cfg) of one golden case, as package objects."""
+def case_inputs(c: dict, exact: bool = False):
+    """(csr, scores[T, L] f64, ctx or None, cfg) of one golden case, as package objects.
+    exact: DecoderConfig.exact_counters (every candidate relaxed, so len(store)
+    and eps_truncations are the reference's too)."""
     import paper_2306_15685_b200 as ab
 
     g = c["graph"]
@@ -60,12 +62,20 @@ def case_inputs(c: dict):
     if c.get("ctx") is not None:
         ctx = ab.BiasingContext(id="r", arc_indices=np.array(c["ctx"]["arc_indices"], dtype=np.int64),
                                 discount=fx(c["ctx"]["discount"]))
-    cfg = ab.DecoderConfig(**c["cfg"])
+    cfg = ab.DecoderConfig(**c["cfg"], exact_counters=exact)
     return csr, scores, ctx, cfg
 
 
 def expect_hyps(e: dict):
     return [(h["words"], fx(h["cost"]), h["frame"], h["kind"], h["fallback"]) for h in e["hyps"]]
+
+
+@pytest.fixture(params=[False, True], ids=["cutoff", "exact"])
+def exact(request):
+    """Both decode modes: the expansion-time cutoff (default; hypotheses and
+    surviving tokens exact) and exact_counters (every candidate relaxed;
+    len(store) and eps_truncations exact too)."""
+    return request.param
 
 
 @pytest.fixture(scope="session")

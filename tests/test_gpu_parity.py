@@ -46,11 +46,11 @@ def _same(got, want, where=""):
         assert a.hits == b.hits, where
 
 
-def test_small_cases_match_reference(small_cases):
+def test_small_cases_match_reference(small_cases, exact):
     """400+ reference-generated instances: ties, epsilon cycles, negative
     weights, max_active binding, epsilon caps, endpointing, dead channels."""
     for c in small_cases:
-        csr, scores, ctx, cfg = case_inputs(c)
+        csr, scores, ctx, cfg = case_inputs(c, exact)
         res, ch = _decode(csr, scores, ctx, cfg)
         e = c["expect"]
         if e["error"] is not None:
@@ -61,14 +61,15 @@ def test_small_cases_match_reference(small_cases):
         got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
         assert got == expect_hyps(e), c["name"]
         assert ch.utterance_index == e["utterance_index"], c["name"]
-        assert ch.eps_truncations == e["eps_truncations"], c["name"]
-        assert len(ch.store) == e["store_len"], c["name"]
+        if exact:
+            assert ch.eps_truncations == e["eps_truncations"], c["name"]
+            assert len(ch.store) == e["store_len"], c["name"]
         hyps, rc, _ = _oracle(csr, scores, ctx, cfg)
         assert [h.hits for h in res.hypotheses] == [h.hits for h in hyps], c["name"]
 
 
 @pytest.mark.parametrize("variant", ["f32", "f64"])
-def test_c1_full_reference_run(variant):
+def test_c1_full_reference_run(variant, exact):
     """C1: G_small, 1 channel x 500 frames, 20-word context, beam 13 - the exact
     run the reference decoded (golden), f32-stored or f64-stored weights."""
     import paper_2306_15685_b200 as ab
@@ -77,7 +78,7 @@ def test_c1_full_reference_run(variant):
     g = load_json("c1_small.json")
     csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=(variant == "f32"))
     ctx = ab.BiasingContext("ctx1", np.array(g["ctx_arcs"], dtype=np.int64), -2.0)
-    cfg = ab.DecoderConfig(**g["cfg"])
+    cfg = ab.DecoderConfig(**g["cfg"], exact_counters=exact)
     scores = np.random.default_rng([7, 0]).uniform(0.0, 6.0, (500, 2000))
     if variant == "f32":
         scores = scores.astype(np.float32)
@@ -86,7 +87,8 @@ def test_c1_full_reference_run(variant):
     e = g["runs"][variant]
     got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
     assert got == expect_hyps(e)
-    assert len(ch.store) == e["store_len"]
+    if exact:
+        assert len(ch.store) == e["store_len"]
     hyps, rc, _ = _oracle(csr, scores, ctx, cfg)
     _same(res.hypotheses, hyps)
     dg = ab.device_graph(csr)
@@ -115,7 +117,7 @@ def test_c2_subset_partials_every_frame():
         _same(res[c].hypotheses, hyps, f"channel {c}")
 
 
-def test_per_frame_token_sets_match_oracle():
+def test_per_frame_token_sets_match_oracle(exact):
     """advance_frame one frame at a time: the surviving token set (states,
     costs, hits) equals the oracle's after every frame, with max_active binding."""
     import paper_2306_15685_b200 as ab
@@ -124,7 +126,7 @@ def test_per_frame_token_sets_match_oracle():
 
     csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
     ctx = synth.unigram_context(csr, 20, 3, num_labels=2000)
-    cfg = ab.DecoderConfig(beam=13.0, max_active=3000)
+    cfg = ab.DecoderConfig(beam=13.0, max_active=3000, exact_counters=exact)
     og = OracleGraph.from_csr(csr)
     och = OracleChannel(og)
     ch = ab.init_channel("t", None, None, cfg)
@@ -139,8 +141,9 @@ def test_per_frame_token_sets_match_oracle():
         assert [x.hits for x in toks] == hi.tolist(), t
         info = och.info()
         assert ch.trailing_silence == info["trailing_silence"]
-        assert ch.eps_truncations == info["eps_truncations"]
-        assert len(ch.store) == info["store_len"]
+        if exact:
+            assert ch.eps_truncations == info["eps_truncations"]
+            assert len(ch.store) == info["store_len"]
         if t % 7 == 3:
             p = ab.partial_hypothesis(ch)
             q = och.partial()
@@ -317,8 +320,8 @@ def test_hashed_token_table_matches_reference(small_cases, monkeypatch):
     from paper_2306_15685_b200 import device, synth
 
     n_hashed = 0
-    for c in small_cases[:200]:
-        csr, scores, ctx, cfg = case_inputs(c)
+    for i, c in enumerate(small_cases[:200]):
+        csr, scores, ctx, cfg = case_inputs(c, exact=bool(i % 2))
         if csr.num_states < 3:
             continue
         # fewer slots than states selects the hashed table (rounded up to a power of two)
@@ -332,7 +335,8 @@ def test_hashed_token_table_matches_reference(small_cases, monkeypatch):
         assert res.error is None, (c["name"], res.error)
         got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
         assert got == expect_hyps(e), c["name"]
-        assert len(ch.store) == e["store_len"], c["name"]
+        if cfg.exact_counters:
+            assert len(ch.store) == e["store_len"], c["name"]
     assert n_hashed > 100
     monkeypatch.setattr(device, "DEFAULT_CAPACITY", device.Capacity(table_slots=16384))
     csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
@@ -347,7 +351,7 @@ def test_hashed_token_table_matches_reference(small_cases, monkeypatch):
 
 
 @pytest.mark.parametrize("beam,max_active", [(float("inf"), 500), (0.25, 7000), (13.0, 1)])
-def test_extreme_beams_and_caps(beam, max_active):
+def test_extreme_beams_and_caps(beam, max_active, exact):
     """Infinite beam (max_active alone prunes), a beam narrower than the cost
     spread, and max_active = 1: the prune's cost-bucket split stays exact."""
     import paper_2306_15685_b200 as ab
@@ -355,14 +359,15 @@ def test_extreme_beams_and_caps(beam, max_active):
 
     csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
     ctx = synth.unigram_context(csr, 20, 9, num_labels=2000)
-    cfg = ab.DecoderConfig(beam=beam, max_active=max_active, partial_every=7)
+    cfg = ab.DecoderConfig(beam=beam, max_active=max_active, partial_every=7, exact_counters=exact)
     scores = synth.channel_scores(13, 0, 30, 2000)
     res, ch = _decode(csr, scores, ctx, cfg)
     assert res.error is None, res.error
     want, rc, info = _oracle(csr, scores, ctx, cfg)
     assert rc == 0
     _same(res.hypotheses, want, f"beam {beam} max_active {max_active}")
-    assert len(ch.store) == info["store_len"]
+    if exact:
+        assert len(ch.store) == info["store_len"]
 
 
 def test_full_size_launch_shapes_agree(monkeypatch):
@@ -450,3 +455,52 @@ def test_smem_token_table_matches_global(monkeypatch):
         want, rc, _ = _oracle(csr, utts[0][c].costs, pool[c], cfg)
         assert rc == 0
         assert [(h.words, h.cost, h.frame, h.kind, h.hits) for h in want] == ref[0][c]
+
+
+def test_cutoff_engages_and_changes_nothing_observable():
+    """The expansion-time cutoff (default mode) relaxes far fewer candidates
+    than exact_counters, yet every hypothesis, surviving token set and
+    trailing-silence count is the same; a margin of zero forces hint misses,
+    whose frames are redone unfiltered (still exact)."""
+    import dataclasses
+    import os
+
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctxs = {f"k{c}": synth.unigram_context(csr, 20, c, num_labels=2000, ctx_id=f"k{c}") for c in range(8)}
+    reg = ab.ContextRegistry(ctxs, graph_fingerprint="")
+    fast = ab.DecoderConfig(beam=13.0, max_active=2000, partial_every=3)
+    mats = [synth.channel_scores(23, c, 80, 2000) for c in range(8)]
+
+    def run(cfg):
+        chans = [ab.init_channel(f"x{c}", reg, f"k{c}", cfg) for c in range(8)]
+        res = ab.decode_batch([(ch, ab.ScoreMatrix(m)) for ch, m in zip(chans, mats)], csr, reg, cfg)
+        return res, chans
+
+    res_f, ch_f = run(fast)
+    res_x, ch_x = run(dataclasses.replace(fast, exact_counters=True))
+    for a, b in zip(res_f, res_x):
+        assert a.error is None and b.error is None
+        _same(a.hypotheses, b.hypotheses)
+    eps_f = sum(ch.work_counters[2] for ch in ch_f)
+    eps_x = sum(ch.work_counters[2] for ch in ch_x)
+    assert eps_f < 0.8 * eps_x, (eps_f, eps_x)
+    # forced hint misses: every filtered attempt fails verification and is redone
+    old = {k: os.environ.get(k) for k in ("AB_CUT_HINT_MIN", "AB_CUT_HINT_EXTRA")}
+    try:
+        os.environ["AB_CUT_HINT_MIN"] = "0"
+        os.environ["AB_CUT_HINT_EXTRA"] = "-3"
+        ab._lib.load().ab_reload_env()
+        res_m, ch_m = run(fast)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        ab._lib.load().ab_reload_env()
+    for a, b in zip(res_m, res_x):
+        _same(a.hypotheses, b.hypotheses)
+    assert sum(ch._page.get(ch._slot).cut_redos for ch in ch_m) > 0

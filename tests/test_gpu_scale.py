@@ -91,7 +91,7 @@ def _oracle_segments(og, jobs, cfg):
 
 
 @pytest.mark.parametrize("block", ["256", "default"])
-def test_g_large_reference_run(g_large, block, monkeypatch):
+def test_g_large_reference_run(g_large, block, exact, monkeypatch):
     """The reference decoder's own output on G_large (5 channels x 2
     context-switched 125-frame segments): hypotheses bit-exact, len(store),
     eps_truncations and utterance counters equal."""
@@ -104,7 +104,7 @@ def test_g_large_reference_run(g_large, block, monkeypatch):
     csr, pool = g_large
     assert _digest(csr) == g["digest"]
     reg = ab.ContextRegistry({c.id: c for c in pool}, graph_fingerprint="")
-    cfg = ab.DecoderConfig(**g["cfg"])
+    cfg = ab.DecoderConfig(**g["cfg"], exact_counters=exact)
     runs = g["c3"]
     chans = sorted({r["channel"] for r in runs})
     mats = {c: synth.channel_scores(7, c, 2 * SEG, L) for c in chans}
@@ -123,12 +123,13 @@ def test_g_large_reference_run(g_large, block, monkeypatch):
             want = [(h["words"], fx(h["cost"]), h["frame"], h["kind"], h["fallback"]) for h in r["hyps"]]
             assert _tuples(got.hypotheses) == want, where
             ch = dev[r["channel"]]
-            assert len(ch.store) == r["store_len"], where
-            assert ch.eps_truncations == r["eps_truncations"], where
+            if exact:
+                assert len(ch.store) == r["store_len"], where
+                assert ch.eps_truncations == r["eps_truncations"], where
             assert ch.utterance_index == r["utterance_index"], where
 
 
-def test_g_large_dense_contexts_reference_run(g_large):
+def test_g_large_dense_contexts_reference_run(g_large, exact):
     """C4's dense contexts on G_large against the reference: a 100-word
     context (5% of arcs, label-closed -> LABELS) and 5% of arcs drawn
     uniformly (not label-closed -> BITSET)."""
@@ -137,7 +138,7 @@ def test_g_large_dense_contexts_reference_run(g_large):
 
     g = load_json("g_large.json")
     csr, _ = g_large
-    cfg = ab.DecoderConfig(**g["cfg"])
+    cfg = ab.DecoderConfig(**g["cfg"], exact_counters=exact)
     ctxs = {"words100": synth.unigram_contexts(csr, 100, [2000], num_labels=L)[0],
             "arcs5pct": synth.dense_context(csr, 0.05, 2000)}
     modes = {"words100": _lib.AB_CTX_LABELS, "arcs5pct": _lib.AB_CTX_BITSET}
@@ -151,7 +152,8 @@ def test_g_large_dense_contexts_reference_run(g_large):
         assert res.error is None, res.error
         want = [(h["words"], fx(h["cost"]), h["frame"], h["kind"], h["fallback"]) for h in r["hyps"]]
         assert _tuples(res.hypotheses) == want, r["name"]
-        assert len(ch.store) == r["store_len"], r["name"]
+        if exact:
+            assert len(ch.store) == r["store_len"], r["name"]
         dg = ab.device_graph(csr)
         assert dg.context_mode(dg.context_handle(ctx)) == modes[r["name"]]
 
