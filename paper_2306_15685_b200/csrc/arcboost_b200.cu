@@ -1010,14 +1010,14 @@ static int ensure_batch(ab_decoder *d, size_t n) {
 // hint's minimum rise per frame and extra margin (decode_kernel.cuh advance()).
 struct Knobs {
   bool loaded = false;
-  double hint_min = 1.0, hint_extra = 0.5;
+  double hint_min = 1.0, hint_extra = 0.25;
 };
 static Knobs &g_knobs() {
   static Knobs k;
   if (!k.loaded) {
     const char *a = getenv("AB_CUT_HINT_MIN"), *b = getenv("AB_CUT_HINT_EXTRA");
     k.hint_min = a ? atof(a) : 1.0;
-    k.hint_extra = b ? atof(b) : 0.5;
+    k.hint_extra = b ? atof(b) : 0.25;
     k.loaded = true;
   }
   return k;

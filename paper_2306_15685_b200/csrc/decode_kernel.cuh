@@ -626,6 +626,7 @@ struct Shared {
   u32 emit_end; // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_hint; // this attempt's cutoff hint (inf: unfiltered), see advance()
+  double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
   int filtered;
 #ifdef AB_PROFILE
   unsigned long long prof[PF_N];
@@ -1557,7 +1558,11 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const double cut = split < bt ? fmin(thr, sh.hbase + ((double)split + 1.0001) / sh.hscale) : thr;
   const bool verified = !sh.filtered || cut <= sh.cut_hint;
   __syncthreads();
-  if (!verified) return false;
+  if (!verified) {
+    if (tid == 0) sh.cut_fail = cut;
+    __syncthreads();
+    return false;
+  }
   if (tid == 0) {
     if (sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
     const double prev = C.cs->prev_cut;
@@ -1915,18 +1920,22 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   // reference computes them.  U is a hint (the previous frame's cutoff plus
   // its recent rise), verified after the closure: the filtered frame's own
   // cutoff C*_f >= C* (its candidates are a subset), so C*_f <= U proves the
-  // frame exact; else the frame is redone unfiltered (prune returns false
-  // before it has written anything).  Emission records and epsilon-round
+  // frame exact; else the frame is redone (prune returns false before it has
+  // written anything) with U = C*_f of the failed attempt, which keeps a
+  // superset of its candidates and so verifies; a third attempt, should one
+  // be needed, is unfiltered.  Emission records and epsilon-round
   // truncations of dropped candidates are not counted (P.exact keeps every
   // candidate and the reference's len(store) / eps_truncations).
   const unsigned long long c_tok = sh.cnt_tok, c_emit = sh.cnt_emit, c_eps = sh.cnt_eps;
   const long long eps_tr = cs->info.eps_truncations;
   bool filt = !P.exact && cs->prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
               P.max_eps <= C.slack_rounds;
-  while (true) {
+  for (int attempt = 0;; ++attempt) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      const double hint = filt ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra : INFINITY;
+      const double hint = !filt ? INFINITY
+                          : attempt == 0 ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra
+                                         : sh.cut_fail;
       sh.cut_hint = hint;
       sh.filtered = filt ? 1 : 0;
       // (+ a margin for the f64 rounding of path sums)
@@ -1963,7 +1972,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       cs->info.eps_truncations = eps_tr;
       cs->info.cut_redos += 1;
     }
-    filt = false;
+    __syncthreads();
+    filt = filt && attempt == 0 && sh.cut_fail < INFINITY; // second attempt: hint = C*_f; third: none
   }
   if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
   __syncthreads();
