@@ -1251,9 +1251,10 @@ static void launch_smem_layout(ab_decoder *d, const int32_t *slots, int n, Decod
   P.neg_words = neg ? NEG_WORDS : 0u;
 }
 
-static size_t dyn_smem(int L, bool s64, const DecodeParams &P) {
+static size_t dyn_smem(int L, bool s64, DecodeParams &P) {
   size_t row = (size_t)L * (s64 ? 8 : 4);
-  row = row > (size_t)SCORE_SMEM_MAX_BYTES ? 0 : (row + 15) / 16 * 16;
+  P.row_in_smem = row <= (size_t)SCORE_SMEM_MAX_BYTES && !getenv("AB_ROW_GLOBAL");
+  row = P.row_in_smem ? (row + 15) / 16 * 16 : 0;
   return (size_t)P.ctx_words_cap * sizeof(u32) + row + (size_t)P.neg_words * sizeof(u32);
 }
 
@@ -1596,6 +1597,7 @@ static int one_hyp(ab_decoder *d, int32_t ch, int which, ab_hyp *hyp, int32_t *w
   CK(cudaMemcpyAsync(d->d_slots, &ch, sizeof(int), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d->d_wused, 0, sizeof(long long), st));
   P.ctx_words_cap = CTX_SMEM_WORDS;
+  P.row_in_smem = 1;
   const size_t smem = CTX_SMEM_WORDS * sizeof(u32);
   cudaError_t le = d->hashed ? (g->fmt16 ? launch_hyp<256, Fmt16<true>, float>(P, which, smem, st)
                                          : launch_hyp<256, Fmt24<true>, float>(P, which, smem, st))

@@ -313,6 +313,7 @@ struct DecodeParams {
   // dynamic shared memory layout (host: launch_smem_layout)
   u32 ctx_words_cap; // context words in shared memory (LABELS bitmap / LIST arcs)
   u32 neg_words;     // 0 or NEG_WORDS: the neg Bloom filter after the score row
+  int row_in_smem;   // the frame's score row is staged in shared memory (else read through L1)
   // config (decoder.py:33-48)
   double beam;
   int max_active, max_eps, partial_every, endpoint_silence_frames, silence_ilabel;
@@ -721,6 +722,22 @@ __device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 a, u32 bw, u
   }
 }
 
+// One candidate: cost in the reference's association order with the boost
+// fused into the weight (_effective_weights, decoder.py:234-240, 378 emitting,
+// 268 epsilon), its row flags, and whether it is relaxed at all: a candidate
+// above the frame's cutoff is provably outside the survivors (advance(); a
+// destination without epsilon arcs has no epsilon path, hence no slack).
+template <bool EMIT, typename F, typename S>
+__device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double w, u32 il, u32 ol, u32 g, u32 d,
+                                          u32 a, u32 bw, u64 &ck, u32 &rflags) {
+  const bool bst = is_boosted(C, a, bw, g & G_MASK, ol);
+  const double we = bst ? w + C.discount : w;
+  const double cand = EMIT ? (cj + we) + (double)C.row[il - 1] : cj + we;
+  ck = cost_key(cand);
+  rflags = (bst ? ROW_BOOST : 0u) | (ol ? ROW_HASOL : 0u) | ((g & G_DEST_EPS) ? ROW_EPS : 0u);
+  return cand <= C.ucut0 || (cand <= C.ucut && (g & G_DEST_EPS) && neg_test(C.neg, d));
+}
+
 __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.error, 0, code); }
 
 template <bool H> __device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
@@ -1110,18 +1127,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       for (int u = 0; u < U; ++u) {
         ck[u] = 0;
         rflags[u] = 0;
-        if (on[u]) {
-          // _effective_weights (decoder.py:234-240): boost fused into the cost add
-          const bool bst = is_boosted(C, a[u], bw[u], g[u] & G_MASK, ol[u]);
-          const double we = bst ? w[u] + C.discount : w[u];
-          double cand;
-          if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
-          else cand = cj[u] + we;                                    // decoder.py:268
-          ck[u] = cost_key(cand);
-          rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
-          // provably outside this frame's survivors (advance())
-          on[u] = cand <= C.ucut0 || (cand <= C.ucut && neg_test(C.neg, d[u]));
-        }
+        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
     }
@@ -1242,18 +1248,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       for (int u = 0; u < U; ++u) {
         ck[u] = 0;
         rflags[u] = 0;
-        if (on[u]) {
-          // _effective_weights (decoder.py:234-240): boost fused into the cost add
-          const bool bst = is_boosted(C, a[u], bw[u], g[u] & G_MASK, ol[u]);
-          const double we = bst ? w[u] + C.discount : w[u];
-          double cand;
-          if (EMIT) cand = (cj[u] + we) + (double)C.row[il[u] - 1]; // decoder.py:378
-          else cand = cj[u] + we;                                    // decoder.py:268
-          ck[u] = cost_key(cand);
-          rflags[u] = (bst ? ROW_BOOST : 0u) | (ol[u] ? ROW_HASOL : 0u) | ((g[u] & G_DEST_EPS) ? ROW_EPS : 0u);
-          // provably outside this frame's survivors (advance())
-          on[u] = cand <= C.ucut0 || (cand <= C.ucut && neg_test(C.neg, d[u]));
-        }
+        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
     }
@@ -2264,7 +2259,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   // channel's direct token table (host: launch_smem_layout, dyn_smem)
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
   S *sh_row = reinterpret_cast<S *>(dyn_smem + P.ctx_words_cap * sizeof(u32));
-  const bool row_in_smem = (size_t)P.L * sizeof(S) <= (size_t)SCORE_SMEM_MAX_BYTES;
+  const bool row_in_smem = P.row_in_smem != 0;
   u32 *sh_neg = reinterpret_cast<u32 *>(dyn_smem + P.ctx_words_cap * sizeof(u32) +
                                         (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
   uint4 *sh_table = reinterpret_cast<uint4 *>(sh_neg + P.neg_words);
