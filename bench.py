@@ -70,6 +70,9 @@ def parse():
     p.add_argument("--parity-channels", type=int, default=16,
                    help="channels whose every segment is checked against the oracle")
     p.add_argument("--density", type=float, default=0.05, help="c4: fraction of arcs boosted")
+    p.add_argument("--ctx-kind", choices=["words", "entities"], default="words",
+                   help="c3 context pool: 20 single-word entities (label-closed, LABELS) or 20 "
+                        "multi-word entities compiled by Alg. 1 (LIST / BITSET)")
     p.add_argument("--c4-kind", choices=["words", "arcs"], default="words",
                    help="c4 contexts: unigram word sets (density x L words) or uniform random arcs")
     return p.parse_args()
@@ -246,6 +249,9 @@ def build_inputs(W, seed_base: int, channel_base: int, want_contexts=True, dense
         elif dense is not None:
             pool = synth.unigram_contexts(csr, max(1, int(round(dense * L))), range(2000, 2008),
                                           num_labels=L)
+        elif kind == "entities":
+            n_pool = CTX_POOL if W["channels"] > 1 else 1
+            pool = synth.entity_contexts(csr, 20, range(1000, 1000 + n_pool))
         else:
             n_pool = CTX_POOL if W["channels"] > 1 else 1
             pool = synth.unigram_contexts(csr, 20, range(1000, 1000 + n_pool), num_labels=L)
@@ -329,7 +335,8 @@ def run_b200(args, W, world, rank, local):
     assert Tseg * S == T
     dense = args.density if args.workload == "c4" else None
     csr, pool, _, prep = build_inputs(W, seed_base=7, channel_base=rank * C, dense=dense,
-                                      kind=args.c4_kind, host_scores=False)
+                                      kind=args.c4_kind if dense is not None else args.ctx_kind,
+                                      host_scores=False)
     cfg = ab.DecoderConfig(beam=13.0, max_active=7000, max_epsilon_expansion=20,
                            partial_every=W["partial_every"])
     t0 = time.time()
@@ -461,6 +468,16 @@ def run_b200(args, W, world, rank, local):
                          "random_read_ceiling_Gsectors_s": pref.get("random_read_Gsectors_s"),
                          "random_cas_ceiling_Gops_s": pref.get("random_cas_Gops_s"),
                          "source": pref.get("ncu_source")}
+    modes = sorted({dg.context_mode(h) for h in handles})
+    mode_names = {_lib.AB_CTX_LIST: "LIST", _lib.AB_CTX_BITSET: "BITSET", _lib.AB_CTX_LABELS: "LABELS"}
+    arcs_per_ctx = float(np.mean([len(c.arc_indices) for c in pool])) if pool else 0.0
+    if dense is not None:
+        ctx_desc = (f"c4 {args.c4_kind} density {dense} ({arcs_per_ctx:.0f} arcs = "
+                    f"{100 * arcs_per_ctx / int(csr.row_offsets[-1]):.2f}% of arcs per context)")
+    else:
+        ctx_desc = (f"pool of {len(pool)} x 20 {'multi-word (Alg. 1)' if args.ctx_kind == 'entities' else 'single-word'}"
+                    f" entities, {arcs_per_ctx:.0f} arcs per context")
+    ctx_desc += f", discount -2.0, device modes {[mode_names.get(m, m) for m in modes]}"
     result = {
         "metric": METRIC,
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -469,7 +486,8 @@ def run_b200(args, W, world, rank, local):
         "data": "synthetic (benchmark_graph seed 421; scores U[0,6) default_rng([7, c]), generated in HBM bit-identically by ab_scores_generate)",
         "config": {"workload": f"{args.workload}: G {W['states']} states x 4 arcs, L={L}, "
                                f"{C} channels/GPU x {T} frames, {S} segments with context switch, "
-                               f"partial_every {W['partial_every']}, beam 13, max_active 7000",
+                               f"partial_every {W['partial_every']}, beam 13, max_active 7000, "
+                               f"contexts: {ctx_desc}",
                    "channels_per_gpu": C, "frames": T, "segments": S,
                    "parallelism": f"channels sharded, {world} GPU(s), no collective",
                    "l2": "inputs (4 GB scores + 0.36 GB graph) exceed L2"},

@@ -61,11 +61,15 @@ struct HostCtx {
   int abi_mode = AB_CTX_LIST;
   u32 words = 0;
   u32 *d_list = nullptr;
+  u32 *d_hash = nullptr; // CTX_SLIST: Bloom filter of the ids (words words)
   u32 *d_bits = nullptr;   // CTX_BITSET: emitting record positions; CTX_LABELS: olabel bitmap
   u32 *d_bits_x = nullptr; // CTX_BITSET: epsilon record positions
   double slack = 0.0;      // eps_slack of the context's weighting
   int slack_rounds = 0;
-  u32 *d_neg = nullptr;    // its neg bitmap (NEG_WORDS)
+  u32 *d_neg = nullptr;    // its neg Bloom filters (NEG_BLOCK_WORDS)
+  u32 neg_count = 0;       // states they flag
+  unsigned char *d_hq = nullptr; // or per-state slack bytes (dense contexts)
+  double hq_unit = 0.0;
 };
 
 struct ab_graph {
@@ -91,7 +95,8 @@ struct ab_graph {
   std::vector<double> h_buf; // eps_slack scratch, one value per state
   double slack0 = 0.0;       // slack of the unbiased graph
   int slack0_rounds = 0;
-  u32 *d_neg0 = nullptr;     // its neg bitmap (NEG_WORDS)
+  u32 *d_neg0 = nullptr;     // its neg Bloom filters (NEG_BLOCK_WORDS)
+  u32 neg0_count = 0;        // states they flag
   uint2 *e_rng = nullptr, *x_rng = nullptr; // per state {begin, end}: one 8-byte request
   unsigned char *deg = nullptr;              // per state arc counts (DecodeParams::deg)
   void *e_arcs = nullptr, *x_arcs = nullptr;
@@ -174,7 +179,8 @@ extern "C" int ab_device_count(int32_t *count) {
 // ------------------------------------------------------------------ graph
 
 static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
-                        std::vector<u32> *neg_bits, int *rounds_ok);
+                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<unsigned char> *hq = nullptr,
+                        double *hq_unit = nullptr, u32 *neg_count = nullptr);
 
 extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states,
                                int64_t num_arcs, const int64_t *row_offsets,
@@ -344,7 +350,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     for (size_t i = 0; i < g->xe_g.size(); ++i) g->xr_arc[fill[g->xe_dst[i]]++] = (u32)i;
   }
   std::vector<u32> neg0;
-  g->slack0 = eps_slack(g, {}, 0.0, &neg0, &g->slack0_rounds);
+  g->slack0 = eps_slack(g, {}, 0.0, &neg0, &g->slack0_rounds, nullptr, nullptr, &g->neg0_count);
   size_t acc = 0;
   unsigned char *de = nullptr, *dx = nullptr;
   std::vector<uint2> erng(num_states), xrng(num_states);
@@ -360,8 +366,8 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   }
   g->e_arcs = de;
   g->x_arcs = dx;
-  if (dmalloc(&g->d_neg0, NEG_WORDS, acc) ||
-      cudaMemcpy(g->d_neg0, neg0.data(), NEG_WORDS * sizeof(u32), cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (dmalloc(&g->d_neg0, NEG_BLOCK_WORDS, acc) ||
+      cudaMemcpy(g->d_neg0, neg0.data(), NEG_BLOCK_WORDS * sizeof(u32), cudaMemcpyHostToDevice) != cudaSuccess) {
     ab_graph_destroy(g);
     return fail(AB_ERR_CUDA, "device allocation for the graph failed");
   }
@@ -385,9 +391,11 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
   cudaSetDevice(g->device);
   for (auto &c : g->ctxs) {
     cudaFree(c.d_list);
+    cudaFree(c.d_hash);
     cudaFree(c.d_bits);
     cudaFree(c.d_bits_x);
     cudaFree(c.d_neg);
+    cudaFree(c.d_hq);
   }
   cudaFree(g->d_ctxs);
   cudaFree(g->e_rng);
@@ -424,10 +432,12 @@ extern "C" int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels,
 // <= 64 only), else INT_MAX.  neg_bits: Bloom filter of the states with
 // h < 0 (decode_kernel.cuh neg_test).  `boosted` = sorted arc ids.
 static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
-                        std::vector<u32> *neg_bits, int *rounds_ok) {
+                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<unsigned char> *hq,
+                        double *hq_unit, u32 *neg_count) {
   if (!boosted.empty() && discount >= 0.0 && g->xe_neg.size() == 0) {
     // boosting only raises weights: no negative epsilon arc anywhere
-    neg_bits->assign(NEG_WORDS, 0u);
+    neg_bits->assign(NEG_BLOCK_WORDS, 0u);
+    if (neg_count) *neg_count = 0;
     *rounds_ok = INT32_MAX;
     return 0.0;
   }
@@ -468,8 +478,18 @@ static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double dis
   }
   double lo = 0.0;
   neg_bits->assign(NEG_WORDS, 0u);
+  size_t n_neg = 0;
+  for (u32 s : touched) lo = std::min(lo, h[s]);
+  for (u32 s : touched) n_neg += h[s] < 0.0;
+  // too many states for the Bloom filter to stay sparse: per-state slack bytes
+  const bool dense = hq && n_neg > HQ_MIN_STATES;
+  if (dense) {
+    hq->assign((size_t)g->num_states, 0);
+    *hq_unit = -lo * (1.0 + 1e-9) / 255.0 + 1e-12;
+  }
   for (u32 s : touched) {
-    lo = std::min(lo, h[s]);
+    if (dense && h[s] < 0.0) // rounded up: a conservative per-state slack
+      (*hq)[s] = (unsigned char)std::min(255.0, std::ceil(-h[s] * (1.0 + 1e-9) / *hq_unit + 1e-9));
     if (h[s] < 0.0) {
       (*neg_bits)[neg_h1(s) >> 5] |= 1u << (neg_h1(s) & 31);
       (*neg_bits)[neg_h2(s) >> 5] |= 1u << (neg_h2(s) & 31);
@@ -477,6 +497,15 @@ static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double dis
     h[s] = 0.0;
   }
   *rounds_ok = front.empty() ? INT32_MAX : 64;
+  // every folded size after the full filter (decode_kernel.cuh NEG_MIN_WORDS)
+  neg_bits->resize(NEG_BLOCK_WORDS, 0u);
+  for (u32 W = NEG_WORDS / 2, at = NEG_WORDS, prev = 0; W >= NEG_MIN_WORDS; prev = at, at += W, W /= 2)
+    for (u32 j = 0; j < 32 * W; ++j) {
+      const u32 b0 = 2 * j, b1 = 2 * j + 1;
+      const u32 *p = neg_bits->data() + prev;
+      if (((p[b0 >> 5] >> (b0 & 31)) | (p[b1 >> 5] >> (b1 & 31))) & 1u) (*neg_bits)[at + (j >> 5)] |= 1u << (j & 31);
+    }
+  if (neg_count) *neg_count = (u32)n_neg;
   // margin for the f64 rounding of path sums (the kernel adds its own for the hint)
   return lo < 0.0 ? -lo * (1.0 + 1e-9) + 1e-9 : 0.0;
 }
@@ -491,11 +520,14 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].words = c.words;
     h[i].pad = 0;
     h[i].list = c.d_list;
+    h[i].hash = c.d_hash;
     h[i].bits = c.d_bits;
     h[i].bits_x = c.d_bits_x;
     h[i].slack = c.slack;
     h[i].slack_rounds = c.slack_rounds;
     h[i].neg = c.d_neg;
+    h[i].hq = c.d_hq;
+    h[i].hq_unit = c.hq_unit;
   }
   if (h.size() > g->d_ctxs_cap) {
     cudaFree(g->d_ctxs);
@@ -545,19 +577,37 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
     }
   }
   if (mode == AB_CTX_AUTO)
-    mode = closed ? AB_CTX_LABELS : (c.k <= (u32)CTX_SMEM_WORDS ? AB_CTX_LIST : AB_CTX_BITSET);
+    mode = closed ? AB_CTX_LABELS : (c.k <= LIST_SMEM_MAX ? AB_CTX_LIST : AB_CTX_BITSET);
   if (mode == AB_CTX_LABELS && !closed)
     return fail(AB_ERR_INVALID, "context is not label-closed: AB_CTX_LABELS would change it");
   if (mode != AB_CTX_LIST && mode != AB_CTX_BITSET && mode != AB_CTX_LABELS)
     return fail(AB_ERR_INVALID, "bad context mode %d", mode);
   c.abi_mode = mode;
   std::vector<u32> negb;
-  c.slack = eps_slack(g, list, discount, &negb, &c.slack_rounds);
-  CK(cudaMalloc(&c.d_neg, NEG_WORDS * sizeof(u32)));
-  CK(cudaMemcpy(c.d_neg, negb.data(), NEG_WORDS * sizeof(u32), cudaMemcpyHostToDevice));
+  std::vector<unsigned char> hq;
+  c.slack = eps_slack(g, list, discount, &negb, &c.slack_rounds, &hq, &c.hq_unit, &c.neg_count);
+  if (!hq.empty()) {
+    CK(cudaMalloc(&c.d_hq, hq.size()));
+    CK(cudaMemcpy(c.d_hq, hq.data(), hq.size(), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&c.d_neg, NEG_BLOCK_WORDS * sizeof(u32)));
+  CK(cudaMemcpy(c.d_neg, negb.data(), NEG_BLOCK_WORDS * sizeof(u32), cudaMemcpyHostToDevice));
   c.mode = mode == AB_CTX_LABELS ? CTX_LABELS : mode == AB_CTX_BITSET ? CTX_BITSET : CTX_SLIST;
   CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
   if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
+  if (mode == AB_CTX_LIST && c.k <= LIST_SMEM_MAX) { // shared-memory Bloom filter (else global search only)
+    u32 words = 64;
+    while (words < c.k) words <<= 1; // 32 bits per arc
+    std::vector<u32> bloom(words, 0u);
+    for (u32 a : list) {
+      const u32 b1 = list_b1(a, 32 * words), b2 = list_b2(a, 32 * words);
+      bloom[b1 >> 5] |= 1u << (b1 & 31);
+      bloom[b2 >> 5] |= 1u << (b2 & 31);
+    }
+    c.words = words;
+    CK(cudaMalloc(&c.d_hash, words * sizeof(u32)));
+    CK(cudaMemcpy(c.d_hash, bloom.data(), words * sizeof(u32), cudaMemcpyHostToDevice));
+  }
   if (mode == AB_CTX_BITSET) {
     // one bit per record position of each arc array (biasing.py:108-117 by
     // position instead of arc id: the same set, addressed without the record)
@@ -629,9 +679,11 @@ extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
   CK(cudaSetDevice(g->device));
   HostCtx &c = g->ctxs[handle];
   cudaFree(c.d_list);
+  cudaFree(c.d_hash);
   cudaFree(c.d_bits);
   cudaFree(c.d_bits_x);
   cudaFree(c.d_neg);
+  cudaFree(c.d_hq);
   c = HostCtx();
   return sync_ctx_table(g);
 }
@@ -1235,20 +1287,23 @@ static void launch_smem_layout(ab_decoder *d, const int32_t *slots, int n, Decod
   const ab_graph *g = d->g;
   u32 words = 0;
   bool neg = false;
+  u32 flagged = 0;
   for (int i = 0; i < n; ++i) {
     const int h = d->slot_ctx[slots[i]];
     const bool live = h >= 0 && h < (int)g->ctxs.size() && g->ctxs[h].live && g->ctxs[h].k;
     if (!live) {
-      neg |= g->slack0 > 0.0;
+      if (g->slack0 > 0.0) neg = true, flagged = std::max(flagged, g->neg0_count);
       continue;
     }
     const HostCtx &c = g->ctxs[h];
     if (c.mode == CTX_LABELS) words = std::max(words, c.words);
-    else if (c.mode == CTX_SLIST && c.k <= (u32)CTX_SMEM_WORDS) words = std::max(words, c.k);
-    neg |= c.slack > 0.0;
+    else if (c.mode == CTX_SLIST && c.words) words = std::max(words, c.words); // its Bloom filter
+    if (c.slack > 0.0 && !c.d_hq) neg = true, flagged = std::max(flagged, c.neg_count);
   }
   P.ctx_words_cap = (words + 3) & ~3u; // keeps the score row 16-byte aligned
-  P.neg_words = neg ? NEG_WORDS : 0u;
+  u32 W = NEG_MIN_WORDS; // ~8 filter bits per flagged state
+  while (W < NEG_WORDS && 32ull * W < 8ull * flagged) W *= 2;
+  P.neg_words = neg ? W : 0u;
 }
 
 static size_t dyn_smem(int L, bool s64, DecodeParams &P) {

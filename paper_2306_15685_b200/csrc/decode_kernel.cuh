@@ -72,7 +72,7 @@ __device__ __forceinline__ u32 aux_src(u32 src, u32 rflags, u32 g) {
   return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u) |
          (g == G_START ? AUX_START : 0u);
 }
-constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (8 KB)
+constexpr int CTX_SMEM_WORDS = 4096;        // sparse contexts / label bitmaps (16 KB, sized per launch)
 // Bloom filter (two hashes, 128 Kbit = 16 KB) of the states from which an
 // epsilon path lowers a cost: the only states the cutoff's slack applies to
 // (advance()).  False positives only keep a few more candidates.
@@ -80,11 +80,19 @@ constexpr int CTX_SMEM_WORDS = 2048;        // sparse contexts / label bitmaps (
 #define AB_NEG_WORDS 4096
 #endif
 constexpr u32 NEG_WORDS = AB_NEG_WORDS;
+constexpr size_t HQ_MIN_STATES = 24 * 1024; // more such states: per-state slack bytes instead
 constexpr int NEG_SHIFT = 32 - 5 - __builtin_ctz(NEG_WORDS); // hashes of log2(32 * NEG_WORDS) bits
+// A context stores the filter at NEG_WORDS and folded to every smaller power
+// of two down to NEG_MIN_WORDS (bit j of the half-size filter = OR of bits 2j,
+// 2j+1: the hashes are top bits, one shift more per halving); a launch copies
+// the smallest one that keeps ~8 bits per flagged state (the rest of shared
+// memory stays L1).  The size-W filter is at word 2 NEG_WORDS - 2 W.
+constexpr u32 NEG_MIN_WORDS = 256;
+constexpr u32 NEG_BLOCK_WORDS = 2 * NEG_WORDS - NEG_MIN_WORDS;
 __host__ __device__ __forceinline__ u32 neg_h1(u32 s) { return (s * 2654435761u) >> NEG_SHIFT; }
 __host__ __device__ __forceinline__ u32 neg_h2(u32 s) { return ((s ^ (s >> 16)) * 0x85EBCA6Bu) >> NEG_SHIFT; }
-__device__ __forceinline__ bool neg_test(const u32 *b, u32 s) {
-  const u32 a = neg_h1(s), c = neg_h2(s);
+__device__ __forceinline__ bool neg_test(const u32 *b, u32 s, u32 fold) {
+  const u32 a = neg_h1(s) >> fold, c = neg_h2(s) >> fold;
   return ((b[a >> 5] >> (a & 31)) & (b[c >> 5] >> (c & 31)) & 1u) != 0;
 }
 constexpr int SCORE_SMEM_MAX_BYTES = 32768; // larger score rows are read from L2
@@ -130,6 +138,14 @@ constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table r
 constexpr int PRUNE_Q = AB_PRUNE_Q; // rows per thread in flight (prune)
 
 enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
+// LIST contexts of up to LIST_SMEM_MAX arcs: a two-hash Bloom filter of their
+// ids in shared memory (32 bits per arc, rounded up to a power of two: false
+// positives ~0.2%, so a warp rarely has a lane that goes further), the sorted
+// ids in global memory (through L1) searched for the filter's hits.  Shared
+// memory not taken stays L1 (the kernel is sensitive to it).
+constexpr u32 LIST_SMEM_MAX = 2048;
+__host__ __device__ __forceinline__ u32 list_b1(u32 g, u32 nbits) { return ((g * 2654435761u) >> 7) & (nbits - 1u); }
+__host__ __device__ __forceinline__ u32 list_b2(u32 g, u32 nbits) { return ((g * 0x85EBCA6Bu) >> 9) & (nbits - 1u); }
 
 // Token provenance carried with every token (decoder.py:58-62 + last_il 138).
 struct __align__(16) TokInfo {
@@ -162,12 +178,17 @@ struct CtxDesc {
   u32 words; // CTX_LABELS: bitmap words
   u32 pad;
   const u32 *list; // sorted arc ids
+  const u32 *hash; // CTX_SLIST: Bloom filter of the ids (words words)
   const u32 *bits;   // CTX_BITSET: bit per emitting record position, CTX_LABELS: olabel bitmap
   const u32 *bits_x; // CTX_BITSET: bit per epsilon record position
   double slack;      // -min over states of the cheapest epsilon path from them (>= 0)
   int slack_rounds;  // slack bounds paths of at most this many epsilon arcs (INT_MAX: any)
   int pad2;
-  const u32 *neg;    // NEG_WORDS Bloom filter of the states where that path is negative
+  const u32 *neg;    // NEG_BLOCK_WORDS: Bloom filters of the states where that path is negative
+  // contexts with too many such states for the filter: per-state slack
+  // ceil(-h(s) / hq_unit) in one byte (0 = none), read for band candidates only
+  const unsigned char *hq;
+  double hq_unit;
 };
 
 // Arc record formats.  Fmt16: f32 weight, 16-bit labels (one 16 B load).
@@ -312,7 +333,7 @@ struct DecodeParams {
   const u32 *neg0; // NEG_WORDS bitmap of the unbiased graph
   // dynamic shared memory layout (host: launch_smem_layout)
   u32 ctx_words_cap; // context words in shared memory (LABELS bitmap / LIST arcs)
-  u32 neg_words;     // 0 or NEG_WORDS: the neg Bloom filter after the score row
+  u32 neg_words;     // 0 or the neg Bloom filter's words (a power of two <= NEG_WORDS) after the score row
   int row_in_smem;   // the frame's score row is staged in shared memory (else read through L1)
   // config (decoder.py:33-48)
   double beam;
@@ -426,6 +447,26 @@ __device__ __forceinline__ u32 ld_deg(const unsigned char *p, u64 pol) {
 // L2 prefetch: memory-level parallelism that costs no registers
 __device__ __forceinline__ void prefetch_l2(const void *p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Bulk asynchronous copy global -> shared (the TMA engine's non-tensor mode,
+// SASS UBLKCP) completing on an mbarrier: the next frame's score row lands in
+// shared memory while the current frame finishes, with no thread involved.
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64 *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_row_load(void *dst, const void *src, u32 bytes, u64 *bar) {
+  // the buffer's previous contents were read through the generic proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, u32 phase) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
 template <int BLOCK> __device__ __forceinline__ u32 block_excl_scan(u32 v, u32 &total, u32 *sh) {
@@ -629,6 +670,12 @@ struct Shared {
   double cut_hint; // this attempt's cutoff hint (inf: unfiltered), see advance()
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
   int filtered;
+  // next frame's score row, bulk-copied into the row buffer once the current
+  // frame's emitting pass is final (prune verified it; see decode_kernel)
+  const void *next_row;
+  u64 row_bar;
+  u32 row_phase;
+  int row_pending;
 #ifdef AB_PROFILE
   unsigned long long prof[PF_N];
   long long prof_t;
@@ -676,6 +723,9 @@ template <typename F, typename S> struct Chan {
   double ucut0; // this attempt's candidate cutoff (candidates above it are not relaxed) ...
   double ucut;  // ... plus the slack, for states in the neg bitmap
   const u32 *neg; // shared-memory copy of the context's (or graph's) neg bitmap
+  u32 neg_fold; // log2(NEG_WORDS / the launch's filter words)
+  const unsigned char *hq; // or the context's per-state slack bytes (CtxDesc::hq)
+  double hq_unit;
   // expansion tile (shared memory)
   u32 *t_a0;
   u32 *t_pref;
@@ -707,8 +757,12 @@ __device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 a, u32 bw, u
   case CTX_NONE: return false;
   case CTX_LABELS: return ol < C.ctx_words * 32u && ((C.ctx_bits[ol >> 5] >> (ol & 31)) & 1u);
   case CTX_BITSET: return (bw >> (a & 31)) & 1u;
+  case CTX_SLIST: { // Bloom filter (shared), then the sorted ids (global) for its few hits
+    const u32 nb = C.ctx_words * 32u, b1 = list_b1(g, nb), b2 = list_b2(g, nb);
+    if (!((C.ctx_bits[b1 >> 5] >> (b1 & 31)) & (C.ctx_bits[b2 >> 5] >> (b2 & 31)) & 1u)) return false;
+  } // fall through
   default: {
-    const u32 *a = C.ctx_list;
+    const u32 *a = C.ctx_list; // CTX_GLIST: binary search of the sorted ids in global memory
     u32 lo = 0, hi = C.ctx_k;
     while (lo < hi) {
       u32 mid = (lo + hi) >> 1;
@@ -735,7 +789,13 @@ __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double
   const double cand = EMIT ? (cj + we) + (double)C.row[il - 1] : cj + we;
   ck = cost_key(cand);
   rflags = (bst ? ROW_BOOST : 0u) | (ol ? ROW_HASOL : 0u) | ((g & G_DEST_EPS) ? ROW_EPS : 0u);
-  return cand <= C.ucut0 || (cand <= C.ucut && (g & G_DEST_EPS) && neg_test(C.neg, d));
+  if (cand <= C.ucut0) return true;
+  if (!(cand <= C.ucut) || !(g & G_DEST_EPS)) return false;
+  if (C.hq) {
+    const u32 q = __ldg(C.hq + d);
+    return q && cand <= C.ucut0 + (double)q * C.hq_unit;
+  }
+  return neg_test(C.neg, d, C.neg_fold);
 }
 
 __device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.error, 0, code); }
@@ -1559,6 +1619,10 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     return false;
   }
   if (tid == 0) {
+    if (sh.next_row) { // the score row is read by the emitting pass only, which is now final
+      bulk_row_load(const_cast<S *>(C.row), sh.next_row, (u32)(P.L * sizeof(S)), &sh.row_bar);
+      sh.row_pending = 1;
+    }
     if (sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
     const double prev = C.cs->prev_cut;
     const double rise = prev < INFINITY ? cut - prev : 0.0;
@@ -2188,6 +2252,9 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.ctx_bits_x = nullptr;
     C.slack = P.slack0;
     C.slack_rounds = P.slack0_rounds;
+    C.hq = nullptr;
+    C.hq_unit = 0.0;
+    C.neg_fold = 0;
     C.ucut0 = C.ucut = INFINITY;
     C.neg = sh_neg;
     C.t_a0 = t_a0;
@@ -2206,8 +2273,8 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
       mode = CTX_LABELS;
     } else if (d.mode == CTX_BITSET) {
       mode = CTX_BITSET;
-    } else if (d.k <= P.ctx_words_cap) {
-      for (u32 i = threadIdx.x; i < d.k; i += BLOCK) sh_ctx[i] = d.list[i];
+    } else if (d.mode == CTX_SLIST && d.words && d.words <= P.ctx_words_cap) {
+      for (u32 i = threadIdx.x; i < d.words; i += BLOCK) sh_ctx[i] = d.hash[i]; // the Bloom filter
       mode = CTX_SLIST;
     } else {
       mode = CTX_GLIST;
@@ -2217,21 +2284,26 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
       C.ctx_k = d.k;
       C.ctx_mode = mode;
       C.ctx_words = d.words;
-      C.ctx_bits = mode == CTX_LABELS ? sh_ctx : d.bits;
+      C.ctx_bits = (mode == CTX_LABELS || mode == CTX_SLIST) ? sh_ctx : d.bits;
       C.ctx_bits_x = d.bits_x;
       if (mode != CTX_NONE) {
         C.slack = d.slack;
         C.slack_rounds = d.slack_rounds;
+        C.hq = d.hq;
+        C.hq_unit = d.hq_unit;
       }
-      C.ctx_list = mode == CTX_SLIST ? sh_ctx : d.list;
+      C.ctx_list = d.list;
     }
   }
   __syncthreads();
-  if (C.slack > 0.0) { // the neg Bloom filter of the weighting in use
+  if (C.slack > 0.0 && !C.hq) { // the neg Bloom filter of the weighting in use
     const u32 *src = P.neg0;
     if (h >= 0 && h < P.num_ctxs && P.ctxs[h].k) src = P.ctxs[h].neg;
     if (sh_neg && src) {
-      for (u32 i = threadIdx.x; i < NEG_WORDS; i += BLOCK) sh_neg[i] = src[i];
+      const u32 W = P.neg_words;
+      src += 2 * NEG_WORDS - 2 * W;
+      for (u32 i = threadIdx.x; i < W; i += BLOCK) sh_neg[i] = src[i];
+      if (threadIdx.x == 0) C.neg_fold = (u32)(__ffs(NEG_WORDS) - __ffs(W));
     } else if (threadIdx.x == 0) {
       C.slack = INFINITY; // no filter in this launch's layout: no cutoff for this channel
     }
@@ -2263,6 +2335,12 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   u32 *sh_neg = reinterpret_cast<u32 *>(dyn_smem + P.ctx_words_cap * sizeof(u32) +
                                         (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
   uint4 *sh_table = reinterpret_cast<uint4 *>(sh_neg + P.neg_words);
+  if (threadIdx.x == 0) {
+    mbar_init(&sh.row_bar);
+    sh.row_phase = 0;
+    sh.row_pending = 0;
+    sh.next_row = nullptr;
+  }
   for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
     setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src,
                          P.neg_words ? sh_neg : nullptr);
@@ -2307,9 +2385,24 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       }
       const S *grow = scores + (size_t)t * P.L;
       if (row_in_smem) {
-        for (int i = threadIdx.x; i < P.L; i += BLOCK) sh_row[i] = grow[i];
+        if (sh.row_pending) { // bulk-copied during the previous frame
+          mbar_wait(&sh.row_bar, sh.row_phase);
+        } else {
+          for (int i = threadIdx.x; i < P.L; i += BLOCK) sh_row[i] = grow[i];
+        }
       } else if (threadIdx.x == 0) {
         C.row = grow;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (sh.row_pending) {
+          sh.row_pending = 0;
+          sh.row_phase ^= 1u;
+        }
+        // the next row goes by bulk copy when it is 16-byte sized and aligned
+        const S *nrow = grow + P.L;
+        sh.next_row = (row_in_smem && t + 1 < T && ((P.L * sizeof(S)) & 15) == 0 &&
+                       (reinterpret_cast<size_t>(nrow) & 15) == 0) ? nrow : nullptr;
       }
       __syncthreads();
       PROF_MARK(sh, PF_ROW);
@@ -2331,6 +2424,15 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       __syncthreads();
       PROF_MARK(sh, PF_HYP);
     }
+    if (sh.row_pending) { // a prefetched row nobody will read: let it land before the buffer is reused
+      mbar_wait(&sh.row_bar, sh.row_phase);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        sh.row_pending = 0;
+        sh.row_phase ^= 1u;
+      }
+    }
+    __syncthreads();
     const bool done = t == T;
     if (P.mode == AB_MODE_STREAM && !sh.error && done && P.final_chunk) {
       // decoder.py:498-501: final hypothesis if frames were consumed or the stream is empty

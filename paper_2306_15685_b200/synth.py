@@ -144,6 +144,45 @@ def dense_context(csr, fraction: float, ctx_seed: int, *, discount: float = -2.0
     return BiasingContext(id=ctx_id or f"dense{ctx_seed}", arc_indices=idx, discount=discount)
 
 
+def graph_entities(csr, n: int, seed: int, *, min_words: int = 2, max_words: int = 3) -> list:
+    """n multi-word entities that occur in the graph: random arc walks that
+    output a word at every step (so Alg. 1 has chains to follow and boosts
+    more than the first word's arcs, biasing.py:203-233)."""
+    rng = random.Random(seed)
+    ro, ol, ns = np.asarray(csr.row_offsets), np.asarray(csr.olabels), np.asarray(csr.next_states)
+    out = []
+    while len(out) < n:
+        g = rng.randrange(len(ol))
+        words = []
+        for _ in range(rng.randint(min_words, max_words)):
+            if ol[g] == 0:
+                break
+            words.append(int(ol[g]))
+            s = int(ns[g])
+            if ro[s + 1] == ro[s]:
+                break
+            g = rng.randrange(int(ro[s]), int(ro[s + 1]))
+        if len(words) >= min_words:
+            out.append(words)
+    return out
+
+
+def entity_contexts(csr, per_context: int, ctx_seeds, *, discount: float = -2.0,
+                    depth: int = 10) -> list:
+    """Contexts of multi-word entities compiled by the native Alg. 1
+    (compiler._compile, all host threads): the C3 contexts of an ATC-style
+    deployment (callsigns), not label-closed, so LIST or BITSET on the device."""
+    from . import compiler as K
+
+    arrays = K.csr_arrays(csr)
+    out = []
+    for s in ctx_seeds:
+        arcs, _ = K._compile(arrays, graph_entities(csr, per_context, s), depth)
+        out.append(BiasingContext(id=f"ent{s}", arc_indices=np.asarray(arcs, dtype=np.int64),
+                                  discount=discount))
+    return out
+
+
 def pcg64_streams(seeds) -> np.ndarray:
     """[n, 4] uint64 {state hi, state lo, inc hi, inc lo} of
     ``np.random.default_rng(seed)`` for each seed (numpy's PCG64 state)."""

@@ -153,9 +153,10 @@ def test_per_frame_token_sets_match_oracle(exact):
     assert f.words == q.words and f.cost == q.cost and f.fallback == q.fallback
 
 
-@pytest.mark.parametrize("mode", ["list", "bitset", "labels", "auto"])
+@pytest.mark.parametrize("mode", ["list", "list_global", "bitset", "labels", "auto"])
 def test_context_representations_agree(mode):
-    """Sparse contexts (shared-memory sorted list) and dense ones (HBM bitset)
+    """Sparse contexts (shared-memory hash set; a LIST too large for it is
+    searched in global memory) and dense ones (HBM bitset by record position)
     give identical decodes; a 5%-dense context is checked against the oracle."""
     import paper_2306_15685_b200 as ab
     from paper_2306_15685_b200 import _lib, synth
@@ -163,11 +164,13 @@ def test_context_representations_agree(mode):
 
     csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
     ctx = synth.dense_context(csr, 0.05, 9) if mode == "bitset" else \
-        synth.unigram_context(csr, 20, 9, num_labels=2000)
+        synth.unigram_context(csr, 80 if mode == "list_global" else 20, 9, num_labels=2000)
+    if mode == "list_global":
+        assert 1365 < len(ctx.arc_indices) <= 2048
     cfg = ab.DecoderConfig(beam=13.0, max_active=7000, partial_every=10)
     scores = synth.channel_scores(3, 1, 60, 2000)
     dg = DeviceGraph(csr)
-    want_mode = {"list": _lib.AB_CTX_LIST, "bitset": _lib.AB_CTX_BITSET,
+    want_mode = {"list": _lib.AB_CTX_LIST, "list_global": _lib.AB_CTX_LIST, "bitset": _lib.AB_CTX_BITSET,
                  "labels": _lib.AB_CTX_LABELS, "auto": _lib.AB_CTX_AUTO}[mode]
     h = dg.register_context(ctx.arc_indices, ctx.discount, want_mode)
     # a unigram context is label-closed: AUTO picks the shared-memory label bitmap
