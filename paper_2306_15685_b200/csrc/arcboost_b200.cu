@@ -68,7 +68,7 @@ struct HostCtx {
   int slack_rounds = 0;
   u32 *d_neg = nullptr;    // its neg Bloom filters (NEG_BLOCK_WORDS)
   u32 neg_count = 0;       // states they flag
-  unsigned char *d_hq = nullptr; // or per-state slack bytes (dense contexts)
+  u32 *d_hq = nullptr;     // or 2-bit per-state slack (dense contexts)
   double hq_unit = 0.0;
 };
 
@@ -179,7 +179,7 @@ extern "C" int ab_device_count(int32_t *count) {
 // ------------------------------------------------------------------ graph
 
 static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
-                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<unsigned char> *hq = nullptr,
+                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<u32> *hq = nullptr,
                         double *hq_unit = nullptr, u32 *neg_count = nullptr);
 
 extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states,
@@ -432,7 +432,7 @@ extern "C" int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels,
 // <= 64 only), else INT_MAX.  neg_bits: Bloom filter of the states with
 // h < 0 (decode_kernel.cuh neg_test).  `boosted` = sorted arc ids.
 static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double discount,
-                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<unsigned char> *hq,
+                        std::vector<u32> *neg_bits, int *rounds_ok, std::vector<u32> *hq,
                         double *hq_unit, u32 *neg_count) {
   if (!boosted.empty() && discount >= 0.0 && g->xe_neg.size() == 0) {
     // boosting only raises weights: no negative epsilon arc anywhere
@@ -481,15 +481,17 @@ static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double dis
   size_t n_neg = 0;
   for (u32 s : touched) lo = std::min(lo, h[s]);
   for (u32 s : touched) n_neg += h[s] < 0.0;
-  // too many states for the Bloom filter to stay sparse: per-state slack bytes
+  // too many states for the Bloom filter to stay sparse: 2-bit per-state slack
   const bool dense = hq && n_neg > HQ_MIN_STATES;
   if (dense) {
-    hq->assign((size_t)g->num_states, 0);
-    *hq_unit = -lo * (1.0 + 1e-9) / 255.0 + 1e-12;
+    hq->assign(((size_t)g->num_states + 15) / 16, 0u);
+    *hq_unit = -lo * (1.0 + 1e-9) / 3.0 + 1e-12;
   }
   for (u32 s : touched) {
-    if (dense && h[s] < 0.0) // rounded up: a conservative per-state slack
-      (*hq)[s] = (unsigned char)std::min(255.0, std::ceil(-h[s] * (1.0 + 1e-9) / *hq_unit + 1e-9));
+    if (dense && h[s] < 0.0) { // rounded up: a conservative per-state slack
+      const u32 q = (u32)std::min(3.0, std::ceil(-h[s] * (1.0 + 1e-9) / *hq_unit + 1e-9));
+      (*hq)[s >> 4] |= std::max(q, 1u) << ((s & 15) * 2);
+    }
     if (h[s] < 0.0) {
       (*neg_bits)[neg_h1(s) >> 5] |= 1u << (neg_h1(s) & 31);
       (*neg_bits)[neg_h2(s) >> 5] |= 1u << (neg_h2(s) & 31);
@@ -584,11 +586,11 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
     return fail(AB_ERR_INVALID, "bad context mode %d", mode);
   c.abi_mode = mode;
   std::vector<u32> negb;
-  std::vector<unsigned char> hq;
+  std::vector<u32> hq;
   c.slack = eps_slack(g, list, discount, &negb, &c.slack_rounds, &hq, &c.hq_unit, &c.neg_count);
   if (!hq.empty()) {
-    CK(cudaMalloc(&c.d_hq, hq.size()));
-    CK(cudaMemcpy(c.d_hq, hq.data(), hq.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c.d_hq, hq.size() * sizeof(u32)));
+    CK(cudaMemcpy(c.d_hq, hq.data(), hq.size() * sizeof(u32), cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&c.d_neg, NEG_BLOCK_WORDS * sizeof(u32)));
   CK(cudaMemcpy(c.d_neg, negb.data(), NEG_BLOCK_WORDS * sizeof(u32), cudaMemcpyHostToDevice));

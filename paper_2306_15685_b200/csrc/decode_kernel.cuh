@@ -186,8 +186,9 @@ struct CtxDesc {
   int pad2;
   const u32 *neg;    // NEG_BLOCK_WORDS: Bloom filters of the states where that path is negative
   // contexts with too many such states for the filter: per-state slack
-  // ceil(-h(s) / hq_unit) in one byte (0 = none), read for band candidates only
-  const unsigned char *hq;
+  // ceil(-h(s) / hq_unit) in 2 bits (0 = none, 16 states per word: 1.25 MB
+  // for 5M states, L2-resident), read for band candidates only
+  const u32 *hq;
   double hq_unit;
 };
 
@@ -724,7 +725,7 @@ template <typename F, typename S> struct Chan {
   double ucut;  // ... plus the slack, for states in the neg bitmap
   const u32 *neg; // shared-memory copy of the context's (or graph's) neg bitmap
   u32 neg_fold; // log2(NEG_WORDS / the launch's filter words)
-  const unsigned char *hq; // or the context's per-state slack bytes (CtxDesc::hq)
+  const u32 *hq; // or the context's per-state 2-bit slack (CtxDesc::hq)
   double hq_unit;
   // expansion tile (shared memory)
   u32 *t_a0;
@@ -792,7 +793,7 @@ __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double
   if (cand <= C.ucut0) return true;
   if (!(cand <= C.ucut) || !(g & G_DEST_EPS)) return false;
   if (C.hq) {
-    const u32 q = __ldg(C.hq + d);
+    const u32 q = (__ldg(C.hq + (d >> 4)) >> ((d & 15u) * 2u)) & 3u;
     return q && cand <= C.ucut0 + (double)q * C.hq_unit;
   }
   return neg_test(C.neg, d, C.neg_fold);
