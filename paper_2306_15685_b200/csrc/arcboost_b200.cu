@@ -1200,6 +1200,62 @@ static cudaError_t launch_decode(const DecodeParams &P, int n, size_t smem, cuda
   return cudaGetLastError();
 }
 
+// One channel per thread-block cluster of CL CTAs (1024 threads, one per SM),
+// the small graph's table split across the cluster's shared memory: C1 / C2,
+// where one CTA per channel would leave most SMs idle.
+template <int CL>
+static cudaError_t launch_decode_cluster(const DecodeParams &P, int n, size_t smem, cudaStream_t st) {
+  auto kern = decode_kernel<1024, Fmt16SC<CL>, float>;
+  static size_t attr_set = 0;
+  static int sms = 0;
+  if (smem > attr_set) {
+    const size_t want = std::max(dyn_smem_max(), smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    attr_set = want;
+  }
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int max_clusters = std::max(1, sms / CL);
+  const int waves = (n + max_clusters - 1) / max_clusters;
+  const int nclu = (n + waves - 1) / waves;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclu * CL), 1, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (getenv("AB_VERBOSE")) {
+    static int said = 0;
+    if (said++ < 4) fprintf(stderr, "[arcboost] decode_kernel<1024, cluster %d>: %d clusters, dynamic %zu\n", CL, nclu, smem);
+  }
+  return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+// CTAs per channel for n channels of a small graph (its table in shared
+// memory): the largest cluster (8 / 4 / 2) with n clusters resident at once;
+// 1 = no cluster.  AB_CLUSTER overrides (1 disables).
+static int pick_cluster(int n) {
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char *e = getenv("AB_CLUSTER")) {
+    const int c = atoi(e);
+    return (c == 2 || c == 4 || c == 8) ? c : 1;
+  }
+  for (int c = 8; c >= 2; c /= 2)
+    if ((long long)n * c <= sms) return c;
+  return 1;
+}
+
 // Whether a channel's direct token table (table_cap 16-byte values) fits in
 // shared memory next to the 1024-thread kernel's static tiles and the dynamic
 // context / score-row area (`smem`): then the table's loads and CAS-128s stay
@@ -1496,8 +1552,14 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       else le = s64 ? launch_decode_b<Fmt24<true>, double>(block, P, m, smem, st)
                     : launch_decode_b<Fmt24<true>, float>(block, P, m, smem, st);
     } else {
-      if (g->fmt16 && block == 1024 && (s64 ? smem_table_fits<double>(smem, P.table_cap)
-                                            : smem_table_fits<float>(smem, P.table_cap)))
+      const int clu = (g->fmt16 && block == 1024 && !s64) ? pick_cluster(m) : 1;
+      const size_t part = ((size_t)P.table_cap + clu - 1) / clu * 16; // a cluster CTA's table share
+      if (clu > 1 && smem_table_fits<float>(smem, (size_t)P.table_cap / clu + 1))
+        le = clu == 8 ? launch_decode_cluster<8>(P, m, smem + part, st)
+           : clu == 4 ? launch_decode_cluster<4>(P, m, smem + part, st)
+                      : launch_decode_cluster<2>(P, m, smem + part, st);
+      else if (g->fmt16 && block == 1024 && (s64 ? smem_table_fits<double>(smem, P.table_cap)
+                                                 : smem_table_fits<float>(smem, P.table_cap)))
         le = s64 ? launch_decode<1024, Fmt16S, double>(P, m, smem + (size_t)P.table_cap * 16, st)
                  : launch_decode<1024, Fmt16S, float>(P, m, smem + (size_t)P.table_cap * 16, st);
       else if (g->fmt16) le = s64 ? launch_decode_b<Fmt16<false>, double>(block, P, m, smem, st)

@@ -203,6 +203,7 @@ struct __align__(8) XArc24 { u32 ns, g, ol, pad; double w; };
 template <bool H, bool SMT = false> struct Fmt16 {
   static constexpr bool hashed = H; // token table: hashed (true) or identity-mapped
   static constexpr bool smem_table = SMT; // identity-mapped table in shared memory (small graphs)
+  static constexpr int cluster = 1;       // CTAs per channel
   typedef EArc16 E;
   typedef XArc16 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -226,6 +227,7 @@ template <bool H, bool SMT = false> struct Fmt16 {
 template <bool H> struct Fmt24 {
   static constexpr bool hashed = H;
   static constexpr bool smem_table = false;
+  static constexpr int cluster = 1;
   typedef EArc24 E;
   typedef XArc24 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -252,6 +254,15 @@ template <bool H> struct Fmt24 {
 };
 
 typedef Fmt16<false, true> Fmt16S; // direct table in shared memory (one macro argument)
+// A channel decoded by a cluster of CL CTAs (C1 / C2: few channels, small
+// graph): the shared-memory table split across the cluster (state s in CTA
+// s % CL), the channel's counters in the leader's shared memory, DSMEM between.
+template <int CL> struct Fmt16SC : Fmt16<false, true> {
+  static constexpr int cluster = CL;
+};
+typedef Fmt16SC<2> Fmt16SC2;
+typedef Fmt16SC<4> Fmt16SC4;
+typedef Fmt16SC<8> Fmt16SC8;
 
 struct ChanState {
   ab_channel_info info; // info.store_len = records appended this utterance (reference len(store))
@@ -372,12 +383,19 @@ __device__ __forceinline__ void ld_cg_entry(const Entry *e, u64 &key, u64 &ck, u
   g = (u32)d;
   info = (u32)(d >> 32);
 }
-// Value accessors; SM = the table lives in shared memory (Fmt::smem_table).
-template <bool SM = false> __device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
+// Value accessors; SM = where the table lives: 0 global memory, 1 this CTA's
+// shared memory (Fmt::smem_table), 2 the cluster's distributed shared memory
+// (generic addresses into the peer CTAs' windows, Fmt::cluster > 1).
+template <typename F> __host__ __device__ constexpr int table_space() {
+  return F::smem_table ? (F::cluster > 1 ? 2 : 1) : 0;
+}
+template <int SM = 0> __device__ __forceinline__ void ld_cg_value(const u64 *v, u64 &ck, u32 &g, u32 &info) {
   u64 a, b;
-  if (SM) {
+  if (SM == 1) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(v);
     asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(sa) : "memory");
+  } else if (SM == 2) {
+    asm volatile("ld.relaxed.cluster.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v) : "memory");
   } else {
     asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v));
   }
@@ -387,9 +405,16 @@ template <bool SM = false> __device__ __forceinline__ void ld_cg_value(const u64
 }
 // CAS-128 that only issues: the old value comes back in (r0, r1); the caller
 // compares, so several can be in flight per thread.
-template <bool SM = false>
+template <int SM = 0>
 __device__ __forceinline__ void cas128(u64 *addr, u64 e0, u64 e1, u64 d0, u64 d1, u64 &r0, u64 &r1) {
-  if (SM) {
+  if (SM == 2) {
+    asm volatile(
+        "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
+        " atom.relaxed.cluster.cas.b128 r, [%6], e, d;\n mov.b128 {%0, %1}, r;\n}\n"
+        : "=l"(r0), "=l"(r1)
+        : "l"(e0), "l"(e1), "l"(d0), "l"(d1), "l"(addr)
+        : "memory");
+  } else if (SM == 1) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(addr);
     asm volatile(
         "{\n .reg .b128 e, d, r;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
@@ -408,7 +433,7 @@ __device__ __forceinline__ void cas128(u64 *addr, u64 e0, u64 e1, u64 d0, u64 d1
 }
 
 // 128-bit compare-and-swap on the value half of an entry (ATOMG.E.CAS.128).
-template <bool SM = false>
+template <int SM = 0>
 __device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u64 nck, u32 ng, u32 ninfo) {
   u64 e0 = ck, e1 = ((u64)info << 32) | g;
   u64 d0 = nck, d1 = ((u64)ninfo << 32) | ng;
@@ -642,18 +667,33 @@ enum {
   E_CAP = AB_ERR_CAPACITY
 };
 
-struct Shared {
-  // per-phase counters
-  u32 n_new, n_app, n_cand, rec_n, n_keep, n_tok, flog_n;
+// A channel's counters.  With one CTA per channel they are in its shared
+// memory; a channel decoded by a thread-block cluster (Fmt::cluster > 1, C1 /
+// C2) keeps them in the leader CTA's, reached over DSMEM (GC()).
+struct Counters {
+  u32 n_new, n_app, n_cand, rec_n, flog_n;
   unsigned long long rec_logical;
   unsigned long long min_ck; // cheapest application of the current frame
   int error;
+  int max_depth;
+  unsigned long long cnt_tok, cnt_emit, cnt_eps;
+  int n_rec_frame; // emission records of the frame (olabel != 0 applications)
+  u32 n_kill;      // kill queue length of the current round
+  u32 eps_n;       // entries in the channel's epsilon-frontier list this frame
+  u32 emit_end;    // rows below come from the emitting pass (their source is a token)
+  int best_last_il;
+  double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
+  u32 out_tok, out_mem; // cluster prune: survivors / split-bucket rows reserved so far
+};
+
+struct Shared {
+  Counters cnt;    // this channel's counters (leader CTA of a cluster)
+  Counters *lead;  // the leader's counters (cluster mode: a DSMEM address)
   u32 sel;
   u32 cum;
+  u32 out_base_tok, out_base_mem; // cluster prune: a tile's reserved output positions
   int shared_words;
-  int max_depth;
   long long words_off;
-  unsigned long long cnt_tok, cnt_emit, cnt_eps;
   // scan / reduce scratch
   u32 scan[32];
   u64 redk[32];
@@ -663,13 +703,7 @@ struct Shared {
   // killed (prune finds its split bucket without a pass over the rows)
   u32 fhist[1024];
   double hbase, hscale;
-  int n_rec_frame; // emission records of the frame (olabel != 0 applications)
-  u32 n_kill;   // kill queue length of the current round
-  u32 eps_n;    // entries in the channel's epsilon-frontier list this frame
-  u32 emit_end; // rows below come from the emitting pass (their source is a token)
-  int best_last_il;
   double cut_hint; // this attempt's cutoff hint (inf: unfiltered), see advance()
-  double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
   int filtered;
   // next frame's score row, bulk-copied into the row buffer once the current
   // frame's emitting pass is final (prune verified it; see decode_kernel)
@@ -683,6 +717,34 @@ struct Shared {
 #endif
 };
 
+// The channel's counters: this CTA's, or the cluster leader's (DSMEM).
+template <typename F> __device__ __forceinline__ Counters &GC(Shared &sh) {
+  if constexpr (F::cluster > 1) return *sh.lead;
+  else return sh.cnt;
+}
+
+// Rank of this CTA in the channel's cluster (0 = leader) and the channel-wide
+// barrier: the cluster barrier (release / acquire at cluster scope, so the
+// leader's counters and every CTA's global writes are visible after it) or
+// the CTA barrier.
+template <typename F> __device__ __forceinline__ u32 crank() {
+  if constexpr (F::cluster > 1) {
+    u32 r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+  } else {
+    return 0;
+  }
+}
+template <typename F> __device__ __forceinline__ void csync() {
+  if constexpr (F::cluster > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
+}
+// thread 0 of the channel (the leader CTA's)
+template <typename F> __device__ __forceinline__ bool chan_t0() { return threadIdx.x == 0 && crank<F>() == 0; }
+
 template <typename F, typename S> struct Chan {
   const DecodeParams *P;
   int b; // batch index of the channel this CTA is decoding
@@ -691,6 +753,8 @@ template <typename F, typename S> struct Chan {
   Entry *table;
   u64 *vals;
   u64 *gvals; // the channel's global direct table (wiped with a shared-memory table)
+  u64 *peer_vals[8]; // cluster: every CTA's part of the shared-memory table (generic DSMEM addresses)
+  Shared *peer_sh[8]; // cluster: every CTA's Shared (histograms, per-CTA best tokens)
   u32 *tok_state;
   double *tok_cost;
   TokInfo *tok_info;
@@ -733,6 +797,19 @@ template <typename F, typename S> struct Chan {
   u32 *t_src;
   double *t_cost;
 };
+
+// The cheapest application of the frame: this CTA's, or the minimum over the
+// cluster's CTAs (each keeps its own, see expand).
+template <typename F, typename S> __device__ __forceinline__ u64 frame_min_ck(const Chan<F, S> &C, Shared &sh) {
+  if constexpr (F::cluster > 1) {
+    u64 m = ~0ull;
+#pragma unroll
+    for (int r = 0; r < F::cluster; ++r) m = min(m, C.peer_sh[r]->cnt.min_ck);
+    return m;
+  } else {
+    return sh.cnt.min_ck;
+  }
+}
 
 constexpr u32 NB_HIST = 1024;
 constexpr double HIST_PER_BEAM = 256.0; // buckets per beam width
@@ -799,13 +876,17 @@ __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double
   return neg_test(C.neg, d, C.neg_fold);
 }
 
-__device__ __forceinline__ void set_error(Shared &sh, int code) { atomicCAS(&sh.error, 0, code); }
+template <typename F> __device__ __forceinline__ void set_error(Shared &sh, int code) {
+  atomicCAS(&GC<F>(sh).error, 0, code);
+}
 
 template <bool H> __device__ __forceinline__ u32 home_slot(const DecodeParams &P, u32 d) {
   return H ? ((d * 2654435761u) >> P.hash_shift) & P.table_mask : d;
 }
 // value of a slot
 template <typename F, typename S> __device__ __forceinline__ u64 *val_at(const Chan<F, S> &C, u32 slot) {
+  // a cluster's table: state s in CTA s % cluster, at s / cluster
+  if constexpr (F::cluster > 1) return C.peer_vals[slot % F::cluster] + 2 * (size_t)(slot / F::cluster);
   return F::hashed ? &C.table[slot].ck : C.vals + 2 * (size_t)slot;
 }
 
@@ -840,9 +921,9 @@ struct RelaxAcc {
 // Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
 template <typename F, typename S>
 __device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 v) {
-  const u32 k = atomicAdd(&sh.n_kill, 1u);
+  const u32 k = atomicAdd(&GC<F>(sh).n_kill, 1u);
   if (k < P.flog_cap) C.app_list[k] = v;
-  else set_error(sh, E_CAP);
+  else set_error<F>(sh, E_CAP);
 }
 
 // Outcome of a successful CAS that replaced old_info.
@@ -882,7 +963,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
     }
     const u32 old_info = vinfo;
     const u64 old_ck = vck;
-    if (cas_value<F::smem_table>(v, vck, vg, vinfo, ck, g, info)) {
+    if (cas_value<table_space<F>()>(v, vck, vg, vinfo, ck, g, info)) {
       installed(P, C, sh, acc, row0, etag, old_info, old_ck, ck);
       return;
     }
@@ -908,22 +989,22 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     if ((u32)key == d) break;
     slot = (slot + 1) & P.table_mask;
     if (++probes > P.table_mask) {
-      set_error(sh, E_CAP);
+      set_error<F>(sh, E_CAP);
       return;
     }
     ld_cg_entry(&C.table[slot], key, vck, vg, vinfo);
   }
   if (!value_better(ck, g, row0, C.etag, vck, vg, vinfo)) return;
-  const u32 row = atomicAdd(&sh.flog_n, 1u);
+  const u32 row = atomicAdd(&GC<F>(sh).flog_n, 1u);
   if (row >= P.flog_cap) {
-    set_error(sh, E_CAP);
+    set_error<F>(sh, E_CAP);
     return;
   }
   C.flog_state[row] = d | rflags;
   C.flog_ck[row] = ck;
   u32 epos = NO_EPS;
   if (rflags & ROW_EPS) {
-    epos = atomicAdd(&sh.eps_n, 1u);
+    epos = atomicAdd(&GC<F>(sh).eps_n, 1u);
     C.eps_list[epos] = make_uint4(row, d | rflags, (u32)ck, (u32)(ck >> 32));
   }
   C.flog_aux[row] = make_uint4(aux_src(src, rflags, g), epos, lab_ol, lab_il);
@@ -957,7 +1038,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     vinfo[u] = 0;
     if (on[u]) {
       if (F::hashed) ld_cg_entry(&C.table[slot[u]], key[u], vck[u], vg[u], vinfo[u]);
-      else ld_cg_value<F::smem_table>(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
+      else ld_cg_value<table_space<F>()>(val_at(C, slot[u]), vck[u], vg[u], vinfo[u]);
     }
   }
   bool fast[U];
@@ -989,16 +1070,16 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     nw += want[u] ? 1u : 0u;
   }
   if (!nw) return;
-  u32 row = agg_reserve(&sh.flog_n, nw);
+  u32 row = agg_reserve(&GC<F>(sh).flog_n, nw);
   if (row + nw > P.flog_cap) {
-    set_error(sh, E_CAP);
+    set_error<F>(sh, E_CAP);
     return;
   }
   u32 rows[U], ninfo[U], eps_pos[U];
   u32 ne = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
-  u32 ep_at = agg_reserve(&sh.eps_n, ne);
+  u32 ep_at = agg_reserve(&GC<F>(sh).eps_n, ne);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
@@ -1021,7 +1102,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (want[u])
-      cas128<F::smem_table>(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u], ((u64)ninfo[u] << 32) | g[u],
+      cas128<table_space<F>()>(val_at(C, slot[u]), vck[u], ((u64)vinfo[u] << 32) | vg[u], ck[u], ((u64)ninfo[u] << 32) | g[u],
              r0[u], r1[u]);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -1081,8 +1162,11 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   u32 *w_pref = t_pref + wid * WT;
   u32 *w_src = t_src + wid * WT;
   double *w_cost = t_cost + wid * WT;
-  const u32 per = n_in >= NW * WT ? WT : max(1u, (n_in + NW - 1) / NW);
-  for (u32 base = wid * per; base < n_in; base += NW * per) {
+  // a cluster's warps share the inputs: warp (rank, wid) is global warp gw of CL * NW
+  constexpr u32 GW = NW * F::cluster;
+  const u32 gw = crank<F>() * NW + wid;
+  const u32 per = n_in >= GW * WT ? WT : max(1u, (n_in + GW - 1) / GW);
+  for (u32 base = gw * per; base < n_in; base += GW * per) {
     const u32 ne = min(per, n_in - base);
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
 #pragma unroll
@@ -1195,8 +1279,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     __syncwarp();
   }
   if (lane == 0 && arcs_seen) {
-    atomicAdd(&sh.n_cand, arcs_seen);
-    atomicAdd(EMIT ? &sh.cnt_emit : &sh.cnt_eps, (unsigned long long)arcs_seen);
+    atomicAdd(&GC<F>(sh).n_cand, arcs_seen);
+    atomicAdd(EMIT ? &GC<F>(sh).cnt_emit : &GC<F>(sh).cnt_eps, (unsigned long long)arcs_seen);
   }
   } else {
   // tile position j = q * BLOCK + tid: input base + j, so every load of the
@@ -1324,17 +1408,20 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   const u32 n_app = __reduce_add_sync(0xFFFFFFFFu, acc.n_app);
   const u32 n_new = __reduce_add_sync(0xFFFFFFFFu, acc.n_new);
   if ((tid & 31) == 0) {
-    if (mck != ~0ull) atomicMin(&sh.min_ck, mck);
-    if (n_rec) atomicAdd(&sh.n_rec_frame, n_rec);
-    if (n_app) atomicAdd(&sh.n_app, n_app);
-    if (n_new && atomicAdd(&sh.n_new, n_new) + n_new > P.tok_cap) set_error(sh, E_CAP);
+    // (each CTA's own minimum: a 64-bit atomicMin into a peer CTA's shared
+    // memory is not atomic on sm_100, bench_tools/dsmem_atomics_probe.cu)
+    if (mck != ~0ull) atomicMin(&sh.cnt.min_ck, mck);
+    if (n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, n_rec);
+    if (n_app) atomicAdd(&GC<F>(sh).n_app, n_app);
+    if (n_new && atomicAdd(&GC<F>(sh).n_new, n_new) + n_new > P.tok_cap) set_error<F>(sh, E_CAP);
   }
-  if (tid == 0) {
-    if (EMIT) sh.cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
+  static_assert(F::cluster == 1 || WARP_TILES, "a cluster's channel uses warp tiles");
+  if (tid == 0 && crank<F>() == 0) {
+    if (EMIT) GC<F>(sh).cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
     if (!WARP_TILES) {
-      sh.n_cand += arcs_seen;
-      if (EMIT) sh.cnt_emit += arcs_seen;
-      else sh.cnt_eps += arcs_seen;
+      GC<F>(sh).n_cand += arcs_seen;
+      if (EMIT) GC<F>(sh).cnt_emit += arcs_seen;
+      else GC<F>(sh).cnt_eps += arcs_seen;
     }
   }
 }
@@ -1343,9 +1430,9 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 // are not applications, superseded ones are applications but not tokens.
 template <int BLOCK, typename F, typename S>
 __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
-  const u32 n = min(sh.n_kill, P.flog_cap);
+  const u32 n = min(GC<F>(sh).n_kill, P.flog_cap);
   u32 unrec = 0;
-  for (u32 i = threadIdx.x; i < n; i += BLOCK) {
+  for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
     const u32 v = C.app_list[i];
     const u32 row = v & VROW_MASK;
     const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
@@ -1358,15 +1445,15 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
     }
   }
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
-  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&sh.n_rec_frame, unrec);
-  __syncthreads();
-  if (threadIdx.x == 0) sh.n_kill = 0;
-  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&GC<F>(sh).n_rec_frame, unrec);
+  csync<F>();
+  if (chan_t0<F>()) GC<F>(sh).n_kill = 0;
+  csync<F>();
 }
 
 // Provenance of a surviving frontier row (decoder.py:385-393, 289-295): one
 // walk over the row's source links back to the token of the previous frame
-// (rows below sh.emit_end are the emitting pass's; their source is a token
+// (rows below GC<F>(sh).emit_end are the emitting pass's; their source is a token
 // index) or to the utterance start.  Each arc with olabel != 0 on the way
 // gets an emission record; a record is written once the next older record of
 // the chain is known, so the chain is walked only once.
@@ -1378,7 +1465,7 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   base.depth = 0;
   base.hits = 0;
   base.last_il = 0;
-  const u32 emit_end = sh.emit_end;
+  const u32 emit_end = GC<F>(sh).emit_end;
   int hits = 0, nrec = 0, newest = -1, pend = -1;
   u32 pend_ol = 0, il = 0;
   u32 cur = row;
@@ -1387,9 +1474,9 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
     if (ax.x & AUX_START) break;
     hits += (ax.x & AUX_BOOST) ? 1 : 0;
     if (ax.x & AUX_HASOL) {
-      const u32 r = atomicAdd(&sh.rec_n, 1u);
+      const u32 r = atomicAdd(&GC<F>(sh).rec_n, 1u);
       if (r >= P.arena_cap) {
-        set_error(sh, E_CAP);
+        set_error<F>(sh, E_CAP);
         break;
       }
       if (pend >= 0) C.arena[pend] = make_int2((int)pend_ol, (int)r); // r is the older record
@@ -1423,31 +1510,31 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
   int rounds = 0;
   while (true) {
     if (!(n_front > 0 && rounds < P.max_eps)) {
-      if (n_front > 0 && threadIdx.x == 0) C.cs->info.eps_truncations += 1; // while-else 314-316
+      if (n_front > 0 && chan_t0<F>()) C.cs->info.eps_truncations += 1; // while-else 314-316
       break;
     }
     rounds++;
-    const u32 row0 = sh.flog_n; // rows below were written by earlier rounds of this frame
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      sh.n_app = 0;
-      sh.n_cand = 0;
-      sh.cnt_tok += n_front; // token expansions of the reference's round
+    const u32 row0 = GC<F>(sh).flog_n; // rows below were written by earlier rounds of this frame
+    csync<F>();
+    if (chan_t0<F>()) {
+      GC<F>(sh).n_app = 0;
+      GC<F>(sh).n_cand = 0;
+      GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
     }
-    __syncthreads();
+    csync<F>();
     expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
-    __syncthreads();
+    csync<F>();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
     PROF_COUNT(sh, PF_ROUNDS, 1);
-    const u32 n_cand = sh.n_cand, n_app = sh.n_app;
-    if (sh.error) return;
+    const u32 n_cand = GC<F>(sh).n_cand, n_app = GC<F>(sh).n_app;
+    if (GC<F>(sh).error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
     lo = hi;
-    hi = sh.eps_n;
+    hi = GC<F>(sh).eps_n;
     n_front = n_app;
   }
-  __syncthreads();
+  csync<F>();
 }
 
 
@@ -1458,32 +1545,34 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
 template <int BLOCK, typename F, typename S>
 __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 n_tok,
                               const u32 *rows, int best_row) {
-  if (threadIdx.x == 0) {
-    sh.max_depth = 0;
-    sh.best_last_il = 0;
+  if (chan_t0<F>()) {
+    GC<F>(sh).max_depth = 0;
+    GC<F>(sh).best_last_il = 0;
   }
-  __syncthreads();
+  csync<F>();
   int md = 0;
-  for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) {
+  for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n_tok; i += BLOCK * F::cluster) {
     const u32 r = rows[i];
     const TokInfo t = resolve_row(P, C, sh, r, C.tok_info);
     md = max(md, t.depth);
     C.tok_info_alt[i] = t;
-    if ((int)r == best_row) sh.best_last_il = t.last_il;
+    if ((int)r == best_row) GC<F>(sh).best_last_il = t.last_il;
   }
   md = __reduce_max_sync(0xFFFFFFFFu, md);
-  if ((threadIdx.x & 31) == 0) atomicMax(&sh.max_depth, md);
-  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicMax(&GC<F>(sh).max_depth, md);
+  csync<F>();
   if (threadIdx.x == 0) {
-    C.cs->max_depth = sh.max_depth;
-    C.cs->info.num_active = (int)n_tok;
-    C.cs->tok_half ^= 1u;
-    Chan<F, S> &M = const_cast<Chan<F, S> &>(C);
+    if (crank<F>() == 0) {
+      C.cs->max_depth = GC<F>(sh).max_depth;
+      C.cs->info.num_active = (int)n_tok;
+      C.cs->tok_half ^= 1u;
+    }
+    Chan<F, S> &M = const_cast<Chan<F, S> &>(C); // every CTA's view swaps its halves
     TokInfo *t = M.tok_info;
     M.tok_info = M.tok_info_alt;
     M.tok_info_alt = t;
   }
-  __syncthreads();
+  csync<F>();
 }
 
 // Radix select over 64-bit keys (MSD, DB-bit digits, starting below the
@@ -1572,8 +1661,8 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   // digit histograms of the split-bucket selection live in the expansion tile
   constexpr int DB = (BLOCK * exp_q<BLOCK>() >= 2048) ? 11 : (BLOCK * exp_q<BLOCK>() >= 1024) ? 10 : (BLOCK * exp_q<BLOCK>() >= 512) ? 9 : 8;
   const int tid = threadIdx.x;
-  const u32 n_rows = sh.flog_n;
-  const u64 best_ck = sh.min_ck;
+  const u32 n_rows = GC<F>(sh).flog_n;
+  const u64 best_ck = frame_min_ck<F>(C, sh);
   const double thr = key_cost(best_ck) + P.beam;
   const u64 thr_ck = cost_key(thr);
   u32 *scr_state = C.app_list; // the kill queue is free until the next frame
@@ -1581,11 +1670,23 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   // max_active; buckets below the threshold's bucket are entirely in the beam
   const u32 bt = hbucket(sh, thr);
   const u32 want = (u32)P.max_active;
+  // the frame's live-row histogram: this CTA's, or the sum over the cluster's
+  const u32 *hist = sh.fhist;
+  if constexpr (F::cluster > 1) {
+    for (u32 b = tid; b < NB_HIST; b += BLOCK) {
+      u32 t = 0;
+#pragma unroll
+      for (int r = 0; r < F::cluster; ++r) t += C.peer_sh[r]->fhist[b];
+      C.t_a0[b] = t;
+    }
+    __syncthreads();
+    hist = C.t_a0;
+  }
   {
     constexpr u32 PER = NB_HIST / BLOCK > 0 ? NB_HIST / BLOCK : 1;
     const u32 b0 = min((u32)tid * PER, bt + 1), b1 = min(b0 + PER, bt + 1);
     u32 lsum = 0;
-    for (u32 b = b0; b < b1; ++b) lsum += sh.fhist[b];
+    for (u32 b = b0; b < b1; ++b) lsum += hist[b];
     u32 total;
     const u32 excl = block_excl_scan<BLOCK>(lsum, total, sh.scan);
     if (tid == 0) {
@@ -1596,8 +1697,8 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     if (excl < want && want <= excl + lsum) {
       u32 cum = excl, b = b0;
       for (; b < b1; ++b) {
-        if (cum + sh.fhist[b] >= want) break;
-        cum += sh.fhist[b];
+        if (cum + hist[b] >= want) break;
+        cum += hist[b];
       }
       if (b < bt) {
         sh.sel = b;
@@ -1615,16 +1716,16 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const bool verified = !sh.filtered || cut <= sh.cut_hint;
   __syncthreads();
   if (!verified) {
-    if (tid == 0) sh.cut_fail = cut;
-    __syncthreads();
+    if (chan_t0<F>()) GC<F>(sh).cut_fail = cut;
+    csync<F>();
     return false;
   }
-  if (tid == 0) {
-    if (sh.next_row) { // the score row is read by the emitting pass only, which is now final
-      bulk_row_load(const_cast<S *>(C.row), sh.next_row, (u32)(P.L * sizeof(S)), &sh.row_bar);
-      sh.row_pending = 1;
-    }
-    if (sh.n_rec_frame) atomicAdd(&sh.rec_logical, (unsigned long long)sh.n_rec_frame);
+  if (tid == 0 && sh.next_row) { // the score row is read by the emitting pass only, which is now final
+    bulk_row_load(const_cast<S *>(C.row), sh.next_row, (u32)(P.L * sizeof(S)), &sh.row_bar);
+    sh.row_pending = 1;
+  }
+  if (chan_t0<F>()) {
+    if (GC<F>(sh).n_rec_frame) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)GC<F>(sh).n_rec_frame);
     const double prev = C.cs->prev_cut;
     const double rise = prev < INFINITY ? cut - prev : 0.0;
     C.cs->cut_rise = fmax(rise, 0.8 * C.cs->cut_rise);
@@ -1637,7 +1738,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   int bi = -1;
   u32 n_tok = 0, n_mem = 0;
   u32 *mem_row = C.scr_row + P.flog_cap; // set-aside rows grow down from the top of scr_row
-  for (u32 base = 0; base < n_rows; base += TILE) {
+  for (u32 base = crank<F>() * TILE; base < n_rows; base += TILE * F::cluster) {
     // rows base + q * BLOCK + tid: warp-coalesced loads
     u32 st[QP], bq[QP];
     u64 ck[QP];
@@ -1660,8 +1761,21 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       nm += (live && bq[q] == split && ck[q] <= thr_ck) ? 1u : 0u;
     }
     u32 tot_s, tot_m;
-    u32 ps = n_tok + block_excl_scan<BLOCK>(ns, tot_s, sh.scan);
-    u32 pm = n_mem + block_excl_scan<BLOCK>(nm, tot_m, sh.scan);
+    u32 ps = block_excl_scan<BLOCK>(ns, tot_s, sh.scan);
+    u32 pm = block_excl_scan<BLOCK>(nm, tot_m, sh.scan);
+    if constexpr (F::cluster > 1) { // output positions reserved on the leader's counters
+      if (tid == 0) {
+        sh.out_base_tok = tot_s ? atomicAdd(&GC<F>(sh).out_tok, tot_s) : 0u;
+        sh.out_base_mem = tot_m ? atomicAdd(&GC<F>(sh).out_mem, tot_m) : 0u;
+      }
+      __syncthreads();
+      ps += sh.out_base_tok;
+      pm += sh.out_base_mem;
+      __syncthreads();
+    } else {
+      ps += n_tok;
+      pm += n_mem;
+    }
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
       if (bq[q] > split || (bq[q] == split && ck[q] > thr_ck)) continue;
@@ -1684,16 +1798,29 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     n_mem += tot_m;
   }
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
+  if constexpr (F::cluster > 1) { // the cluster's best and totals
+    csync<F>();
+    for (int r = 0; r < F::cluster; ++r) {
+      const Shared *o = C.peer_sh[r];
+      const u64 k2 = o->redk[0];
+      const u32 s2 = o->reds[0];
+      if (k2 < bk || (k2 == bk && s2 < bs)) bk = k2, bs = s2, bi = o->redi[0];
+    }
+    n_tok = GC<F>(sh).out_tok;
+    n_mem = GC<F>(sh).out_mem;
+    csync<F>();
+  }
   PROF_MARK(sh, PF_PRUNE_SCAN);
   if (below == 0xFFFFFFFFu) below = n_tok; // split at bt: everything below survives
   const u32 need = want > below ? want - below : 0u;
   if (n_mem > need) {
     if (n_tok + n_mem + need > P.flog_cap) { // survivors' rows would reach the set-aside rows
-      if (tid == 0) set_error(sh, E_CAP);
-      __syncthreads();
+      if (chan_t0<F>()) set_error<F>(sh, E_CAP);
+      csync<F>();
       return true;
     }
-    // exact (cost, state) order inside the split bucket
+    // exact (cost, state) order inside the split bucket (a cluster's leader alone)
+    if (crank<F>() == 0) {
     u64 tc = ~0ull;
     u32 ts = 0xFFFFFFFFu;
     if (need > 0) {
@@ -1747,31 +1874,32 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       }
       n_tok += total;
     }
-  } else if (n_mem > 0) { // the whole split bucket survives
-    for (u32 base = 0; base < n_mem; base += BLOCK) {
-      const u32 m = base + tid;
-      const bool keep = m < n_mem;
-      u32 total;
-      const u32 p = n_tok + block_excl_scan<BLOCK>(keep ? 1u : 0u, total, sh.scan);
-      if (keep) {
-        C.tok_state[p] = scr_state[m];
-        C.tok_cost[p] = key_cost(C.scr_key[m]);
-        C.scr_row[p] = *(mem_row - 1 - m);
-      }
-      n_tok += total;
+    if (F::cluster > 1 && tid == 0) GC<F>(sh).out_tok = n_tok;
     }
+    if constexpr (F::cluster > 1) {
+      csync<F>();
+      n_tok = GC<F>(sh).out_tok;
+    }
+  } else if (n_mem > 0) { // the whole split bucket survives (split across a cluster's CTAs)
+    const u32 n0 = n_tok;
+    for (u32 m = crank<F>() * BLOCK + tid; m < n_mem; m += BLOCK * F::cluster) {
+      C.tok_state[n0 + m] = scr_state[m];
+      C.tok_cost[n0 + m] = key_cost(C.scr_key[m]);
+      C.scr_row[n0 + m] = *(mem_row - 1 - m);
+    }
+    n_tok += n_mem;
   }
-  __syncthreads();
+  csync<F>();
   PROF_MARK(sh, PF_PRUNE_SEL);
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, bi);
-  if (tid == 0) {
-    if (P.silence_ilabel > 0 && sh.best_last_il == P.silence_ilabel)
+  if (chan_t0<F>()) {
+    if (P.silence_ilabel > 0 && GC<F>(sh).best_last_il == P.silence_ilabel)
       C.cs->info.trailing_silence += 1;
     else
       C.cs->info.trailing_silence = 0;
     C.cs->prev_best = key_cost(best_ck);
   }
-  __syncthreads();
+  csync<F>();
   PROF_MARK(sh, PF_PRUNE_OUT);
   return true;
 }
@@ -1780,14 +1908,16 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
 // closure, which is not pruned).
 template <int BLOCK, typename F, typename S>
 __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
-  const u32 n_rows = sh.flog_n;
+  const u32 n_rows = GC<F>(sh).flog_n;
   u32 n_tok = 0;
-  for (u32 i0 = 0; i0 < n_rows; i0 += BLOCK) {
+  csync<F>();
+  // (a cluster's leader alone: the utterance start's closure is small)
+  for (u32 i0 = 0; i0 < n_rows && crank<F>() == 0; i0 += BLOCK) {
     const u32 i = i0 + threadIdx.x;
     const u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
     const bool live = !(st & (ROW_DEAD | ROW_DISP));
     const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, (st & (ROW_DISP | ROW_HASOL)) == ROW_HASOL));
-    if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&sh.rec_logical, (unsigned long long)nrec);
+    if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)nrec);
     u32 total;
     const u32 p = n_tok + block_excl_scan<BLOCK>(live ? 1u : 0u, total, sh.scan);
     if (live) {
@@ -1797,14 +1927,19 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
     }
     n_tok += total;
   }
-  __syncthreads();
+  if constexpr (F::cluster > 1) {
+    if (chan_t0<F>()) GC<F>(sh).out_tok = n_tok;
+    csync<F>();
+    n_tok = GC<F>(sh).out_tok;
+  }
+  csync<F>();
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, -1);
-  if (threadIdx.x == 0) {
-    C.cs->prev_best = key_cost(sh.min_ck);
+  if (chan_t0<F>()) {
+    C.cs->prev_best = key_cost(frame_min_ck<F>(C, sh));
     C.cs->prev_cut = INFINITY; // the start closure is not pruned: no cutoff to start from
     C.cs->cut_rise = 0.0;
   }
-  __syncthreads();
+  csync<F>();
 }
 
 // Moves the channel to a fresh table epoch; the table is wiped when the
@@ -1825,34 +1960,41 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
         C.table[i].info = 0;
       }
     } else {
+      // (a cluster's CTAs each wipe their part: C.vals is this CTA's)
       uint4 *v = reinterpret_cast<uint4 *>(C.vals);
-      for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) v[i] = make_uint4(0, 0, 0, 0);
+      const u32 part = (P.table_cap + F::cluster - 1) / F::cluster;
+      for (u32 i = threadIdx.x; i < part; i += BLOCK) v[i] = make_uint4(0, 0, 0, 0);
       if (F::smem_table && C.gvals) { // keep the global table's tags consistent for later launches
         uint4 *gv = reinterpret_cast<uint4 *>(C.gvals);
-        for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) gv[i] = make_uint4(0, 0, 0, 0);
+        for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < P.table_cap; i += BLOCK * F::cluster)
+          gv[i] = make_uint4(0, 0, 0, 0);
       }
     }
     e += 1;
   }
   for (u32 b = threadIdx.x; b < NB_HIST; b += BLOCK) sh.fhist[b] = 0;
-  __syncthreads();
+  csync<F>(); // every CTA has read the old epoch
   if (threadIdx.x == 0) {
-    C.cs->epoch = e;
     C.epoch = e;
     C.etag = e & TAG_MASK;
-    sh.n_new = 0;
-    sh.n_app = 0;
-    sh.n_cand = 0;
-    sh.flog_n = 0;
-    sh.n_kill = 0;
-    sh.eps_n = 0;
-    sh.emit_end = 0;
-    sh.min_ck = ~0ull;
-    sh.n_rec_frame = 0;
     sh.hbase = C.cs->prev_best - P.beam;
     sh.hscale = HIST_PER_BEAM / P.beam;
+    sh.cnt.min_ck = ~0ull; // every CTA's own frame minimum (frame_min_ck)
   }
-  __syncthreads();
+  if (chan_t0<F>()) {
+    C.cs->epoch = e;
+    GC<F>(sh).out_tok = 0;
+    GC<F>(sh).out_mem = 0;
+    GC<F>(sh).n_new = 0;
+    GC<F>(sh).n_app = 0;
+    GC<F>(sh).n_cand = 0;
+    GC<F>(sh).flog_n = 0;
+    GC<F>(sh).n_kill = 0;
+    GC<F>(sh).eps_n = 0;
+    GC<F>(sh).emit_end = 0;
+    GC<F>(sh).n_rec_frame = 0;
+  }
+  csync<F>();
 }
 
 // Copying collector for the emission arena: records reachable from the token
@@ -1861,9 +2003,12 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
 // change: only record ids do, so the prefix-sharing path is reset.
 template <int BLOCK, typename F, typename S>
 __device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
-  const u32 n = sh.rec_n;
+  const u32 n = GC<F>(sh).rec_n;
   const u32 nw = (n + 31) / 32;
   const u32 n_tok = (u32)C.cs->info.num_active;
+  u32 carry = 0;
+  csync<F>();
+  if (crank<F>() == 0) { // a cluster's leader alone (rare)
   for (u32 w = threadIdx.x; w < nw; w += BLOCK) C.gc_bits[w] = 0;
   __syncthreads();
   for (u32 i = threadIdx.x; i < n_tok; i += BLOCK) {
@@ -1876,7 +2021,6 @@ __device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     }
   }
   __syncthreads();
-  u32 carry = 0;
   for (u32 base = 0; base < nw; base += BLOCK) {
     const u32 w = base + threadIdx.x;
     const u32 c = w < nw ? __popc(C.gc_bits[w]) : 0u;
@@ -1905,16 +2049,19 @@ __device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     const int bp = C.tok_info[i].bp;
     if (bp >= 0) C.tok_info[i].bp = newid(bp);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  }
+  csync<F>();
+  if (threadIdx.x == 0) { // every CTA's view swaps the halves
     int2 *t = C.arena;
     C.arena = C.arena_to;
     C.arena_to = t;
-    sh.rec_n = carry;
-    C.cs->arena_half ^= 1;
-    C.cs->path_len = 0;
+    if (crank<F>() == 0) {
+      GC<F>(sh).rec_n = carry;
+      C.cs->arena_half ^= 1;
+      C.cs->path_len = 0;
+    }
   }
-  __syncthreads();
+  csync<F>();
 }
 
 // Puts the utterance-start token into a fresh epoch (decoder.py:243-247):
@@ -1922,7 +2069,7 @@ __device__ void gc_arena(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
 template <int BLOCK, typename F, typename S>
 __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   next_epoch<BLOCK>(P, C, sh);
-  if (threadIdx.x == 0) {
+  if (chan_t0<F>()) {
     RelaxAcc acc;
     acc.min_ck = ~0ull;
     acc.n_new = acc.n_app = 0;
@@ -1931,11 +2078,11 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
     relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, z1, z1, 0u);
-    sh.n_kill = 0;
-    sh.emit_end = 0;
-    sh.min_ck = cost_key(0.0);
+    GC<F>(sh).n_kill = 0;
+    GC<F>(sh).emit_end = 0;
+    sh.cnt.min_ck = cost_key(0.0);
   }
-  __syncthreads();
+  csync<F>();
 }
 
 // advance_frame (decoder.py:341-411) for frame row C.row.
@@ -1943,33 +2090,32 @@ template <int BLOCK, typename F, typename S>
 __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   ChanState *cs = C.cs;
   if (cs->info.status != AB_IDLE && cs->info.status != AB_DECODING) {
-    if (threadIdx.x == 0) set_error(sh, E_STATUS);
-    __syncthreads();
+    if (chan_t0<F>()) set_error<F>(sh, E_STATUS);
+    csync<F>();
     return;
   }
   // one frame appends at most flog_cap records: collect first if they might not fit
-  if (!cs->info.fresh && (unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
+  if (!cs->info.fresh && (unsigned long long)GC<F>(sh).rec_n + P.flog_cap > P.arena_cap) {
     gc_arena<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_GC);
-    if ((unsigned long long)sh.rec_n + P.flog_cap > P.arena_cap) {
-      if (threadIdx.x == 0) set_error(sh, E_CAP);
-      __syncthreads();
+    if ((unsigned long long)GC<F>(sh).rec_n + P.flog_cap > P.arena_cap) {
+      if (chan_t0<F>()) set_error<F>(sh, E_CAP);
+      csync<F>();
       return;
     }
   }
   if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
-  __syncthreads();
+  csync<F>();
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
-    epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, 1u); // utterance-start closure, no prune
-    if (sh.error) return;
+    epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, 1u); // utterance-start closure, no prune
+    if (GC<F>(sh).error) return;
     rows_to_tokens<BLOCK>(P, C, sh);
-    if (threadIdx.x == 0) cs->info.fresh = 0;
+    if (chan_t0<F>()) cs->info.fresh = 0;
   }
-  __syncthreads();
+  csync<F>();
   PROF_MARK(sh, PF_START);
   const u32 n_tok = (u32)cs->info.num_active;
-  if (threadIdx.x == 0) cs->info.status = AB_DECODING;
   // Expansion-time cutoff.  No token whose cost exceeds the frame's cutoff C*
   // (min(best + beam, max_active-th cost)) survives prune, and an epsilon
   // path from a state lowers a cost by at most the context's slack S (-min
@@ -1986,16 +2132,18 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   // be needed, is unfiltered.  Emission records and epsilon-round
   // truncations of dropped candidates are not counted (P.exact keeps every
   // candidate and the reference's len(store) / eps_truncations).
-  const unsigned long long c_tok = sh.cnt_tok, c_emit = sh.cnt_emit, c_eps = sh.cnt_eps;
+  const unsigned long long c_tok = GC<F>(sh).cnt_tok, c_emit = GC<F>(sh).cnt_emit, c_eps = GC<F>(sh).cnt_eps;
   const long long eps_tr = cs->info.eps_truncations;
   bool filt = !P.exact && cs->prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
               P.max_eps <= C.slack_rounds;
+  csync<F>(); // every CTA has read the channel state above
+  if (chan_t0<F>()) cs->info.status = AB_DECODING;
   for (int attempt = 0;; ++attempt) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const double hint = !filt ? INFINITY
                           : attempt == 0 ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra
-                                         : sh.cut_fail;
+                                         : GC<F>(sh).cut_fail;
       sh.cut_hint = hint;
       sh.filtered = filt ? 1 : 0;
       // (+ a margin for the f64 rounding of path sums)
@@ -2005,43 +2153,42 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     }
     next_epoch<BLOCK>(P, C, sh);
     expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
-    __syncthreads();
+    csync<F>();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EMIT_X);
-    if (sh.error) return;
-    const u32 n_app = sh.n_app;
-    if (threadIdx.x == 0) sh.emit_end = sh.flog_n;
-    __syncthreads();
+    if (GC<F>(sh).error) return;
+    const u32 n_app = GC<F>(sh).n_app;
+    if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
+    csync<F>();
     bool ok = true;
     if (n_app == 0) {
       // no emitting arcs: every token dies (decoder.py:394-398); a filtered
       // attempt proves nothing here
       if (filt) ok = false;
-      else if (threadIdx.x == 0) cs->info.num_active = 0;
+      else if (chan_t0<F>()) cs->info.num_active = 0;
     } else {
-      epsilon_rounds<BLOCK>(P, C, sh, 0u, sh.eps_n, n_app);
-      if (sh.error) return;
+      epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, n_app);
+      if (GC<F>(sh).error) return;
       ok = prune<BLOCK>(P, C, sh);
     }
     if (ok) break;
-    __syncthreads();
-    if (threadIdx.x == 0) { // redo unfiltered: undo the attempt's counters
-      sh.cnt_tok = c_tok;
-      sh.cnt_emit = c_emit;
-      sh.cnt_eps = c_eps;
+    csync<F>();
+    if (chan_t0<F>()) { // redo: undo the attempt's counters
+      GC<F>(sh).cnt_tok = c_tok;
+      GC<F>(sh).cnt_emit = c_emit;
+      GC<F>(sh).cnt_eps = c_eps;
       cs->info.eps_truncations = eps_tr;
       cs->info.cut_redos += 1;
     }
-    __syncthreads();
-    filt = filt && attempt == 0 && sh.cut_fail < INFINITY; // second attempt: hint = C*_f; third: none
+    csync<F>();
+    filt = filt && attempt == 0 && GC<F>(sh).cut_fail < INFINITY; // second attempt: hint = C*_f; third: none
   }
   if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (chan_t0<F>()) {
     cs->info.frame_index += 1;
     cs->info.total_frames += 1;
   }
-  __syncthreads();
+  csync<F>();
 }
 
 // Traceback with prefix sharing against the channel's previous hypothesis
@@ -2053,7 +2200,7 @@ __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   if (threadIdx.x == 0) {
     int shared_words = 0;
     if ((u32)depth > P.path_cap) {
-      set_error(sh, E_CAP);
+      set_error<F>(sh, E_CAP);
     } else {
       int rec = bp, d = depth;
       const int plen = cs->path_len;
@@ -2069,14 +2216,14 @@ __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
       cs->path_len = depth;
       const long long need = depth - shared_words;
       const long long off = P.words_used[C.b];
-      if (off + need > P.words_stride || out_idx >= P.hyp_stride) set_error(sh, E_CAP);
+      if (off + need > P.words_stride || out_idx >= P.hyp_stride) set_error<F>(sh, E_CAP);
       else P.words_used[C.b] = off + need;
       sh.shared_words = shared_words;
       sh.words_off = (long long)C.b * P.words_stride + off;
     }
   }
   __syncthreads();
-  if (sh.error) return;
+  if (GC<F>(sh).error) return;
   const int s0 = sh.shared_words;
   const long long off = sh.words_off;
   for (int i = s0 + threadIdx.x; i < depth; i += BLOCK) P.words[off + (i - s0)] = C.path_words[i];
@@ -2106,7 +2253,7 @@ __device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int ou
   }
   const u32 n = (u32)cs->info.num_active;
   if (n == 0) {
-    if (threadIdx.x == 0) set_error(sh, E_DEAD);
+    if (threadIdx.x == 0) set_error<F>(sh, E_DEAD);
     __syncthreads();
     return;
   }
@@ -2130,7 +2277,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   ChanState *cs = C.cs;
   const int st = cs->info.status;
   if (st != AB_DECODING && st != AB_ENDPOINTED && !(st == AB_IDLE && cs->info.fresh)) {
-    if (threadIdx.x == 0) set_error(sh, E_STATUS);
+    if (threadIdx.x == 0) set_error<F>(sh, E_STATUS);
     __syncthreads();
     return;
   }
@@ -2153,7 +2300,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   }
   const u32 n = (u32)cs->info.num_active;
   if (n == 0) {
-    if (threadIdx.x == 0) set_error(sh, E_DEAD);
+    if (threadIdx.x == 0) set_error<F>(sh, E_DEAD);
     __syncthreads();
     return;
   }
@@ -2187,15 +2334,15 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   }
   const TokInfo t = C.tok_info[b];
   emit_hyp<BLOCK>(P, C, sh, out_idx, AB_FINAL, fallback, cost, t.bp, t.depth, t.hits);
-  if (sh.error) return;
+  if (GC<F>(sh).error) return;
   if (threadIdx.x == 0) {
     // _reset_utterance (decoder.py:151-159)
     cs->info.num_active = 0;
     cs->info.fresh = 1;
     cs->info.frame_index = 0;
     cs->info.trailing_silence = 0;
-    sh.rec_n = 0;
-    sh.rec_logical = 0;
+    GC<F>(sh).rec_n = 0;
+    GC<F>(sh).rec_logical = 0;
     cs->path_len = 0;
     cs->max_depth = 0;
     cs->prev_cut = INFINITY;
@@ -2342,34 +2489,49 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
     sh.row_pending = 0;
     sh.next_row = nullptr;
   }
-  for (int b = blockIdx.x; b < P.n; b += gridDim.x) {
+  // a channel per CTA, or per cluster of F::cluster CTAs (leader = rank 0)
+  constexpr int CLU = F::cluster;
+  const bool lead = crank<F>() == 0;
+  const u32 part = (P.table_cap + CLU - 1) / CLU; // this CTA's share of a shared-memory table
+  for (int b = blockIdx.x / CLU; b < P.n; b += gridDim.x / CLU) {
     setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src,
                          P.neg_words ? sh_neg : nullptr);
     ChanState *cs = C.cs;
     if (F::smem_table) { // a fresh table per channel: zero tags are never current
-      for (u32 i = threadIdx.x; i < P.table_cap; i += BLOCK) sh_table[i] = make_uint4(0, 0, 0, 0);
+      for (u32 i = threadIdx.x; i < part; i += BLOCK) sh_table[i] = make_uint4(0, 0, 0, 0);
     }
     if (threadIdx.x == 0) {
       if (F::smem_table) C.vals = reinterpret_cast<u64 *>(sh_table);
-      sh.error = 0;
-      sh.rec_n = cs->rec_phys;
-      sh.rec_logical = (unsigned long long)cs->info.store_len;
-      sh.cnt_tok = sh.cnt_emit = sh.cnt_eps = 0;
-      sh.n_new = sh.n_app = sh.n_cand = sh.flog_n = 0;
+      if constexpr (CLU > 1) { // the leader's counters and every CTA's table part / Shared, over DSMEM
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        sh.lead = cl.map_shared_rank(&sh.cnt, 0);
+        for (int r = 0; r < CLU; ++r) {
+          C.peer_vals[r] = reinterpret_cast<u64 *>(cl.map_shared_rank(sh_table, r));
+          C.peer_sh[r] = cl.map_shared_rank(&sh, r);
+        }
+      }
+    }
+    if (chan_t0<F>()) {
+      Counters &G = sh.cnt;
+      G.error = 0;
+      G.rec_n = cs->rec_phys;
+      G.rec_logical = (unsigned long long)cs->info.store_len;
+      G.cnt_tok = G.cnt_emit = G.cnt_eps = 0;
+      G.n_new = G.n_app = G.n_cand = G.flog_n = 0;
 #ifdef AB_PROFILE
       for (int q = 0; q < PF_N; ++q) sh.prof[q] = 0;
       sh.prof_t = clock64();
 #endif
     }
-    __syncthreads();
+    csync<F>();
     const int T = P.frames[b];
     const S *scores = reinterpret_cast<const S *>(P.scores) + P.score_off[b];
     int n_out = 0;
-    if (P.mode == AB_MODE_STREAM && cs->info.status == AB_FINISHED) {
-      __syncthreads();
-      if (threadIdx.x == 0) cs->info.status = AB_IDLE; // decoder.py:488-489
-    }
-    __syncthreads();
+    const bool was_finished = P.mode == AB_MODE_STREAM && cs->info.status == AB_FINISHED;
+    csync<F>();
+    if (was_finished && chan_t0<F>()) cs->info.status = AB_IDLE; // decoder.py:488-489
+    csync<F>();
     int t = 0;
     for (; t < T; ++t) {
       if (P.mode == AB_MODE_STREAM) {
@@ -2380,7 +2542,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
         const long long bound =
             min((long long)(cs->info.fresh ? E : cs->max_depth) + 2 + E, (long long)P.path_cap);
         if (P.words_used[b] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
-          if (t == 0 && threadIdx.x == 0) set_error(sh, E_CAP); // no progress possible
+          if (t == 0 && chan_t0<F>()) set_error<F>(sh, E_CAP); // no progress possible
           break;
         }
       }
@@ -2405,24 +2567,29 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
         sh.next_row = (row_in_smem && t + 1 < T && ((P.L * sizeof(S)) & 15) == 0 &&
                        (reinterpret_cast<size_t>(nrow) & 15) == 0) ? nrow : nullptr;
       }
-      __syncthreads();
+      csync<F>();
       PROF_MARK(sh, PF_ROW);
       advance<BLOCK>(P, C, sh);
-      if (sh.error) break;
+      if (GC<F>(sh).error) break;
       if (P.mode == AB_MODE_STREAM) {
+        // hypotheses: the leader CTA alone (every CTA counts them)
         if (cs->info.frame_index % P.partial_every == 0) {
-          partial<BLOCK>(P, C, sh, n_out++);
-          if (sh.error) break;
+          if (lead) partial<BLOCK>(P, C, sh, n_out);
+          ++n_out;
+          csync<F>();
+          if (GC<F>(sh).error) break;
         }
         if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
-          __syncthreads();
-          if (threadIdx.x == 0) cs->info.status = AB_ENDPOINTED;
-          __syncthreads();
-          finalize<BLOCK>(P, C, sh, n_out++);
-          if (sh.error) break;
+          csync<F>();
+          if (chan_t0<F>()) cs->info.status = AB_ENDPOINTED;
+          csync<F>();
+          if (lead) finalize<BLOCK>(P, C, sh, n_out);
+          ++n_out;
+          csync<F>();
+          if (GC<F>(sh).error) break;
         }
       }
-      __syncthreads();
+      csync<F>();
       PROF_MARK(sh, PF_HYP);
     }
     if (sh.row_pending) { // a prefetched row nobody will read: let it land before the buffer is reused
@@ -2433,29 +2600,35 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
         sh.row_phase ^= 1u;
       }
     }
-    __syncthreads();
+    csync<F>();
     const bool done = t == T;
-    if (P.mode == AB_MODE_STREAM && !sh.error && done && P.final_chunk) {
+    if (P.mode == AB_MODE_STREAM && !GC<F>(sh).error && done && P.final_chunk) {
       // decoder.py:498-501: final hypothesis if frames were consumed or the stream is empty
-      if (cs->info.frame_index > 0 || P.stream_frames[b] == 0) finalize<BLOCK>(P, C, sh, n_out++);
-      __syncthreads();
-      if (!sh.error && threadIdx.x == 0) cs->info.status = AB_FINISHED;
+      const bool fin = cs->info.frame_index > 0 || P.stream_frames[b] == 0;
+      csync<F>();
+      if (fin) {
+        if (lead) finalize<BLOCK>(P, C, sh, n_out);
+        ++n_out;
+      }
+      csync<F>();
+      if (!GC<F>(sh).error && chan_t0<F>()) cs->info.status = AB_FINISHED;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      cs->rec_phys = sh.rec_n;
-      cs->info.store_len = (long long)sh.rec_logical;
-      cs->info.tok_expansions += sh.cnt_tok;
-      cs->info.emit_arcs += sh.cnt_emit;
-      cs->info.eps_arcs += sh.cnt_eps;
-      cs->info.error = sh.error;
+    csync<F>();
+    if (chan_t0<F>()) {
+      cs->rec_phys = GC<F>(sh).rec_n;
+      cs->info.store_len = (long long)GC<F>(sh).rec_logical;
+      cs->info.tok_expansions += GC<F>(sh).cnt_tok;
+      cs->info.emit_arcs += GC<F>(sh).cnt_emit;
+      cs->info.eps_arcs += GC<F>(sh).cnt_eps;
+      cs->info.error = GC<F>(sh).error;
       P.n_hyps[b] = n_out;
-      P.errors[b] = sh.error;
+      P.errors[b] = GC<F>(sh).error;
       P.frames_done[b] = t;
 #ifdef AB_PROFILE
       for (int q = 0; q < PF_N; ++q) atomicAdd(&P.prof[q], sh.prof[q]);
 #endif
     }
+    csync<F>(); // no CTA of the cluster reuses its shared memory while a peer may still read it
   }
 }
 
@@ -2469,19 +2642,19 @@ __global__ void __launch_bounds__(BLOCK) hyp_kernel(const __grid_constant__ Deco
   __shared__ Chan<F, S> C;
   setup_channel<BLOCK>(C, P, (int)blockIdx.x, sh_row, sh_ctx);
   if (threadIdx.x == 0) {
-    sh.error = 0;
-    sh.rec_n = C.cs->rec_phys;
-    sh.rec_logical = (unsigned long long)C.cs->info.store_len;
+    GC<F>(sh).error = 0;
+    GC<F>(sh).rec_n = C.cs->rec_phys;
+    GC<F>(sh).rec_logical = (unsigned long long)C.cs->info.store_len;
   }
   __syncthreads();
   if (which == AB_PARTIAL) partial<BLOCK>(P, C, sh, 0);
   else finalize<BLOCK>(P, C, sh, 0);
   __syncthreads();
   if (threadIdx.x == 0) {
-    C.cs->rec_phys = sh.rec_n;
-    C.cs->info.store_len = (long long)sh.rec_logical;
-    P.n_hyps[C.b] = sh.error ? 0 : 1;
-    P.errors[C.b] = sh.error;
+    C.cs->rec_phys = GC<F>(sh).rec_n;
+    C.cs->info.store_len = (long long)GC<F>(sh).rec_logical;
+    P.n_hyps[C.b] = GC<F>(sh).error ? 0 : 1;
+    P.errors[C.b] = GC<F>(sh).error;
   }
 }
 
