@@ -671,14 +671,17 @@ enum {
 // memory; a channel decoded by a thread-block cluster (Fmt::cluster > 1, C1 /
 // C2) keeps them in the leader CTA's, reached over DSMEM (GC()).
 struct Counters {
-  u32 n_new, n_app, n_cand, rec_n, flog_n;
+  // n_app / n_cand / n_kill: per pass, by pass parity (Shared::rpar; always
+  // 0 with one CTA per channel): a cluster resets a pass's slot after the
+  // pass's last barrier, so a round needs two cluster barriers, not five
+  u32 n_new, n_app[2], n_cand[2], rec_n, flog_n;
   unsigned long long rec_logical;
   unsigned long long min_ck; // cheapest application of the current frame
   int error;
   int max_depth;
   unsigned long long cnt_tok, cnt_emit, cnt_eps;
   int n_rec_frame; // emission records of the frame (olabel != 0 applications)
-  u32 n_kill;      // kill queue length of the current round
+  u32 n_kill[2];   // kill queue length of the current round
   u32 eps_n;       // entries in the channel's epsilon-frontier list this frame
   u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
@@ -692,6 +695,7 @@ struct Shared {
   u32 sel;
   u32 cum;
   u32 out_base_tok, out_base_mem; // cluster prune: a tile's reserved output positions
+  u32 rpar;        // parity of the current pass (cluster: alternates; else 0)
   int shared_words;
   long long words_off;
   // scan / reduce scratch
@@ -921,8 +925,10 @@ struct RelaxAcc {
 // Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
 template <typename F, typename S>
 __device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 v) {
-  const u32 k = atomicAdd(&GC<F>(sh).n_kill, 1u);
-  if (k < P.flog_cap) C.app_list[k] = v;
+  // (a cluster's passes alternate between the two halves of the kill queue)
+  const u32 cap = F::cluster > 1 ? P.flog_cap / 2 : P.flog_cap;
+  const u32 k = atomicAdd(&GC<F>(sh).n_kill[sh.rpar], 1u);
+  if (k < cap) C.app_list[sh.rpar * cap + k] = v;
   else set_error<F>(sh, E_CAP);
 }
 
@@ -1279,7 +1285,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     __syncwarp();
   }
   if (lane == 0 && arcs_seen) {
-    atomicAdd(&GC<F>(sh).n_cand, arcs_seen);
+    atomicAdd(&GC<F>(sh).n_cand[sh.rpar], arcs_seen);
     atomicAdd(EMIT ? &GC<F>(sh).cnt_emit : &GC<F>(sh).cnt_eps, (unsigned long long)arcs_seen);
   }
   } else {
@@ -1412,14 +1418,14 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     // memory is not atomic on sm_100, bench_tools/dsmem_atomics_probe.cu)
     if (mck != ~0ull) atomicMin(&sh.cnt.min_ck, mck);
     if (n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, n_rec);
-    if (n_app) atomicAdd(&GC<F>(sh).n_app, n_app);
+    if (n_app) atomicAdd(&GC<F>(sh).n_app[sh.rpar], n_app);
     if (n_new && atomicAdd(&GC<F>(sh).n_new, n_new) + n_new > P.tok_cap) set_error<F>(sh, E_CAP);
   }
   static_assert(F::cluster == 1 || WARP_TILES, "a cluster's channel uses warp tiles");
   if (tid == 0 && crank<F>() == 0) {
     if (EMIT) GC<F>(sh).cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
     if (!WARP_TILES) {
-      GC<F>(sh).n_cand += arcs_seen;
+      GC<F>(sh).n_cand[sh.rpar] += arcs_seen;
       if (EMIT) GC<F>(sh).cnt_emit += arcs_seen;
       else GC<F>(sh).cnt_eps += arcs_seen;
     }
@@ -1430,7 +1436,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 // are not applications, superseded ones are applications but not tokens.
 template <int BLOCK, typename F, typename S>
 __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
-  const u32 n = min(GC<F>(sh).n_kill, P.flog_cap);
+  const u32 n = min(GC<F>(sh).n_kill[0], P.flog_cap);
   u32 unrec = 0;
   for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
     const u32 v = C.app_list[i];
@@ -1447,7 +1453,7 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
   if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&GC<F>(sh).n_rec_frame, unrec);
   csync<F>();
-  if (chan_t0<F>()) GC<F>(sh).n_kill = 0;
+  if (chan_t0<F>()) GC<F>(sh).n_kill[0] = 0;
   csync<F>();
 }
 
@@ -1517,8 +1523,8 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     const u32 row0 = GC<F>(sh).flog_n; // rows below were written by earlier rounds of this frame
     csync<F>();
     if (chan_t0<F>()) {
-      GC<F>(sh).n_app = 0;
-      GC<F>(sh).n_cand = 0;
+      GC<F>(sh).n_app[0] = 0;
+      GC<F>(sh).n_cand[0] = 0;
       GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
     }
     csync<F>();
@@ -1527,7 +1533,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
     PROF_COUNT(sh, PF_ROUNDS, 1);
-    const u32 n_cand = GC<F>(sh).n_cand, n_app = GC<F>(sh).n_app;
+    const u32 n_cand = GC<F>(sh).n_cand[0], n_app = GC<F>(sh).n_app[0];
     if (GC<F>(sh).error) return;
     if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
     lo = hi;
@@ -1537,6 +1543,77 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
   csync<F>();
 }
 
+
+// --- a cluster's passes: two cluster barriers per pass -----------------------
+// What a pass leaves for the next one, read by every CTA between the pass's
+// two barriers (rows, epsilon entries and counts are final after the first,
+// and nothing is reserved again before the second).
+struct PassEnd {
+  u32 row0_next; // rows so far: the next pass's first row
+  u32 n_cand, n_app, eps_n;
+};
+
+// apply_kills for a cluster: the pass's kill queue (half rpar), then the
+// pass's counts, the barrier, and the reset of the pass's counter slot (its
+// next use is two passes later, behind two more barriers).
+template <int BLOCK, typename F, typename S>
+__device__ PassEnd apply_kills_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+  const u32 p = sh.rpar;
+  const u32 half = P.flog_cap / 2;
+  Counters &G = GC<F>(sh);
+  const u32 n = min(G.n_kill[p], half);
+  const u32 *q = C.app_list + p * half;
+  u32 unrec = 0;
+  for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
+    const u32 v = q[i];
+    const u32 row = v & VROW_MASK;
+    const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    if ((v & KILL_DISP) && (old & ROW_HASOL)) unrec++; // displaced: no record (DISP read at listing)
+  }
+  unrec = __reduce_add_sync(0xFFFFFFFFu, unrec);
+  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&G.n_rec_frame, unrec);
+  PassEnd e;
+  e.row0_next = G.flog_n;
+  e.n_cand = G.n_cand[p];
+  e.n_app = G.n_app[p];
+  e.eps_n = G.eps_n;
+  csync<F>();
+  if (chan_t0<F>()) {
+    G.n_kill[p] = 0;
+    G.n_cand[p] = 0;
+    G.n_app[p] = 0;
+  }
+  if (threadIdx.x == 0) sh.rpar = p ^ 1u;
+  __syncthreads();
+  return e;
+}
+
+// _epsilon_rounds (decoder.py:250-316) for a cluster: row0 of each round is
+// passed in (read before the previous pass's last barrier).
+template <int BLOCK, typename F, typename S>
+__device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
+                                 u32 n_front, u32 row0) {
+  static_assert(disp_at_listing<BLOCK>(), "a cluster's rounds skip displaced entries at listing");
+  int rounds = 0;
+  while (true) {
+    if (!(n_front > 0 && rounds < P.max_eps)) {
+      if (n_front > 0 && chan_t0<F>()) C.cs->info.eps_truncations += 1; // while-else 314-316
+      break;
+    }
+    rounds++;
+    if (chan_t0<F>()) GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
+    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
+    csync<F>();
+    const PassEnd e = apply_kills_c<BLOCK>(P, C, sh);
+    if (GC<F>(sh).error) return;
+    if (e.n_cand == 0 || e.n_app == 0) break; // decoder.py:263-265, 285-287
+    lo = hi;
+    hi = e.eps_n;
+    n_front = e.n_app;
+    row0 = e.row0_next;
+  }
+  csync<F>();
+}
 
 // Provenance of a new token list (token i comes from frontier row rows[i]):
 // resolve_row per token into the idle half of the provenance buffer (the
@@ -1980,16 +2057,17 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.hbase = C.cs->prev_best - P.beam;
     sh.hscale = HIST_PER_BEAM / P.beam;
     sh.cnt.min_ck = ~0ull; // every CTA's own frame minimum (frame_min_ck)
+    sh.rpar = 0;
   }
   if (chan_t0<F>()) {
     C.cs->epoch = e;
     GC<F>(sh).out_tok = 0;
     GC<F>(sh).out_mem = 0;
     GC<F>(sh).n_new = 0;
-    GC<F>(sh).n_app = 0;
-    GC<F>(sh).n_cand = 0;
+    GC<F>(sh).n_app[0] = GC<F>(sh).n_app[1] = 0;
+    GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = 0;
     GC<F>(sh).flog_n = 0;
-    GC<F>(sh).n_kill = 0;
+    GC<F>(sh).n_kill[0] = GC<F>(sh).n_kill[1] = 0;
     GC<F>(sh).eps_n = 0;
     GC<F>(sh).emit_end = 0;
     GC<F>(sh).n_rec_frame = 0;
@@ -2078,7 +2156,8 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
     relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, z1, z1, 0u);
-    GC<F>(sh).n_kill = 0;
+    GC<F>(sh).n_kill[0] = 0;
+    GC<F>(sh).n_app[0] = GC<F>(sh).n_cand[0] = 0; // the closure's first round counts its own
     GC<F>(sh).emit_end = 0;
     sh.cnt.min_ck = cost_key(0.0);
   }
@@ -2108,7 +2187,13 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   csync<F>();
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
-    epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, 1u); // utterance-start closure, no prune
+    if constexpr (F::cluster > 1) { // one row (the start token) so far
+      const u32 hi0 = GC<F>(sh).eps_n;
+      csync<F>();
+      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, hi0, 1u, 1u);
+    } else {
+      epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, 1u); // utterance-start closure, no prune
+    }
     if (GC<F>(sh).error) return;
     rows_to_tokens<BLOCK>(P, C, sh);
     if (chan_t0<F>()) cs->info.fresh = 0;
@@ -2154,12 +2239,23 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     next_epoch<BLOCK>(P, C, sh);
     expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
     csync<F>();
-    apply_kills<BLOCK>(P, C, sh);
+    u32 n_app, eps_hi, row0_eps;
+    if constexpr (F::cluster > 1) {
+      const PassEnd e = apply_kills_c<BLOCK>(P, C, sh);
+      n_app = e.n_app;
+      eps_hi = e.eps_n;
+      row0_eps = e.row0_next;
+      if (chan_t0<F>()) GC<F>(sh).emit_end = e.row0_next; // read in resolve_row, behind more barriers
+    } else {
+      apply_kills<BLOCK>(P, C, sh);
+      n_app = GC<F>(sh).n_app[0];
+      eps_hi = GC<F>(sh).eps_n;
+      row0_eps = 0;
+      if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
+      csync<F>();
+    }
     PROF_MARK(sh, PF_EMIT_X);
     if (GC<F>(sh).error) return;
-    const u32 n_app = GC<F>(sh).n_app;
-    if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
-    csync<F>();
     bool ok = true;
     if (n_app == 0) {
       // no emitting arcs: every token dies (decoder.py:394-398); a filtered
@@ -2167,7 +2263,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       if (filt) ok = false;
       else if (chan_t0<F>()) cs->info.num_active = 0;
     } else {
-      epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, n_app);
+      if constexpr (F::cluster > 1) epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
+      else epsilon_rounds<BLOCK>(P, C, sh, 0u, eps_hi, n_app);
       if (GC<F>(sh).error) return;
       ok = prune<BLOCK>(P, C, sh);
     }
@@ -2484,6 +2581,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
                                         (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
   uint4 *sh_table = reinterpret_cast<uint4 *>(sh_neg + P.neg_words);
   if (threadIdx.x == 0) {
+    sh.rpar = 0;
     mbar_init(&sh.row_bar);
     sh.row_phase = 0;
     sh.row_pending = 0;
@@ -2518,7 +2616,8 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       G.rec_n = cs->rec_phys;
       G.rec_logical = (unsigned long long)cs->info.store_len;
       G.cnt_tok = G.cnt_emit = G.cnt_eps = 0;
-      G.n_new = G.n_app = G.n_cand = G.flog_n = 0;
+      G.n_new = G.flog_n = 0;
+      G.n_app[0] = G.n_app[1] = G.n_cand[0] = G.n_cand[1] = 0;
 #ifdef AB_PROFILE
       for (int q = 0; q < PF_N; ++q) sh.prof[q] = 0;
       sh.prof_t = clock64();
