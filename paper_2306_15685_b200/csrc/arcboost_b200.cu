@@ -1064,7 +1064,8 @@ static int ensure_batch(ab_decoder *d, size_t n) {
 // hint's minimum rise per frame and extra margin (decode_kernel.cuh advance()).
 struct Knobs {
   bool loaded = false;
-  double hint_min = 1.0, hint_extra = 0.25;
+  double hint_min = 1.0, hint_extra = 0.25, hint_warm = 0.0;
+  int hint_warm_frames = 0;
 };
 static Knobs &g_knobs() {
   static Knobs k;
@@ -1072,6 +1073,9 @@ static Knobs &g_knobs() {
     const char *a = getenv("AB_CUT_HINT_MIN"), *b = getenv("AB_CUT_HINT_EXTRA");
     k.hint_min = a ? atof(a) : 1.0;
     k.hint_extra = b ? atof(b) : 0.25;
+    const char *c = getenv("AB_CUT_HINT_WARM"), *d = getenv("AB_CUT_HINT_WARM_FRAMES");
+    k.hint_warm = c ? atof(c) : 0.0;
+    k.hint_warm_frames = d ? atoi(d) : 0;
     k.loaded = true;
   }
   return k;
@@ -1096,6 +1100,8 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.neg0 = g->d_neg0;
   P.hint_min = g_knobs().hint_min;
   P.hint_extra = g_knobs().hint_extra;
+  P.hint_warm = g_knobs().hint_warm;
+  P.hint_warm_frames = g_knobs().hint_warm_frames;
   P.e_arcs = g->e_arcs;
   P.x_rng = g->x_rng;
   P.x_arcs = g->x_arcs;

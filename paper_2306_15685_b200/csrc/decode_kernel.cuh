@@ -341,6 +341,10 @@ struct DecodeParams {
   // decoding; hint = previous cutoff + max(rise, hint_min) + hint_extra
   int exact;
   double slack0, hint_min, hint_extra;
+  // an utterance's first frames (token set still growing, the cutoff's rise
+  // irregular) get hint_warm more margin
+  double hint_warm;
+  int hint_warm_frames;
   int slack0_rounds;
   const u32 *neg0; // NEG_WORDS bitmap of the unbiased graph
   // dynamic shared memory layout (host: launch_smem_layout)
@@ -2227,7 +2231,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const double hint = !filt ? INFINITY
-                          : attempt == 0 ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra
+                          : attempt == 0 ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra +
+                                               (cs->info.frame_index < P.hint_warm_frames ? P.hint_warm : 0.0)
                                          : GC<F>(sh).cut_fail;
       sh.cut_hint = hint;
       sh.filtered = filt ? 1 : 0;

@@ -507,3 +507,29 @@ def test_cutoff_engages_and_changes_nothing_observable():
     for a, b in zip(res_m, res_x):
         _same(a.hypotheses, b.hypotheses)
     assert sum(ch._page.get(ch._slot).cut_redos for ch in ch_m) > 0
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4", "8"])
+def test_cluster_sizes_agree(cluster, exact, monkeypatch):
+    """A channel decoded by a thread-block cluster (table split
+    over DSMEM, counters in the leader) gives the oracle's hypotheses and,
+    with exact_counters, its len(store) - for every cluster size, with the
+    max_active cut binding and hint misses."""
+    import paper_2306_15685_b200 as ab
+    from paper_2306_15685_b200 import synth
+
+    monkeypatch.setenv("AB_CLUSTER", cluster)
+    csr = synth.benchmark_graph(10_000, 4, 2000, seed=421, f32_weights=True)
+    ctxs = {f"q{c}": synth.unigram_context(csr, 20, 40 + c, num_labels=2000, ctx_id=f"q{c}") for c in range(6)}
+    reg = ab.ContextRegistry(ctxs, graph_fingerprint="")
+    cfg = ab.DecoderConfig(beam=13.0, max_active=2500, partial_every=4, exact_counters=exact)
+    mats = [synth.channel_scores(31, c, 50, 2000) for c in range(6)]
+    chans = [ab.init_channel(f"k{c}", reg, f"q{c}", cfg) for c in range(6)]
+    res = ab.decode_batch([(ch, ab.ScoreMatrix(m)) for ch, m in zip(chans, mats)], csr, reg, cfg)
+    for c in range(6):
+        assert res[c].error is None, res[c].error
+        want, rc, info = _oracle(csr, mats[c], ctxs[f"q{c}"], cfg)
+        assert rc == 0
+        _same(res[c].hypotheses, want, f"cluster {cluster} channel {c}")
+        if exact:
+            assert chans[c].eps_truncations == info["eps_truncations"]
