@@ -13,7 +13,9 @@
  * Host input buffers are copied; the caller keeps ownership.  Device memory
  * is owned by the library.  One decoder per device; calls on one decoder must
  * be serialised by the caller (different decoders may run on different host
- * threads).  No torch types cross this boundary.
+ * threads), and so must context registration / release on one graph (the
+ * context store and its slack scratch are per graph).  No torch types cross
+ * this boundary.
  */
 #ifndef ARCBOOST_B200_H
 #define ARCBOOST_B200_H
@@ -169,7 +171,11 @@ int ab_graph_query(const ab_graph *g, int32_t *num_emitting_labels, int32_t *wei
 int ab_context_slack(const ab_graph *g, int32_t handle, double *slack, int32_t *neg_states);
 
 /* BiasingContext (biasing.py:86-117) → device context store entry.  arc_indices
-   must be strictly increasing and non-negative (indices >= num_arcs never match). */
+   must be strictly increasing and non-negative (indices >= num_arcs never match).
+   mode: AB_CTX_AUTO (LABELS when the set is exactly the arcs of some output
+   labels, LIST up to 2048 arcs, else BITSET) or a forced representation.  Also
+   computes the context's epsilon slack for the expansion-time cutoff (host,
+   from the negative epsilon arcs backwards). */
 int ab_context_register(ab_graph *g, const int64_t *arc_indices, int64_t k, double discount,
                         int32_t mode, int32_t *handle);
 /* representation the context store chose for a handle (AB_CTX_LIST/BITSET/LABELS) */

@@ -109,7 +109,9 @@ class DeviceGraph:
         return m.value
 
     def context_slack(self, handle: int) -> tuple[float, int]:
-        """(epsilon slack, states flagged in its bitmap) of a context (-1: unbiased)."""
+        """(epsilon slack, set bits of its Bloom filter of slack states) of a
+        context (-1: unbiased); the count is negative when the slack bounds
+        paths of at most 64 epsilon arcs only (ab_context_slack)."""
         v = C.c_double()
         n = C.c_int32()
         check(_lib.load().ab_context_slack(self.handle, int(handle), C.byref(v), C.byref(n)))
