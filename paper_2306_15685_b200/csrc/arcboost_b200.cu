@@ -912,6 +912,7 @@ __global__ void scatter_infos(int n, const int *slots, ChanState *chans,
       chans[slots[i]].rec_phys = 0;
       chans[slots[i]].prev_cut = INFINITY;
       chans[slots[i]].cut_rise = 0.0;
+      chans[slots[i]].best_tok = -1;
     }
   }
 }

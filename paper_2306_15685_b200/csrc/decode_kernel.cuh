@@ -275,6 +275,7 @@ struct ChanState {
   double prev_best; // best token cost of the previous frame (cost histogram window)
   double prev_cut;  // the previous frame's pruning cutoff (inf: none yet), see advance()
   double cut_rise;  // recent rise of the cutoff per frame (decaying maximum)
+  int best_tok;     // token-list index of the best (cost, state) token from prune, -1 = unknown
 };
 
 struct DevHyp {
@@ -1629,6 +1630,7 @@ __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared
   if (chan_t0<F>()) {
     GC<F>(sh).max_depth = 0;
     GC<F>(sh).best_last_il = 0;
+    C.cs->best_tok = -1;
   }
   csync<F>();
   int md = 0;
@@ -1637,7 +1639,10 @@ __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared
     const TokInfo t = resolve_row(P, C, sh, r, C.tok_info);
     md = max(md, t.depth);
     C.tok_info_alt[i] = t;
-    if ((int)r == best_row) GC<F>(sh).best_last_il = t.last_il;
+    if ((int)r == best_row) {
+      GC<F>(sh).best_last_il = t.last_il;
+      C.cs->best_tok = (int)i; // partial() reads it instead of another pass over the tokens
+    }
   }
   md = __reduce_max_sync(0xFFFFFFFFu, md);
   if ((threadIdx.x & 31) == 0) atomicMax(&GC<F>(sh).max_depth, md);
@@ -2359,15 +2364,19 @@ __device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int ou
     __syncthreads();
     return;
   }
-  u64 bk = ~0ull;
-  u32 bs = 0xFFFFFFFFu;
-  int bi = -1;
-  for (u32 i = threadIdx.x; i < n; i += BLOCK) {
-    const u64 k = cost_key(C.tok_cost[i]);
-    const u32 s = C.tok_state[i];
-    if (k < bk || (k == bk && s < bs)) bk = k, bs = s, bi = (int)i;
+  // the best (cost, state) token: prune found it (best_tok), else one pass
+  int bi = cs->best_tok;
+  if (bi < 0 || (u32)bi >= n) {
+    u64 bk = ~0ull;
+    u32 bs = 0xFFFFFFFFu;
+    bi = -1;
+    for (u32 i = threadIdx.x; i < n; i += BLOCK) {
+      const u64 k = cost_key(C.tok_cost[i]);
+      const u32 s = C.tok_state[i];
+      if (k < bk || (k == bk && s < bs)) bk = k, bs = s, bi = (int)i;
+    }
+    block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   }
-  block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   const TokInfo t = C.tok_info[bi];
   emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, C.tok_cost[bi], t.bp, t.depth, t.hits);
 }
