@@ -67,7 +67,6 @@ constexpr u32 AUX_BOOST = 0x80000000u;
 constexpr u32 AUX_HASOL = 0x40000000u;
 constexpr u32 AUX_START = 0x20000000u; // the utterance-start row (no source arc)
 constexpr u32 AUX_SRC = 0x1FFFFFFFu;
-constexpr u32 NO_EPS = 0xFFFFFFFFu;    // aux.y of a row that is not in the epsilon-frontier list
 __device__ __forceinline__ u32 aux_src(u32 src, u32 rflags, u32 g) {
   return src | ((rflags & ROW_BOOST) ? AUX_BOOST : 0u) | ((rflags & ROW_HASOL) ? AUX_HASOL : 0u) |
          (g == G_START ? AUX_START : 0u);
@@ -108,14 +107,32 @@ constexpr u32 DEG_OVF = 15;                   // degree nibble: arcs live in the
 // pass: with many channels per SM (256-thread CTAs, DRAM-bound) they are
 // stored evict-first so L2 keeps the token-table lines between load and CAS;
 // a 1024-thread CTA (few channels, L2-resident working set) stores normally.
-// How a displaced row leaves the next round's epsilon frontier: 1024-thread
-// CTAs (L2-resident rows) check the row's DISP flag when the round lists its
-// entries; smaller CTAs (rows evicted to DRAM by then) mark the entry when the
-// kill is applied, so listing needs no second read.
-template <int BLOCK> __host__ __device__ constexpr bool disp_at_listing() { return BLOCK >= 1024; }
+// A displaced row leaves the next round's epsilon frontier through its own
+// DISP flag, read when the round lists its entries (the entry is not marked
+// at kill time, so rows carry no epsilon-list position).
 template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T v) {
   if (BLOCK <= 256) __stcs(p, v);
   else *p = v;
+}
+// A frontier row's aux word {source | AUX flags, olabel, ilabel}: 8 bytes
+// (labels packed 16:16) with 16-bit labels, else 16 (F::aux8); the pool is
+// sized for 16 per row either way.
+template <int BLOCK, typename F> __device__ __forceinline__ void store_aux(uint4 *aux, u32 row, u32 x, u32 ol, u32 il) {
+  if constexpr (F::aux8) st_row<BLOCK>(reinterpret_cast<uint2 *>(aux) + row, make_uint2(x, (ol << 16) | il));
+  else st_row<BLOCK>(aux + row, make_uint4(x, 0u, ol, il));
+}
+template <typename F> __device__ __forceinline__ void load_aux(const uint4 *aux, u32 row, u32 &x, u32 &ol, u32 &il) {
+  if constexpr (F::aux8) {
+    const uint2 a = reinterpret_cast<const uint2 *>(aux)[row];
+    x = a.x;
+    ol = a.y >> 16;
+    il = a.y & 0xFFFFu;
+  } else {
+    const uint4 a = aux[row];
+    x = a.x;
+    ol = a.z;
+    il = a.w;
+  }
 }
 #ifndef AB_EXP_Q1024
 #define AB_EXP_Q1024 1 // 1024-thread CTAs: 32-input warp sub-tiles
@@ -204,6 +221,7 @@ template <bool H, bool SMT = false> struct Fmt16 {
   static constexpr bool hashed = H; // token table: hashed (true) or identity-mapped
   static constexpr bool smem_table = SMT; // identity-mapped table in shared memory (small graphs)
   static constexpr int cluster = 1;       // CTAs per channel
+  static constexpr bool aux8 = true;      // 8-byte frontier-row aux (16-bit labels)
   typedef EArc16 E;
   typedef XArc16 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -228,6 +246,7 @@ template <bool H> struct Fmt24 {
   static constexpr bool hashed = H;
   static constexpr bool smem_table = false;
   static constexpr int cluster = 1;
+  static constexpr bool aux8 = false;
   typedef EArc24 E;
   typedef XArc24 X;
   static __device__ __forceinline__ void emit(const void *base, u32 a, u32 &ns, u32 &g, double &w,
@@ -315,7 +334,7 @@ struct DecodeParams {
   u32 tok_cap;
   u32 *flog_state;
   u64 *flog_ck;
-  uint4 *flog_aux; // {source | AUX flags, epsilon-list position, olabel, ilabel} per frontier row
+  uint4 *flog_aux; // {source | AUX flags, olabel, ilabel} per frontier row (store_aux)
   uint4 *eps_list; // [channel][flog_cap] {row, state | flags, cost key}: rows whose state has
                    // epsilon arcs, in write order (the next round's frontier)
   u32 flog_cap;
@@ -959,15 +978,14 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
 
 // CAS retry loop after a lost race; the candidate's row is `row`.  A
 // candidate that stops being better marks its own row displaced.
-template <bool MARK_EPS, typename F, typename S>
+template <typename F, typename S>
 __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc, u64 *v,
                             u64 ck, u32 g, u32 info, u32 row0, u64 vck, u32 vg, u32 vinfo, u32 row,
-                            u32 eps_pos, bool hasol) {
+                            bool hasol) {
   const u32 etag = C.etag;
   while (true) {
     if (!value_better(ck, g, row0, etag, vck, vg, vinfo)) {
       atomicOr(&C.flog_state[row], ROW_DISP);
-      if (MARK_EPS && eps_pos != NO_EPS) atomicOr(&C.eps_list[eps_pos].y, ROW_DISP);
       atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
       acc.n_rec -= hasol ? 1 : 0;
       return;
@@ -1013,16 +1031,15 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   }
   C.flog_state[row] = d | rflags;
   C.flog_ck[row] = ck;
-  u32 epos = NO_EPS;
   if (rflags & ROW_EPS) {
-    epos = atomicAdd(&GC<F>(sh).eps_n, 1u);
+    const u32 epos = atomicAdd(&GC<F>(sh).eps_n, 1u);
     C.eps_list[epos] = make_uint4(row, d | rflags, (u32)ck, (u32)(ck >> 32));
   }
-  C.flog_aux[row] = make_uint4(aux_src(src, rflags, g), epos, lab_ol, lab_il);
+  store_aux<1024, F>(C.flog_aux, row, aux_src(src, rflags, g), lab_ol, lab_il);
   atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
   acc.n_rec += (rflags & ROW_HASOL) ? 1 : 0;
   const u32 info = (C.etag << TAG_SHIFT) | row;
-  relax_retry<true>(P, C, sh, acc, val_at(C, slot), ck, g, info, row0, vck, vg, vinfo, row, epos,
+  relax_retry(P, C, sh, acc, val_at(C, slot), ck, g, info, row0, vck, vg, vinfo, row,
               (rflags & ROW_HASOL) != 0);
 }
 
@@ -1086,7 +1103,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     set_error<F>(sh, E_CAP);
     return;
   }
-  u32 rows[U], ninfo[U], eps_pos[U];
+  u32 rows[U], ninfo[U];
   u32 ne = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
@@ -1095,16 +1112,14 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
     ninfo[u] = 0;
-    eps_pos[u] = NO_EPS;
     if (!want[u]) continue;
     rows[u] = row++;
     if (rflags[u] & ROW_EPS) { // next round's epsilon frontier
-      eps_pos[u] = ep_at++;
-      st_row<BLOCK>(&C.eps_list[eps_pos[u]], make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32)));
+      st_row<BLOCK>(&C.eps_list[ep_at++], make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32)));
     }
     st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | rflags[u]);
     st_row<BLOCK>(&C.flog_ck[rows[u]], (unsigned long long)ck[u]);
-    st_row<BLOCK>(&C.flog_aux[rows[u]], make_uint4(aux_src(src[u], rflags[u], g[u]), eps_pos[u], ol[u], il[u]));
+    store_aux<BLOCK, F>(C.flog_aux, rows[u], aux_src(src[u], rflags[u], g[u]), ol[u], il[u]);
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
     acc.n_rec += (rflags[u] & ROW_HASOL) ? 1 : 0;
     ninfo[u] = (etag << TAG_SHIFT) | rows[u];
@@ -1121,8 +1136,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     if (r0[u] == vck[u] && r1[u] == (((u64)vinfo[u] << 32) | vg[u]))
       installed(P, C, sh, acc, row0, etag, vinfo[u], vck[u], ck[u]);
     else
-      relax_retry<!disp_at_listing<BLOCK>()>(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], row0, r0[u], (u32)r1[u],
-                  (u32)(r1[u] >> 32), rows[u], eps_pos[u], (rflags[u] & ROW_HASOL) != 0);
+      relax_retry(P, C, sh, acc, val_at(C, slot[u]), ck[u], g[u], ninfo[u], row0, r0[u], (u32)r1[u],
+                  (u32)(r1[u] >> 32), rows[u], (rflags[u] & ROW_HASOL) != 0);
   }
 }
 
@@ -1144,7 +1159,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
   // with other channels, which hide the tile barrier (CTA-wide tiles)
   constexpr bool WARP_TILES = AB_WARP_TILES_MIN_BLOCK > 0 && BLOCK >= AB_WARP_TILES_MIN_BLOCK;
-  constexpr bool DISP_AT_LISTING = disp_at_listing<BLOCK>();
+  constexpr bool DISP_AT_LISTING = true; // displaced rows leave the epsilon frontier at listing
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
   u32 *t_src = C.t_src;
@@ -1449,10 +1464,6 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
     const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
     if (v & KILL_DISP) { // a displaced row is no application (no record) and leaves the epsilon frontier
       if (old & ROW_HASOL) unrec++;
-      if (!disp_at_listing<BLOCK>()) {
-        const u32 ep = C.flog_aux[row].y;
-        if (ep != NO_EPS) atomicOr(&C.eps_list[ep].y, ROW_DISP);
-      }
     }
   }
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
@@ -1481,10 +1492,11 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   u32 pend_ol = 0, il = 0;
   u32 cur = row;
   while (true) {
-    const uint4 ax = C.flog_aux[cur];
-    if (ax.x & AUX_START) break;
-    hits += (ax.x & AUX_BOOST) ? 1 : 0;
-    if (ax.x & AUX_HASOL) {
+    u32 ax_x, ax_ol, ax_il;
+    load_aux<F>(C.flog_aux, cur, ax_x, ax_ol, ax_il);
+    if (ax_x & AUX_START) break;
+    hits += (ax_x & AUX_BOOST) ? 1 : 0;
+    if (ax_x & AUX_HASOL) {
       const u32 r = atomicAdd(&GC<F>(sh).rec_n, 1u);
       if (r >= P.arena_cap) {
         set_error<F>(sh, E_CAP);
@@ -1493,15 +1505,15 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
       if (pend >= 0) C.arena[pend] = make_int2((int)pend_ol, (int)r); // r is the older record
       else newest = (int)r;
       pend = (int)r;
-      pend_ol = ax.z;
+      pend_ol = ax_ol;
       ++nrec;
     }
     if (cur < emit_end) {
-      il = ax.w;
-      base = prev_tok[ax.x & AUX_SRC];
+      il = ax_il;
+      base = prev_tok[ax_x & AUX_SRC];
       break;
     }
-    cur = ax.x & AUX_SRC;
+    cur = ax_x & AUX_SRC;
   }
   if (pend >= 0) C.arena[pend] = make_int2((int)pend_ol, base.bp);
   TokInfo t;
@@ -1598,7 +1610,6 @@ __device__ PassEnd apply_kills_c(const DecodeParams &P, const Chan<F, S> &C, Sha
 template <int BLOCK, typename F, typename S>
 __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
                                  u32 n_front, u32 row0) {
-  static_assert(disp_at_listing<BLOCK>(), "a cluster's rounds skip displaced entries at listing");
   int rounds = 0;
   while (true) {
     if (!(n_front > 0 && rounds < P.max_eps)) {
