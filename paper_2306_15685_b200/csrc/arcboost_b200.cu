@@ -301,19 +301,26 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   g->e_tot = e_tot;
   g->x_tot = x_tot;
   g->arc_pos.resize(num_arcs);
+  // a record's next-state word carries the destination's degree codes
+  // (decode_kernel.cuh CODE_SHIFT): the kernel never loads the degree array
+  auto codes = [&](int t) -> u32 {
+    const u32 e = (u32)(deg[t] & 15u), x = (u32)(deg[t] >> 4);
+    return ((e == DEG_OVF ? ECODE_OVF : e) | ((x == DEG_OVF ? XCODE_OVF : x) << 3)) << CODE_SHIFT;
+  };
   for (int s = 0; s < num_states; ++s) {
     u32 pe = e_beg[s], px = x_beg[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
       const int dst = next_states[a];
       const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
+      const u32 nsw = (u32)dst | codes(dst);
       if (ilabels[a] != 0) {
         const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
         if (f16) {
-          EArc16 r{(u32)next_states[a], ga, (float)weights[a],
+          EArc16 r{nsw, ga, (float)weights[a],
                    (u32)ilabels[a] | ((u32)olabels[a] << 16)};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         } else {
-          EArc24 r{(u32)next_states[a], ga, (u32)ilabels[a], (u32)olabels[a], weights[a]};
+          EArc24 r{nsw, ga, (u32)ilabels[a], (u32)olabels[a], weights[a]};
           memcpy(&eh[(size_t)pe * esz], &r, esz);
         }
         g->arc_pos[a] = pe;
@@ -321,10 +328,10 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
       } else {
         const u32 ga = (u32)a | (dst_eps ? G_DEST_EPS : 0u);
         if (f16) {
-          XArc16 r{(u32)next_states[a], ga, (float)weights[a], (u32)olabels[a]};
+          XArc16 r{nsw, ga, (float)weights[a], (u32)olabels[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         } else {
-          XArc24 r{(u32)next_states[a], ga, (u32)olabels[a], 0u, weights[a]};
+          XArc24 r{nsw, ga, (u32)olabels[a], 0u, weights[a]};
           memcpy(&xh[(size_t)px * xsz], &r, xsz);
         }
         g->arc_pos[a] = px | 0x80000000u;
@@ -1004,7 +1011,10 @@ extern "C" int ab_channel_tokens(ab_decoder *d, int32_t ch, int32_t *states, dou
   int m = std::min(cap, info.num_active);
   if (m <= 0) return AB_OK;
   const size_t base = (size_t)ch * d->tok_cap;
-  if (states) CK(cudaMemcpy(states, d->tok_state + base, m * sizeof(u32), cudaMemcpyDeviceToHost));
+  if (states) {
+    CK(cudaMemcpy(states, d->tok_state + base, m * sizeof(u32), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) states[i] &= (int32_t)ROW_STATE; // the device word keeps degree codes
+  }
   if (costs) CK(cudaMemcpy(costs, d->tok_cost + base, m * sizeof(double), cudaMemcpyDeviceToHost));
   if (hits || bps) {
     ChanState cs;

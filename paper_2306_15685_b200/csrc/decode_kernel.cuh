@@ -61,6 +61,17 @@ constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
 constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
 constexpr u32 ROW_HASOL = 0x08000000u; // the winning arc has an output label (an emission record)
 constexpr u32 ROW_STATE = 0x07FFFFFFu;
+// Out-degree codes travel with a state (no per-expansion degree load): an arc
+// record's next-state word is dest | ecode << 27 | xcode << 30 (ecode =
+// emitting arcs 0..4, 7 = overflow; xcode = epsilon arcs 0..2, 3 = overflow);
+// a frontier row's and a token's state word keep the ecode (bits 27-29, the
+// row's DISP / DEAD flags are bits 30 / 31), an epsilon-frontier entry's the
+// xcode (bits 27-28).
+constexpr u32 CODE_SHIFT = 27;
+constexpr u32 ECODE_MASK = 7u << CODE_SHIFT;
+constexpr u32 ECODE_OVF = 7, XCODE_OVF = 3;
+__device__ __forceinline__ u32 ecode_of(u32 dc) { return dc & 7u; }  // dc = record word >> 27
+__device__ __forceinline__ u32 xcode_of(u32 dc) { return dc >> 3; }
 // frontier row aux word {source | AUX_BOOST | AUX_HASOL, arc id}: the
 // provenance walk reads one 8-byte word per step
 constexpr u32 AUX_BOOST = 0x80000000u;
@@ -120,6 +131,13 @@ template <int BLOCK, typename T> __device__ __forceinline__ void st_row(T *p, T 
 template <int BLOCK, typename F> __device__ __forceinline__ void store_aux(uint4 *aux, u32 row, u32 x, u32 ol, u32 il) {
   if constexpr (F::aux8) st_row<BLOCK>(reinterpret_cast<uint2 *>(aux) + row, make_uint2(x, (ol << 16) | il));
   else st_row<BLOCK>(aux + row, make_uint4(x, 0u, ol, il));
+}
+template <typename F> __device__ __forceinline__ void load_aux(const uint4 *aux, u32 row, u32 &x, u32 &ol, u32 &il);
+// whether a frontier row's arc has an output label (an emission record)
+template <typename F, typename C_> __device__ __forceinline__ bool row_hasol(const C_ &C, u32 row) {
+  u32 x, ol, il;
+  load_aux<F>(C.flog_aux, row, x, ol, il);
+  return (x & AUX_HASOL) != 0;
 }
 template <typename F> __device__ __forceinline__ void load_aux(const uint4 *aux, u32 row, u32 &x, u32 &ol, u32 &il) {
   if constexpr (F::aux8) {
@@ -470,28 +488,13 @@ __device__ __forceinline__ bool cas_value(u64 *v, u64 &ck, u32 &g, u32 &info, u6
   return ok;
 }
 
-// Degree byte of a state (a 5 MB array read for every expanded state): loaded
-// with an L2 evict_last policy so it stays resident next to the streams of
-// per-channel rows and token-table lines that flow through L2.
-#ifndef AB_DEG_KEEP
-#define AB_DEG_KEEP 1
-#endif
-__device__ __forceinline__ u64 l2_keep_policy() {
-  u64 pol = 0;
-#if AB_DEG_KEEP
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#endif
-  return pol;
-}
-__device__ __forceinline__ u32 ld_deg(const unsigned char *p, u64 pol) {
-#if AB_DEG_KEEP
-  u32 v;
-  asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-#else
-  (void)pol;
-  return __ldg(p);
-#endif
+// A state's degree codes (record-word bits >> 27: ecode | xcode << 3) from
+// the degree array, for the utterance-start token (every other state gets
+// them from the arc record that reaches it).
+__device__ __forceinline__ u32 state_codes(const DecodeParams &P, u32 s) {
+  const u32 dg = __ldg(&P.deg[s]);
+  const u32 e = dg & 15u, x = dg >> 4;
+  return (e == DEG_OVF ? ECODE_OVF : e) | ((x == DEG_OVF ? XCODE_OVF : x) << 3);
 }
 
 // L2 prefetch: memory-level parallelism that costs no registers
@@ -1003,7 +1006,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
 // belongs to another state).  (key, vck, vg, vinfo) = contents of `slot`.
 template <typename F, typename S>
 __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
-                                         u32 d, u64 ck, u32 g, u32 src, u32 rflags, u32 lab_ol, u32 lab_il,
+                                         u32 d, u32 dc, u64 ck, u32 g, u32 src, u32 rflags, u32 lab_ol, u32 lab_il,
                                          u32 row0, u32 slot, u64 key, u64 vck, u32 vg, u32 vinfo) {
   const u64 ep = (u64)C.epoch << 32;
   u32 probes = 0;
@@ -1029,11 +1032,11 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     set_error<F>(sh, E_CAP);
     return;
   }
-  C.flog_state[row] = d | rflags;
+  C.flog_state[row] = d | (ecode_of(dc) << CODE_SHIFT);
   C.flog_ck[row] = ck;
   if (rflags & ROW_EPS) {
     const u32 epos = atomicAdd(&GC<F>(sh).eps_n, 1u);
-    C.eps_list[epos] = make_uint4(row, d | rflags, (u32)ck, (u32)(ck >> 32));
+    C.eps_list[epos] = make_uint4(row, d | (xcode_of(dc) << CODE_SHIFT), (u32)ck, (u32)(ck >> 32));
   }
   store_aux<1024, F>(C.flog_aux, row, aux_src(src, rflags, g), lab_ol, lab_il);
   atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
@@ -1049,7 +1052,8 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
 // and probe chains fall back to the sequential path.
 template <int BLOCK, int U, typename F, typename S>
 __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
-                                            const bool (&on)[U], const u32 (&d)[U], const u64 (&ck)[U],
+                                            const bool (&on)[U], const u32 (&d)[U], const u32 (&dc)[U],
+                                            const u64 (&ck)[U],
                                             const u32 (&g)[U], const u32 (&src)[U], const u32 (&rflags)[U],
                                             const u32 (&ol)[U], const u32 (&il)[U], u32 row0) {
   const u32 etag = C.etag;
@@ -1084,8 +1088,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (on[u] && !fast[u])
-        relax_probe<F, S>(P, C, sh, acc, d[u], ck[u], g[u], src[u], rflags[u], ol[u], il[u], row0, slot[u],
-                          key[u], vck[u], vg[u], vinfo[u]);
+        relax_probe<F, S>(P, C, sh, acc, d[u], dc[u], ck[u], g[u], src[u], rflags[u], ol[u], il[u], row0,
+                          slot[u], key[u], vck[u], vg[u], vinfo[u]);
   } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) fast[u] = on[u];
@@ -1115,9 +1119,10 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     if (!want[u]) continue;
     rows[u] = row++;
     if (rflags[u] & ROW_EPS) { // next round's epsilon frontier
-      st_row<BLOCK>(&C.eps_list[ep_at++], make_uint4(rows[u], d[u] | rflags[u], (u32)ck[u], (u32)(ck[u] >> 32)));
+      st_row<BLOCK>(&C.eps_list[ep_at++],
+                    make_uint4(rows[u], d[u] | (xcode_of(dc[u]) << CODE_SHIFT), (u32)ck[u], (u32)(ck[u] >> 32)));
     }
-    st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | rflags[u]);
+    st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | (ecode_of(dc[u]) << CODE_SHIFT));
     st_row<BLOCK>(&C.flog_ck[rows[u]], (unsigned long long)ck[u]);
     store_aux<BLOCK, F>(C.flog_aux, rows[u], aux_src(src[u], rflags[u], g[u]), ol[u], il[u]);
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
@@ -1174,7 +1179,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   acc.n_app = 0;
   acc.n_rec = 0;
   u32 arcs_seen = 0;
-  const u64 deg_pol = l2_keep_policy();
   if constexpr (WARP_TILES) {
   // Each warp works through its own sub-tiles (32 * Q inputs; smaller when
   // the input is short, so every warp gets some): a warp-level scan of the
@@ -1220,10 +1224,9 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       cnt[q] = 0;
       // (with the DISP check at listing, the degree load does not wait for it)
       if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
-        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
-        const u32 dg = ld_deg(&P.deg[s], deg_pol);
-        const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
-        if (c == DEG_OVF) {
+        const u32 s = st[q] & ROW_STATE;
+        const u32 c = EMIT ? (st[q] >> CODE_SHIFT) & 7u : (st[q] >> CODE_SHIFT) & 3u;
+        if (c == (EMIT ? ECODE_OVF : XCODE_OVF)) {
           const uint2 r = __ldg(&rng[s]);
           a0[q] = r.x;
           cnt[q] = r.y - r.x;
@@ -1279,7 +1282,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = w_cost[lo];
         }
       }
-      u32 d[U], g[U], il[U], ol[U], bw[U];
+      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1291,6 +1294,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
+        dc[u] = d[u] >> CODE_SHIFT; // the destination's degree codes
+        d[u] &= ROW_STATE;
       }
       u64 ck[U];
       u32 rflags[U];
@@ -1300,7 +1305,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         rflags[u] = 0;
         if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
       }
-      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
     }
     __syncwarp();
   }
@@ -1349,10 +1354,9 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       cnt[q] = 0;
       // (with the DISP check at listing, the degree load does not wait for it)
       if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
-        const u32 s = EMIT ? st[q] : (st[q] & ROW_STATE);
-        const u32 dg = ld_deg(&P.deg[s], deg_pol);
-        const u32 c = EMIT ? (dg & 15u) : (dg >> 4);
-        if (c == DEG_OVF) {
+        const u32 s = st[q] & ROW_STATE;
+        const u32 c = EMIT ? (st[q] >> CODE_SHIFT) & 7u : (st[q] >> CODE_SHIFT) & 3u;
+        if (c == (EMIT ? ECODE_OVF : XCODE_OVF)) {
           const uint2 r = __ldg(&rng[s]);
           a0[q] = r.x;
           cnt[q] = r.y - r.x;
@@ -1400,7 +1404,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = t_cost[lo];
         }
       }
-      u32 d[U], g[U], il[U], ol[U], bw[U];
+      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1412,6 +1416,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
+        dc[u] = d[u] >> CODE_SHIFT; // the destination's degree codes
+        d[u] &= ROW_STATE;
       }
       u64 ck[U];
       u32 rflags[U];
@@ -1421,7 +1427,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         rflags[u] = 0;
         if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
       }
-      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, ck, g, src, rflags, ol, il, row0);
+      relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
     }
     __syncthreads();
   }
@@ -1461,10 +1467,8 @@ __device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &
   for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
     const u32 v = C.app_list[i];
     const u32 row = v & VROW_MASK;
-    const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
-    if (v & KILL_DISP) { // a displaced row is no application (no record) and leaves the epsilon frontier
-      if (old & ROW_HASOL) unrec++;
-    }
+    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    if (v & KILL_DISP) unrec += row_hasol<F>(C, row) ? 1u : 0u; // a displaced row is no application (no record)
   }
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
   if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&GC<F>(sh).n_rec_frame, unrec);
@@ -1584,8 +1588,8 @@ __device__ PassEnd apply_kills_c(const DecodeParams &P, const Chan<F, S> &C, Sha
   for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
     const u32 v = q[i];
     const u32 row = v & VROW_MASK;
-    const u32 old = atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
-    if ((v & KILL_DISP) && (old & ROW_HASOL)) unrec++; // displaced: no record (DISP read at listing)
+    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
+    if ((v & KILL_DISP) && row_hasol<F>(C, row)) unrec++; // displaced: no record (DISP read at listing)
   }
   unrec = __reduce_add_sync(0xFFFFFFFFu, unrec);
   if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&G.n_rec_frame, unrec);
@@ -1877,16 +1881,17 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     for (int q = 0; q < QP; ++q) {
       if (bq[q] > split || (bq[q] == split && ck[q] > thr_ck)) continue;
       const u32 s = st[q] & ROW_STATE;
+      const u32 sw = st[q] & (ROW_STATE | ECODE_MASK); // the token's state word keeps its ecode
       const u32 i = base + (u32)q * BLOCK + (u32)tid;
       if (ck[q] < bk || (ck[q] == bk && s < bs)) bk = ck[q], bs = s, bi = (int)i;
       if (bq[q] < split) {
-        C.tok_state[ps] = s;
+        C.tok_state[ps] = sw;
         C.tok_cost[ps] = key_cost(ck[q]);
         C.scr_row[ps] = i;
         ++ps;
       } else {
         C.scr_key[pm] = ck[q];
-        scr_state[pm] = s;
+        scr_state[pm] = sw;
         *(mem_row - 1 - pm) = i;
         ++pm;
       }
@@ -1943,7 +1948,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       if (exact) { // ties at the threshold cost: the smallest states survive
         auto sf = [&](u32 i, bool &ok) -> u64 {
           const u64 k = C.scr_key[i];
-          const u32 s = scr_state[i];
+          const u32 s = scr_state[i] & ROW_STATE;
           ok = k == tc;
           return (u64)s;
         };
@@ -1960,7 +1965,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
         k = C.scr_key[m];
         s = scr_state[m];
         r = *(mem_row - 1 - m);
-        keep = k < tc || (k == tc && s <= ts);
+        keep = k < tc || (k == tc && (s & ROW_STATE) <= ts);
       }
       u32 total;
       const u32 p = n_tok + block_excl_scan<BLOCK>(keep ? 1u : 0u, total, sh.scan);
@@ -2013,12 +2018,13 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
     const u32 i = i0 + threadIdx.x;
     const u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
     const bool live = !(st & (ROW_DEAD | ROW_DISP));
-    const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, (st & (ROW_DISP | ROW_HASOL)) == ROW_HASOL));
+    const bool rec = i < n_rows && !(st & ROW_DISP) && row_hasol<F>(C, i);
+    const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, rec));
     if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)nrec);
     u32 total;
     const u32 p = n_tok + block_excl_scan<BLOCK>(live ? 1u : 0u, total, sh.scan);
     if (live) {
-      C.tok_state[p] = st & ROW_STATE;
+      C.tok_state[p] = st & (ROW_STATE | ECODE_MASK);
       C.tok_cost[p] = key_cost(C.flog_ck[i]);
       C.scr_row[p] = i;
     }
@@ -2173,9 +2179,10 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     acc.n_new = acc.n_app = 0;
     acc.n_rec = 0;
     const bool on1[1] = {true};
-    const u32 d1[1] = {(u32)P.start}, g1[1] = {G_START}, s1[1] = {0u}, f1[1] = {ROW_EPS}, z1[1] = {0u};
+    const u32 d1[1] = {(u32)P.start}, dc1[1] = {state_codes(P, (u32)P.start)}, g1[1] = {G_START}, s1[1] = {0u},
+              f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
-    relax_batch<1>(P, C, sh, acc, on1, d1, c1, g1, s1, f1, z1, z1, 0u);
+    relax_batch<1>(P, C, sh, acc, on1, d1, dc1, c1, g1, s1, f1, z1, z1, 0u);
     GC<F>(sh).n_kill[0] = 0;
     GC<F>(sh).n_app[0] = GC<F>(sh).n_cand[0] = 0; // the closure's first round counts its own
     GC<F>(sh).emit_end = 0;
@@ -2383,7 +2390,7 @@ __device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int ou
     bi = -1;
     for (u32 i = threadIdx.x; i < n; i += BLOCK) {
       const u64 k = cost_key(C.tok_cost[i]);
-      const u32 s = C.tok_state[i];
+      const u32 s = C.tok_state[i] & ROW_STATE;
       if (k < bk || (k == bk && s < bs)) bk = k, bs = s, bi = (int)i;
     }
     block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
@@ -2412,7 +2419,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
       t.depth = 0;
       t.hits = 0;
       t.last_il = 0;
-      C.tok_state[0] = (u32)P.start;
+      C.tok_state[0] = (u32)P.start | (ecode_of(state_codes(P, (u32)P.start)) << CODE_SHIFT);
       C.tok_cost[0] = 0.0;
       C.tok_info[0] = t;
       cs->info.num_active = 1;
@@ -2431,7 +2438,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   int fi = -1, bi = -1;
   for (u32 i = threadIdx.x; i < n; i += BLOCK) {
     const double c = C.tok_cost[i];
-    const u32 s = C.tok_state[i];
+    const u32 s = C.tok_state[i] & ROW_STATE;
     const u64 k = cost_key(c);
     if (k < bk || (k == bk && s < bs)) bk = k, bs = s, bi = (int)i;
     const double fc = __ldg(&P.final_cost[s]);
@@ -2448,7 +2455,7 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   if (fi >= 0) {
     b = fi;
     fallback = 0;
-    cost = C.tok_cost[b] + __ldg(&P.final_cost[C.tok_state[b]]);
+    cost = C.tok_cost[b] + __ldg(&P.final_cost[C.tok_state[b] & ROW_STATE]);
   } else {
     b = bi;
     fallback = 1;
