@@ -3,7 +3,8 @@
 ``benchmark_graph`` reproduces the reference's ``build_benchmark_graph``
 (arcboost/synth.py:294-322) draw for draw, but returns the CSR arrays directly
 (vectorised; the reference builds Python Arc objects, which does not scale to
-2e7 arcs).  tests/test_synth_golden.py pins the arrays against the reference.
+2e7 arcs).  tests/test_cpu_host.py (test_benchmark_graph_matches_reference)
+pins the arrays against the reference's digest.
 With ``f32_weights`` the weights are rounded once to float32 so the device can
 store 4-byte weights while accumulating bit-exactly in f64; the same rounded
 arrays are what the CPU oracle sees.
