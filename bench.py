@@ -63,6 +63,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-overhead", action="store_true", help="skip the unbiased / zero-discount runs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--partial-every", type=int, default=None, help="override the workload's partial cadence")
     p.add_argument("--exact", action="store_true",
                    help="relax every candidate (exact_counters): no expansion-time cutoff")
     p.add_argument("--table-slots", type=int, default=0,
@@ -92,6 +93,8 @@ def workload(args):
         cfg["segments"] = args.segments
     if args.states:
         cfg["states"] = args.states
+    if args.partial_every:
+        cfg["partial_every"] = args.partial_every
     cfg["frames"] = args.frames
     return cfg
 
