@@ -54,13 +54,14 @@ constexpr u32 G_MASK = 0x7FFFFFFFu;
 constexpr u32 G_START = 0xFFFFFFFFu; // frontier row of the utterance-start token
 constexpr u32 MAX_TOKENS = 1u << 17;            // distinct tokens per channel-frame
 constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per channel
-// frontier row word: state | flags
+// frontier row word: state | ecode (below) | DISP | DEAD
 constexpr u32 ROW_DEAD = 0x80000000u;  // superseded by a later round (an application, not a token)
 constexpr u32 ROW_DISP = 0x40000000u;  // displaced in its own round (not an application)
+constexpr u32 ROW_STATE = 0x07FFFFFFu;
+// a candidate's flags (registers; boost / output label also go to the row's aux word)
 constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
 constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
 constexpr u32 ROW_HASOL = 0x08000000u; // the winning arc has an output label (an emission record)
-constexpr u32 ROW_STATE = 0x07FFFFFFu;
 // Out-degree codes travel with a state (no per-expansion degree load): an arc
 // record's next-state word is dest | ecode << 27 | xcode << 30 (ecode =
 // emitting arcs 0..4, 7 = overflow; xcode = epsilon arcs 0..2, 3 = overflow);
@@ -817,8 +818,8 @@ template <typename F, typename S> struct Chan {
   double slack; // the context's epsilon slack (CtxDesc::slack)
   int slack_rounds;
   double ucut0; // this attempt's candidate cutoff (candidates above it are not relaxed) ...
-  double ucut;  // ... plus the slack, for states in the neg bitmap
-  const u32 *neg; // shared-memory copy of the context's (or graph's) neg bitmap
+  double ucut;  // ... plus the slack, for states in the slack Bloom filter
+  const u32 *neg; // shared-memory copy of the context's (or graph's) slack Bloom filter
   u32 neg_fold; // log2(NEG_WORDS / the launch's filter words)
   const u32 *hq; // or the context's per-state 2-bit slack (CtxDesc::hq)
   double hq_unit;
