@@ -168,6 +168,7 @@ template <int BLOCK> __host__ __device__ constexpr int exp_q() {
   return BLOCK <= 256 ? AB_EXP_Q256 : (BLOCK >= 1024 ? AB_EXP_Q1024 : AB_EXP_Q);
 }
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
+constexpr u32 TILE_COARSE = 128; // coarse search index entries (tiles of up to 4096 arcs)
 #ifndef AB_PRUNE_Q
 #define AB_PRUNE_Q 4
 #endif
@@ -828,6 +829,7 @@ template <typename F, typename S> struct Chan {
   u32 *t_pref;
   u32 *t_src;
   double *t_cost;
+  u32 *t_coarse; // CTA tiles: owner of every 32nd arc (TILE_COARSE entries)
 };
 
 // The cheapest application of the frame: this CTA's, or the minimum over the
@@ -1370,14 +1372,20 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     }
     u32 total, pref[Q];
     block_excl_scan_q<BLOCK, Q>(cnt, pref, total, sh.scan);
+    // coarse index of the arc -> input search: the input owning arc 32 b
+    // (written by the input whose range holds it) bounds every arc of block b
+    const bool coarse = total <= 32u * TILE_COARSE;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const u32 j = (u32)q * BLOCK + (u32)tid;
       t_a0[j] = a0[q];
       t_pref[j] = pref[q];
+      if (coarse)
+        for (u32 m = (pref[q] + 31u) & ~31u; m < pref[q] + cnt[q]; m += 32u) C.t_coarse[m >> 5] = j;
     }
     if (tid == 0) t_pref[TILE] = total;
     __syncthreads();
+    const u32 nblk = (total + 31u) >> 5;
     arcs_seen += total;
     // arcs k = tid, tid + BLOCK, ...: the lanes of a warp read consecutive
     // arc records (one state's arcs are contiguous), so a warp load touches
@@ -1394,7 +1402,14 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         src[u] = 0;
         cj[u] = 0.0;
         if (on[u]) {
-          u32 lo = 0, hi = TILE - 1; // largest j with t_pref[j] <= k (its range holds k)
+          // largest j with t_pref[j] <= k (its range holds k), between the
+          // owners of the 32-arc blocks around k
+          u32 lo = 0, hi = TILE - 1;
+          if (coarse) {
+            const u32 b = k >> 5;
+            lo = C.t_coarse[b];
+            if (b + 1 < nblk) hi = C.t_coarse[b + 1];
+          }
           while (lo < hi) {
             const u32 mid = (lo + hi + 1) >> 1;
             if (t_pref[mid] <= k) lo = mid;
@@ -2488,7 +2503,8 @@ __device__ void finalize(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
 template <int BLOCK, typename F, typename S>
 __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh_row,
                               u32 *sh_ctx, u32 *t_a0 = nullptr, u32 *t_pref = nullptr,
-                              double *t_cost = nullptr, u32 *t_src = nullptr, u32 *sh_neg = nullptr) {
+                              double *t_cost = nullptr, u32 *t_src = nullptr, u32 *sh_neg = nullptr,
+                              u32 *t_coarse = nullptr) {
   const int slot = P.slots[b];
   const int h = P.chans[slot].info.context;
   __syncthreads(); // the previous channel of this CTA is done with C
@@ -2539,6 +2555,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.t_pref = t_pref;
     C.t_cost = t_cost;
     C.t_src = t_src;
+    C.t_coarse = t_coarse;
   }
   __syncthreads();
   if (h >= 0 && h < P.num_ctxs) {
@@ -2605,6 +2622,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   __shared__ u32 tile_a0[BLOCK * exp_q<BLOCK>()];
   __shared__ u32 tile_pref[BLOCK * exp_q<BLOCK>() + 1];
   __shared__ u32 tile_src[BLOCK * exp_q<BLOCK>()];
+  __shared__ u32 tile_coarse[BLOCK >= AB_WARP_TILES_MIN_BLOCK ? 1 : TILE_COARSE]; // CTA tiles only
   // dynamic: context words | score row | neg Bloom filter | (small graphs) the
   // channel's direct token table (host: launch_smem_layout, dyn_smem)
   u32 *sh_ctx = reinterpret_cast<u32 *>(dyn_smem);
@@ -2626,7 +2644,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
   const u32 part = (P.table_cap + CLU - 1) / CLU; // this CTA's share of a shared-memory table
   for (int b = blockIdx.x / CLU; b < P.n; b += gridDim.x / CLU) {
     setup_channel<BLOCK>(C, P, b, sh_row, sh_ctx, tile_a0, tile_pref, tile_cost, tile_src,
-                         P.neg_words ? sh_neg : nullptr);
+                         P.neg_words ? sh_neg : nullptr, tile_coarse);
     ChanState *cs = C.cs;
     if (F::smem_table) { // a fresh table per channel: zero tags are never current
       for (u32 i = threadIdx.x; i < part; i += BLOCK) sh_table[i] = make_uint4(0, 0, 0, 0);
