@@ -222,11 +222,12 @@ def profile_ref():
         if "dram_bytes_per_channel_frame" in k:
             out["dram_bytes_per_channel_frame"] = float(k["dram_bytes_per_channel_frame"])
             out["ncu_source"] = "profiles/ncu_current.json"
-    q = ROOT / "profiles" / "random_access_peak.json"
-    if q.exists():
+    q = ROOT / "profiles" / "r02_dram_bytes_per_random_access.json"
+    if q.exists():  # bench_tools/fetch_probe.cu: random 16-B loads over 32 GB
         r = json.loads(q.read_text())
-        out["random_read_Gsectors_s"] = r.get("read16_64GB_Gsect_s")
-        out["random_cas_Gops_s"] = r.get("cas16_64GB_Gop_s")
+        first = r["launches"][0]
+        out["random_line_ceiling_Gps"] = r["accesses_per_launch"] / (first["kernel_us"] * 1e3)
+        out["dram_bytes_per_random_load"] = first["dram_read_B_per_access"]
     return out
 
 
@@ -465,11 +466,12 @@ def run_b200(args, W, world, rank, local):
         bpcf = pref["dram_bytes_per_channel_frame"]
         traffic = bpcf * C * Tseg
         kernel_fps = C * T / (kms / 1000.0)
+        # a random access that misses L2 moves a whole 128-B line (fetch_probe)
         random_access = {"dram_bytes_per_channel_frame": bpcf,
                          "dram_GBps_at_kernel_rate": bpcf * kernel_fps / 1e9,
-                         "sectors_Gps_at_kernel_rate": bpcf * kernel_fps / 32 / 1e9,
-                         "random_read_ceiling_Gsectors_s": pref.get("random_read_Gsectors_s"),
-                         "random_cas_ceiling_Gops_s": pref.get("random_cas_Gops_s"),
+                         "lines_Gps_at_kernel_rate": bpcf * kernel_fps / 128 / 1e9,
+                         "random_line_ceiling_Gps": pref.get("random_line_ceiling_Gps"),
+                         "dram_bytes_per_random_16B_load": pref.get("dram_bytes_per_random_load"),
                          "source": pref.get("ncu_source")}
     modes = sorted({dg.context_mode(h) for h in handles})
     mode_names = {_lib.AB_CTX_LIST: "LIST", _lib.AB_CTX_BITSET: "BITSET", _lib.AB_CTX_LABELS: "LABELS"}
