@@ -1319,8 +1319,12 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   } else {
   // tile position j = q * BLOCK + tid: input base + j, so every load of the
   // tile's inputs is warp-coalesced (the degree scan runs in the same order)
+  // (the tile's shared arrays are written after the degree scan, whose
+  // barriers every thread reaches only after the previous tile's arcs: no
+  // barrier at the end of a tile)
   for (u32 base = 0; base < n_in; base += TILE) {
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
+    double cq[Q];
     if (EMIT) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -1330,11 +1334,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 #pragma unroll
       for (int q = 0; q < Q; ++q) st[q] = idx[q] == 0xFFFFFFFFu ? ROW_DISP : C.tok_state[idx[q]];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const u32 j = (u32)q * BLOCK + (u32)tid;
-        t_src[j] = idx[q];
-        if (idx[q] != 0xFFFFFFFFu) t_cost[j] = C.tok_cost[idx[q]];
-      }
+      for (int q = 0; q < Q; ++q) cq[q] = idx[q] != 0xFFFFFFFFu ? C.tok_cost[idx[q]] : 0.0;
     } else {
       // epsilon-frontier entries carry the row's state, flags and cost
 #pragma unroll
@@ -1342,13 +1342,13 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         const u32 j = (u32)q * BLOCK + (u32)tid;
         idx[q] = 0xFFFFFFFFu;
         st[q] = ROW_DISP;
+        cq[q] = 0.0;
         if (base + j < n_in) {
           const uint4 e = list[base + j];
           idx[q] = e.x;
           st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
-          t_cost[j] = key_cost(((u64)e.w << 32) | e.z);
+          cq[q] = key_cost(((u64)e.w << 32) | e.z);
         }
-        t_src[j] = idx[q];
       }
     }
 #pragma unroll
@@ -1380,6 +1380,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       const u32 j = (u32)q * BLOCK + (u32)tid;
       t_a0[j] = a0[q];
       t_pref[j] = pref[q];
+      t_src[j] = idx[q];
+      t_cost[j] = cq[q];
       if (coarse)
         for (u32 m = (pref[q] + 31u) & ~31u; m < pref[q] + cnt[q]; m += 32u) C.t_coarse[m >> 5] = j;
     }
@@ -1445,7 +1447,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
     }
-    __syncthreads();
   }
   }
   // per-warp totals first: one shared atomic per warp and counter
