@@ -1878,9 +1878,14 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       ns += (live && bq[q] < split) ? 1u : 0u;
       nm += (live && bq[q] == split && ck[q] <= thr_ck) ? 1u : 0u;
     }
-    u32 tot_s, tot_m;
-    u32 ps = block_excl_scan<BLOCK>(ns, tot_s, sh.scan);
-    u32 pm = block_excl_scan<BLOCK>(nm, tot_m, sh.scan);
+    // both counts in one scan (survivors low, split-bucket rows high half:
+    // a tile has at most BLOCK * QP of each, no carry between the halves)
+    static_assert(BLOCK * QP < 65536, "packed prune scan");
+    u32 tot_sm;
+    const u32 psm = block_excl_scan<BLOCK>(ns | (nm << 16), tot_sm, sh.scan);
+    const u32 tot_s = tot_sm & 0xFFFFu, tot_m = tot_sm >> 16;
+    u32 ps = psm & 0xFFFFu;
+    u32 pm = psm >> 16;
     if constexpr (F::cluster > 1) { // output positions reserved on the leader's counters
       if (tid == 0) {
         sh.out_base_tok = tot_s ? atomicAdd(&GC<F>(sh).out_tok, tot_s) : 0u;
