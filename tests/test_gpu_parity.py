@@ -533,3 +533,21 @@ def test_cluster_sizes_agree(cluster, exact, monkeypatch):
         _same(res[c].hypotheses, want, f"cluster {cluster} channel {c}")
         if exact:
             assert chans[c].eps_truncations == info["eps_truncations"]
+
+
+@pytest.mark.parametrize("block", ["256", "512"])
+def test_small_cases_at_bench_cta_sizes(small_cases, block, monkeypatch):
+    """The reference's small cases through the CTA-tile expansion of the
+    256 / 512-thread kernels (the bench's C3 shape; small graphs otherwise
+    run 1024-thread or cluster kernels), with the cutoff."""
+    monkeypatch.setenv("AB_BLOCK", block)
+    for c in small_cases[:250]:
+        csr, scores, ctx, cfg = case_inputs(c)
+        res, ch = _decode(csr, scores, ctx, cfg)
+        e = c["expect"]
+        if e["error"] is not None:
+            assert res.error is not None, c["name"]
+            continue
+        assert res.error is None, (c["name"], res.error)
+        got = [(h.words, h.cost, h.frame, h.kind, h.fallback) for h in res.hypotheses]
+        assert got == expect_hyps(e), c["name"]
