@@ -129,6 +129,7 @@ struct ab_decoder {
   uint4 *flog_aux = nullptr;
   uint4 *eps_list = nullptr;
   u32 *app_list = nullptr;
+  u32 *flog_kill = nullptr; // kill words of the cluster kernels (allocated with the first cluster launch)
   u64 *scr_key = nullptr;
   u32 *scr_row = nullptr;
   int2 *arena = nullptr;
@@ -820,7 +821,7 @@ extern "C" void ab_decoder_destroy(ab_decoder *d) {
   cudaSetDevice(d->device); // never touches d->g: the graph may already be gone
   void *ptrs[] = {d->chans,     d->table,     d->vals, d->tok_state, d->tok_cost, d->tok_info,
                   d->flog_state, d->flog_ck,  d->flog_aux, d->eps_list, d->app_list,
-                  d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
+                  d->flog_kill, d->scr_key,   d->scr_row,   d->arena,     d->path_rec, d->path_words,
                   d->gc_bits,   d->gc_rank,
                   d->d_slots,   d->d_frames,  d->d_sframes, d->d_nhyps,   d->d_errors, d->d_done,
                   d->d_soff,    d->d_wused,   d->d_hyps,    d->d_words,  d->d_packh,
@@ -1142,6 +1143,7 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
   P.eps_list = d->eps_list;
   P.flog_cap = d->flog_cap;
   P.app_list = d->app_list;
+  P.flog_kill = d->flog_kill;
   P.scr_key = d->scr_key;
   P.scr_row = d->scr_row;
   P.arena = d->arena;
@@ -1571,7 +1573,16 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     } else {
       const int clu = (g->fmt16 && block == 1024 && !s64) ? pick_cluster(m) : 1;
       const size_t part = ((size_t)P.table_cap + clu - 1) / clu * 16; // a cluster CTA's table share
-      if (clu > 1 && smem_table_fits<float>(smem, (size_t)P.table_cap / clu + 1))
+      const bool use_clu = clu > 1 && smem_table_fits<float>(smem, (size_t)P.table_cap / clu + 1);
+      if (use_clu && !d->flog_kill) { // kill words (zero: no valid tag) for every slot
+        size_t acc = 0;
+        const size_t nk = (size_t)d->max_ch * d->flog_cap;
+        if (dmalloc(&d->flog_kill, nk, acc) || cudaMemsetAsync(d->flog_kill, 0, nk * sizeof(u32), st) != cudaSuccess)
+          return fail(AB_ERR_CUDA, "kill-word allocation failed");
+        d->bytes += acc;
+      }
+      P.flog_kill = d->flog_kill;
+      if (use_clu)
         le = clu == 8 ? launch_decode_cluster<8>(P, m, smem + part, st)
            : clu == 4 ? launch_decode_cluster<4>(P, m, smem + part, st)
                       : launch_decode_cluster<2>(P, m, smem + part, st);

@@ -58,6 +58,15 @@ constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per 
 constexpr u32 ROW_DEAD = 0x80000000u;  // superseded by a later round (an application, not a token)
 constexpr u32 ROW_DISP = 0x40000000u;  // displaced in its own round (not an application)
 constexpr u32 ROW_STATE = 0x07FFFFFFu;
+// A cluster's rows keep DEAD / DISP in a separate kill word per row, written
+// once, by the thread whose CAS replaced the row, with the epoch tag: (tag <<
+// 2) | KW_*.  No kill queue and no pass applying it, so a cluster's pass needs
+// one barrier (the listing of the next pass reads DISP behind it; DEAD is
+// read by prune only).  Their row state words carry ROW_REC at bit 30 (the
+// row has an output label: an emission record unless displaced).
+constexpr u32 KW_DEAD = 1u, KW_DISP = 2u;
+constexpr u32 ROW_REC = 0x40000000u;
+template <typename F> __host__ __device__ constexpr bool direct_kills() { return F::cluster > 1; }
 // a candidate's flags (registers; boost / output label also go to the row's aux word)
 constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
 constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
@@ -359,6 +368,7 @@ struct DecodeParams {
                    // epsilon arcs, in write order (the next round's frontier)
   u32 flog_cap;
   u32 *app_list;
+  u32 *flog_kill; // [channel][flog_cap] kill words (cluster kernels; else null)
   u64 *scr_key;
   u32 *scr_row;
   int2 *arena;   // [channel][2][arena_cap]: live half + GC to-space
@@ -700,22 +710,24 @@ enum {
 // memory; a channel decoded by a thread-block cluster (Fmt::cluster > 1, C1 /
 // C2) keeps them in the leader CTA's, reached over DSMEM (GC()).
 struct Counters {
-  // n_app / n_cand / n_kill: per pass, by pass parity (Shared::rpar; always
-  // 0 with one CTA per channel): a cluster resets a pass's slot after the
-  // pass's last barrier, so a round needs two cluster barriers, not five
-  u32 n_new, n_app[2], n_cand[2], rec_n, flog_n;
+  // n_app / n_cand: per pass, by pass index mod 3 (Shared::rpar; always 0
+  // with one CTA per channel): a cluster reads a pass's slot after the pass's
+  // barrier and resets the slot of the pass after next, so a pass needs one
+  // cluster barrier
+  u32 n_new, n_app[3], n_cand[3], rec_n, flog_n;
   unsigned long long rec_logical;
   unsigned long long min_ck; // cheapest application of the current frame
   int error;
   int max_depth;
   unsigned long long cnt_tok, cnt_emit, cnt_eps;
   int n_rec_frame; // emission records of the frame (olabel != 0 applications)
-  u32 n_kill[2];   // kill queue length of the current round
+  u32 n_kill[1];   // kill queue length of the current round (one CTA per channel)
   u32 eps_n;       // entries in the channel's epsilon-frontier list this frame
   u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
   u32 out_tok, out_mem; // cluster prune: survivors / split-bucket rows reserved so far
+  u32 out_sel;          // cluster prune: survivors after the split-bucket selection
 };
 
 struct Shared {
@@ -724,7 +736,10 @@ struct Shared {
   u32 sel;
   u32 cum;
   u32 out_base_tok, out_base_mem; // cluster prune: a tile's reserved output positions
-  u32 rpar;        // parity of the current pass (cluster: alternates; else 0)
+  u64 xbest_k; // cluster prune: this CTA's best (cost, state) row, read by its peers
+  u32 xbest_s;
+  int xbest_i;
+  u32 rpar;        // counter slot of the current pass (cluster: pass index mod 3; else 0)
   int shared_words;
   long long words_off;
   // scan / reduce scratch
@@ -797,6 +812,7 @@ template <typename F, typename S> struct Chan {
   uint4 *eps_list;
   TokInfo *tok_info_alt; // the other half of the channel's provenance buffer
   u32 *app_list;
+  u32 *kill; // the channel's kill words (direct_kills)
   u64 *scr_key;
   u32 *scr_row;
   int2 *arena; // live half
@@ -952,13 +968,18 @@ struct RelaxAcc {
   int n_rec;   // rows written with an output label (emission records, net of self-displacement)
 };
 
+// DEAD / DISP of a cluster's row (0 if neither), from its kill word.
+template <typename F, typename S> __device__ __forceinline__ u32 kill_flags(const Chan<F, S> &C, u32 row) {
+  const u32 w = C.kill[row];
+  return (w >> 2) != C.etag ? 0u : (w & KW_DEAD) ? ROW_DEAD : ROW_DISP;
+}
+
 // Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
 template <typename F, typename S>
 __device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 v) {
-  // (a cluster's passes alternate between the two halves of the kill queue)
-  const u32 cap = F::cluster > 1 ? P.flog_cap / 2 : P.flog_cap;
-  const u32 k = atomicAdd(&GC<F>(sh).n_kill[sh.rpar], 1u);
-  if (k < cap) C.app_list[sh.rpar * cap + k] = v;
+  static_assert(!direct_kills<F>(), "a cluster writes kill words");
+  const u32 k = atomicAdd(&GC<F>(sh).n_kill[0], 1u);
+  if (k < P.flog_cap) C.app_list[k] = v;
   else set_error<F>(sh, E_CAP);
 }
 
@@ -974,12 +995,10 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
   }
   // the replaced winner's row leaves the live rows (its cost is the CAS's expected key)
   atomicSub(&sh.fhist[hbucket(sh, key_cost(old_ck))], 1u);
-  if ((old_info & VROW_MASK) < row0) {
-    acc.n_app++;
-    queue_kill(P, C, sh, old_info & VROW_MASK);
-  } else {
-    queue_kill(P, C, sh, (old_info & VROW_MASK) | KILL_DISP);
-  }
+  const bool earlier = (old_info & VROW_MASK) < row0;
+  acc.n_app += earlier ? 1 : 0;
+  if constexpr (direct_kills<F>()) C.kill[old_info & VROW_MASK] = (etag << 2) | (earlier ? KW_DEAD : KW_DISP);
+  else queue_kill(P, C, sh, (old_info & VROW_MASK) | (earlier ? 0u : KILL_DISP));
 }
 
 // CAS retry loop after a lost race; the candidate's row is `row`.  A
@@ -991,7 +1010,8 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
   const u32 etag = C.etag;
   while (true) {
     if (!value_better(ck, g, row0, etag, vck, vg, vinfo)) {
-      atomicOr(&C.flog_state[row], ROW_DISP);
+      if constexpr (direct_kills<F>()) C.kill[row] = (etag << 2) | KW_DISP;
+      else atomicOr(&C.flog_state[row], ROW_DISP);
       atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
       acc.n_rec -= hasol ? 1 : 0;
       return;
@@ -1125,7 +1145,8 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
       st_row<BLOCK>(&C.eps_list[ep_at++],
                     make_uint4(rows[u], d[u] | (xcode_of(dc[u]) << CODE_SHIFT), (u32)ck[u], (u32)(ck[u] >> 32)));
     }
-    st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | (ecode_of(dc[u]) << CODE_SHIFT));
+    st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | (ecode_of(dc[u]) << CODE_SHIFT) |
+                                              ((direct_kills<F>() && (rflags[u] & ROW_HASOL)) ? ROW_REC : 0u));
     st_row<BLOCK>(&C.flog_ck[rows[u]], (unsigned long long)ck[u]);
     store_aux<BLOCK, F>(C.flog_aux, rows[u], aux_src(src[u], rflags[u], g[u]), ol[u], il[u]);
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
@@ -1215,7 +1236,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         } else { // epsilon-frontier entries carry the row's state, flags and cost
           const uint4 e = list[base + j];
           idx[q] = e.x;
-          st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
+          st[q] = e.y | (direct_kills<F>() ? (kill_flags(C, e.x) & ROW_DISP)
+                         : DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
           w_cost[j] = key_cost(((u64)e.w << 32) | e.z);
         }
         w_src[j] = idx[q];
@@ -1346,7 +1368,8 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         if (base + j < n_in) {
           const uint4 e = list[base + j];
           idx[q] = e.x;
-          st[q] = e.y | (DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
+          st[q] = e.y | (direct_kills<F>() ? (kill_flags(C, e.x) & ROW_DISP)
+                         : DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
           cq[q] = key_cost(((u64)e.w << 32) | e.z);
         }
       }
@@ -1460,7 +1483,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     // (each CTA's own minimum: a 64-bit atomicMin into a peer CTA's shared
     // memory is not atomic on sm_100, bench_tools/dsmem_atomics_probe.cu)
     if (mck != ~0ull) atomicMin(&sh.cnt.min_ck, mck);
-    if (n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, n_rec);
+    if (n_rec && !direct_kills<F>()) atomicAdd(&GC<F>(sh).n_rec_frame, n_rec); // (direct: prune counts)
     if (n_app) atomicAdd(&GC<F>(sh).n_app[sh.rpar], n_app);
     if (n_new && atomicAdd(&GC<F>(sh).n_new, n_new) + n_new > P.tok_cap) set_error<F>(sh, E_CAP);
   }
@@ -1582,46 +1605,33 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
 }
 
 
-// --- a cluster's passes: two cluster barriers per pass -----------------------
-// What a pass leaves for the next one, read by every CTA between the pass's
-// two barriers (rows, epsilon entries and counts are final after the first,
-// and nothing is reserved again before the second).
+// --- a cluster's passes: one cluster barrier per pass ----------------------
+// What a pass leaves for the next one, read by every CTA after the pass's
+// barrier (kills are written during the pass: direct_kills).
 struct PassEnd {
   u32 row0_next; // rows so far: the next pass's first row
   u32 n_cand, n_app, eps_n;
 };
 
-// apply_kills for a cluster: the pass's kill queue (half rpar), then the
-// pass's counts, the barrier, and the reset of the pass's counter slot (its
-// next use is two passes later, behind two more barriers).
+// After a pass's barrier: its counts, then the next pass's slot; the slot of
+// the pass after next (last read before this pass's barrier) is reset here.
 template <int BLOCK, typename F, typename S>
-__device__ PassEnd apply_kills_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
+__device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const u32 p = sh.rpar;
-  const u32 half = P.flog_cap / 2;
   Counters &G = GC<F>(sh);
-  const u32 n = min(G.n_kill[p], half);
-  const u32 *q = C.app_list + p * half;
-  u32 unrec = 0;
-  for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
-    const u32 v = q[i];
-    const u32 row = v & VROW_MASK;
-    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
-    if ((v & KILL_DISP) && row_hasol<F>(C, row)) unrec++; // displaced: no record (DISP read at listing)
-  }
-  unrec = __reduce_add_sync(0xFFFFFFFFu, unrec);
-  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&G.n_rec_frame, unrec);
   PassEnd e;
   e.row0_next = G.flog_n;
   e.n_cand = G.n_cand[p];
   e.n_app = G.n_app[p];
   e.eps_n = G.eps_n;
-  csync<F>();
+  const u32 nx = p == 2 ? 0u : p + 1u;
   if (chan_t0<F>()) {
-    G.n_kill[p] = 0;
-    G.n_cand[p] = 0;
-    G.n_app[p] = 0;
+    const u32 z = nx == 2 ? 0u : nx + 1u;
+    G.n_cand[z] = 0;
+    G.n_app[z] = 0;
   }
-  if (threadIdx.x == 0) sh.rpar = p ^ 1u;
+  __syncthreads(); // every thread of the CTA has read rpar
+  if (threadIdx.x == 0) sh.rpar = nx;
   __syncthreads();
   return e;
 }
@@ -1641,7 +1651,7 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
     if (chan_t0<F>()) GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
     expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
     csync<F>();
-    const PassEnd e = apply_kills_c<BLOCK>(P, C, sh);
+    const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
     if (GC<F>(sh).error) return;
     if (e.n_cand == 0 || e.n_app == 0) break; // decoder.py:263-265, 285-287
     lo = hi;
@@ -1649,7 +1659,8 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
     n_front = e.n_app;
     row0 = e.row0_next;
   }
-  csync<F>();
+  // (no barrier: a pass ends with one, after which rows, kills, histograms
+  // and minima are final, and the next reader, prune(), resets nothing)
 }
 
 // Provenance of a new token list (token i comes from frontier row rows[i]):
@@ -1659,12 +1670,7 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
 template <int BLOCK, typename F, typename S>
 __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 n_tok,
                               const u32 *rows, int best_row) {
-  if (chan_t0<F>()) {
-    GC<F>(sh).max_depth = 0;
-    GC<F>(sh).best_last_il = 0;
-    C.cs->best_tok = -1;
-  }
-  csync<F>();
+  // (max_depth, best_last_il and best_tok were reset by next_epoch())
   int md = 0;
   for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n_tok; i += BLOCK * F::cluster) {
     const u32 r = rows[i];
@@ -1690,7 +1696,7 @@ __device__ void finish_tokens(const DecodeParams &P, const Chan<F, S> &C, Shared
     M.tok_info = M.tok_info_alt;
     M.tok_info_alt = t;
   }
-  csync<F>();
+  __syncthreads(); // the channel state above is read by peers after the caller's next cluster barrier
 }
 
 // Radix select over 64-bit keys (MSD, DB-bit digits, starting below the
@@ -1843,7 +1849,8 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     sh.row_pending = 1;
   }
   if (chan_t0<F>()) {
-    if (GC<F>(sh).n_rec_frame) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)GC<F>(sh).n_rec_frame);
+    if (!direct_kills<F>() && GC<F>(sh).n_rec_frame)
+      atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)GC<F>(sh).n_rec_frame);
     const double prev = C.cs->prev_cut;
     const double rise = prev < INFINITY ? cut - prev : 0.0;
     C.cs->cut_rise = fmax(rise, 0.8 * C.cs->cut_rise);
@@ -1855,6 +1862,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
   u32 n_tok = 0, n_mem = 0;
+  u32 n_rec = 0; // direct_kills: the frame's emission records (rows with an output label, not displaced)
   u32 *mem_row = C.scr_row + P.flog_cap; // set-aside rows grow down from the top of scr_row
   for (u32 base = crank<F>() * TILE; base < n_rows; base += TILE * F::cluster) {
     // rows base + q * BLOCK + tid: warp-coalesced loads
@@ -1869,6 +1877,15 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     for (int q = 0; q < QP; ++q) {
       const u32 i = base + (u32)q * BLOCK + (u32)tid;
       ck[q] = i < n_rows ? C.flog_ck[i] : ~0ull;
+    }
+    if constexpr (direct_kills<F>()) {
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const u32 i = base + (u32)q * BLOCK + (u32)tid;
+        const u32 kf = i < n_rows ? kill_flags(C, i) : ROW_DISP; // (beyond the rows: not live)
+        n_rec += ((st[q] & ROW_REC) && !(kf & ROW_DISP)) ? 1u : 0u;
+        st[q] = (st[q] & (ROW_STATE | ECODE_MASK)) | kf;
+      }
     }
     u32 ns = 0, nm = 0;
 #pragma unroll
@@ -1921,18 +1938,30 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     n_tok += tot_s;
     n_mem += tot_m;
   }
+  if constexpr (direct_kills<F>()) {
+    n_rec = __reduce_add_sync(0xFFFFFFFFu, n_rec);
+    if ((tid & 31) == 0 && n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, (int)n_rec);
+  }
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   if constexpr (F::cluster > 1) { // the cluster's best and totals
+    // (peers read xbest_* and out_tok / out_mem, written again only in the
+    // next attempt, behind more barriers: no second barrier here)
+    if (tid == 0) {
+      sh.xbest_k = bk;
+      sh.xbest_s = bs;
+      sh.xbest_i = bi;
+    }
     csync<F>();
     for (int r = 0; r < F::cluster; ++r) {
       const Shared *o = C.peer_sh[r];
-      const u64 k2 = o->redk[0];
-      const u32 s2 = o->reds[0];
-      if (k2 < bk || (k2 == bk && s2 < bs)) bk = k2, bs = s2, bi = o->redi[0];
+      const u64 k2 = o->xbest_k;
+      const u32 s2 = o->xbest_s;
+      if (k2 < bk || (k2 == bk && s2 < bs)) bk = k2, bs = s2, bi = o->xbest_i;
     }
     n_tok = GC<F>(sh).out_tok;
     n_mem = GC<F>(sh).out_mem;
-    csync<F>();
+    if (chan_t0<F>() && GC<F>(sh).n_rec_frame) // (rec_logical is the leader's own)
+      GC<F>(sh).rec_logical += (unsigned long long)GC<F>(sh).n_rec_frame;
   }
   PROF_MARK(sh, PF_PRUNE_SCAN);
   if (below == 0xFFFFFFFFu) below = n_tok; // split at bt: everything below survives
@@ -1998,11 +2027,11 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       }
       n_tok += total;
     }
-    if (F::cluster > 1 && tid == 0) GC<F>(sh).out_tok = n_tok;
+    if (F::cluster > 1 && tid == 0) GC<F>(sh).out_sel = n_tok;
     }
     if constexpr (F::cluster > 1) {
       csync<F>();
-      n_tok = GC<F>(sh).out_tok;
+      n_tok = GC<F>(sh).out_sel;
     }
   } else if (n_mem > 0) { // the whole split bucket survives (split across a cluster's CTAs)
     const u32 n0 = n_tok;
@@ -2023,7 +2052,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       C.cs->info.trailing_silence = 0;
     C.cs->prev_best = key_cost(best_ck);
   }
-  csync<F>();
+  // (the channel state written above is read after advance()'s last barrier)
   PROF_MARK(sh, PF_PRUNE_OUT);
   return true;
 }
@@ -2038,9 +2067,16 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   // (a cluster's leader alone: the utterance start's closure is small)
   for (u32 i0 = 0; i0 < n_rows && crank<F>() == 0; i0 += BLOCK) {
     const u32 i = i0 + threadIdx.x;
-    const u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
+    u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
+    bool rec;
+    if constexpr (direct_kills<F>()) {
+      const u32 kf = i < n_rows ? kill_flags(C, i) : ROW_DISP;
+      rec = (st & ROW_REC) && !(kf & ROW_DISP);
+      st = (st & (ROW_STATE | ECODE_MASK)) | kf;
+    } else {
+      rec = i < n_rows && !(st & ROW_DISP) && row_hasol<F>(C, i);
+    }
     const bool live = !(st & (ROW_DEAD | ROW_DISP));
-    const bool rec = i < n_rows && !(st & ROW_DISP) && row_hasol<F>(C, i);
     const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, rec));
     if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)nrec);
     u32 total;
@@ -2063,6 +2099,7 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
     C.cs->prev_best = key_cost(frame_min_ck<F>(C, sh));
     C.cs->prev_cut = INFINITY; // the start closure is not pruned: no cutoff to start from
     C.cs->cut_rise = 0.0;
+    C.cs->info.fresh = 0;
   }
   csync<F>();
 }
@@ -2072,9 +2109,13 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
 // carrying it can still be in the table.  Also opens the frame's cost
 // histogram: buckets of beam / HIST_PER_BEAM from one beam below the previous
 // frame's best cost (values outside clamp into the end buckets).
+//
+// One cluster barrier: every CTA derives the epoch from its own view (C.epoch
+// follows cs->epoch), and the counters reset here were last read by peers
+// before an earlier cluster barrier (the previous frame's, or a redo's).
 template <int BLOCK, typename F, typename S>
 __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
-  u32 e = C.cs->epoch + 1;
+  u32 e = C.epoch + 1;
   if ((e & 0x7FFFFFFFu) == 0) e = 0x100; // 31-bit key epochs (wrap also wipes below)
   if ((e & TAG_MASK) == 0) {
     if (F::hashed) {
@@ -2095,10 +2136,12 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
           gv[i] = make_uint4(0, 0, 0, 0);
       }
     }
+    if (C.kill) // kill words carry the tag too
+      for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < P.flog_cap; i += BLOCK * F::cluster) C.kill[i] = 0;
     e += 1;
   }
   for (u32 b = threadIdx.x; b < NB_HIST; b += BLOCK) sh.fhist[b] = 0;
-  csync<F>(); // every CTA has read the old epoch
+  __syncthreads(); // this CTA's threads have read C.epoch
   if (threadIdx.x == 0) {
     C.epoch = e;
     C.etag = e & TAG_MASK;
@@ -2109,13 +2152,16 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   }
   if (chan_t0<F>()) {
     C.cs->epoch = e;
+    GC<F>(sh).max_depth = 0; // finish_tokens()
+    GC<F>(sh).best_last_il = 0;
+    C.cs->best_tok = -1;
     GC<F>(sh).out_tok = 0;
     GC<F>(sh).out_mem = 0;
     GC<F>(sh).n_new = 0;
-    GC<F>(sh).n_app[0] = GC<F>(sh).n_app[1] = 0;
-    GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = 0;
+    GC<F>(sh).n_app[0] = GC<F>(sh).n_app[1] = GC<F>(sh).n_app[2] = 0;
+    GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = GC<F>(sh).n_cand[2] = 0;
     GC<F>(sh).flog_n = 0;
-    GC<F>(sh).n_kill[0] = GC<F>(sh).n_kill[1] = 0;
+    GC<F>(sh).n_kill[0] = 0;
     GC<F>(sh).eps_n = 0;
     GC<F>(sh).emit_end = 0;
     GC<F>(sh).n_rec_frame = 0;
@@ -2233,7 +2279,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     }
   }
   if (threadIdx.x == 0) C.ucut0 = C.ucut = INFINITY;
-  csync<F>();
+  // (no barrier: the channel state read below was written before the
+  // previous frame's last cluster barrier; next_epoch() has the next one)
   if (cs->info.fresh) {
     materialize_start<BLOCK>(P, C, sh);
     if constexpr (F::cluster > 1) { // one row (the start token) so far
@@ -2244,10 +2291,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, 1u); // utterance-start closure, no prune
     }
     if (GC<F>(sh).error) return;
-    rows_to_tokens<BLOCK>(P, C, sh);
-    if (chan_t0<F>()) cs->info.fresh = 0;
+    rows_to_tokens<BLOCK>(P, C, sh); // (clears fresh; ends with a cluster barrier)
   }
-  csync<F>();
   PROF_MARK(sh, PF_START);
   const u32 n_tok = (u32)cs->info.num_active;
   // Expansion-time cutoff.  No token whose cost exceeds the frame's cutoff C*
@@ -2270,8 +2315,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   const long long eps_tr = cs->info.eps_truncations;
   bool filt = !P.exact && cs->prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
               P.max_eps <= C.slack_rounds;
-  csync<F>(); // every CTA has read the channel state above
-  if (chan_t0<F>()) cs->info.status = AB_DECODING;
+  // (a peer may still read the status above: IDLE or DECODING, both pass)
+  if (chan_t0<F>() && cs->info.status != AB_DECODING) cs->info.status = AB_DECODING;
   for (int attempt = 0;; ++attempt) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2291,7 +2336,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     csync<F>();
     u32 n_app, eps_hi, row0_eps;
     if constexpr (F::cluster > 1) {
-      const PassEnd e = apply_kills_c<BLOCK>(P, C, sh);
+      const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
       n_app = e.n_app;
       eps_hi = e.eps_n;
       row0_eps = e.row0_next;
@@ -2313,7 +2358,10 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       if (filt) ok = false;
       else if (chan_t0<F>()) cs->info.num_active = 0;
     } else {
-      if constexpr (F::cluster > 1) epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
+      if constexpr (F::cluster > 1) {
+        epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
+        PROF_MARK(sh, PF_EPS_X);
+      }
       else epsilon_rounds<BLOCK>(P, C, sh, 0u, eps_hi, n_app);
       if (GC<F>(sh).error) return;
       ok = prune<BLOCK>(P, C, sh);
@@ -2532,6 +2580,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.flog_aux = P.flog_aux + s * P.flog_cap;
     C.eps_list = P.eps_list + s * P.flog_cap;
     C.app_list = P.app_list + s * P.flog_cap;
+    C.kill = P.flog_kill ? P.flog_kill + s * P.flog_cap : nullptr;
     C.scr_key = P.scr_key + s * P.flog_cap;
     C.scr_row = P.scr_row + s * P.flog_cap;
     C.arena = P.arena + (2 * s + (C.cs->arena_half & 1)) * P.arena_cap;
@@ -2674,7 +2723,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       G.rec_logical = (unsigned long long)cs->info.store_len;
       G.cnt_tok = G.cnt_emit = G.cnt_eps = 0;
       G.n_new = G.flog_n = 0;
-      G.n_app[0] = G.n_app[1] = G.n_cand[0] = G.n_cand[1] = 0;
+      G.n_app[0] = G.n_app[1] = G.n_app[2] = G.n_cand[0] = G.n_cand[1] = G.n_cand[2] = 0;
 #ifdef AB_PROFILE
       for (int q = 0; q < PF_N; ++q) sh.prof[q] = 0;
       sh.prof_t = clock64();
@@ -2723,7 +2772,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
         sh.next_row = (row_in_smem && t + 1 < T && ((P.L * sizeof(S)) & 15) == 0 &&
                        (reinterpret_cast<size_t>(nrow) & 15) == 0) ? nrow : nullptr;
       }
-      csync<F>();
+      __syncthreads(); // (the row and next_row are this CTA's)
       PROF_MARK(sh, PF_ROW);
       advance<BLOCK>(P, C, sh);
       if (GC<F>(sh).error) break;
@@ -2736,16 +2785,15 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
           if (GC<F>(sh).error) break;
         }
         if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
-          csync<F>();
           if (chan_t0<F>()) cs->info.status = AB_ENDPOINTED;
-          csync<F>();
+          __syncthreads(); // (finalize() runs in the leader CTA, which wrote the status)
           if (lead) finalize<BLOCK>(P, C, sh, n_out);
           ++n_out;
           csync<F>();
           if (GC<F>(sh).error) break;
         }
       }
-      csync<F>();
+      // (no barrier: advance() and each hypothesis end with one)
       PROF_MARK(sh, PF_HYP);
     }
     if (sh.row_pending) { // a prefetched row nobody will read: let it land before the buffer is reused
