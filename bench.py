@@ -351,7 +351,9 @@ def run_b200(args, W, world, rank, local):
     # emission arena: ~16 frames of appends (~45k records per channel-frame on
     # G_large); the in-kernel copying GC reclaims records of pruned paths
     big = W["states"] > 1_000_000
-    cap = Capacity(table_slots=args.table_slots, arena_records=(1 << 20) if big else (1 << 19))
+    # (small graphs, few channels: 2M records per channel, so the collector
+    # runs ~4x less often; C3 keeps 1M x 1024 channels)
+    cap = Capacity(table_slots=args.table_slots, arena_records=(1 << 20) if big else (1 << 21))
     dec = BatchDecoder(dg, C, cap)
     prep["upload_s"] = time.time() - t0
     # the same numpy streams, generated in HBM (ab_scores_generate, bit-identical

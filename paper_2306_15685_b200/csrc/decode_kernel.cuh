@@ -177,6 +177,11 @@ template <int BLOCK> __host__ __device__ constexpr int exp_q() {
   return BLOCK <= 256 ? AB_EXP_Q256 : (BLOCK >= 1024 ? AB_EXP_Q1024 : AB_EXP_Q);
 }
 constexpr int EXP_U = AB_EXP_U; // arcs per thread in flight (arc loads, table round trips)
+// A cluster's channel (one 1024-thread CTA per SM, latency-bound): more arcs
+// per thread in flight
+#ifndef AB_EXP_U_CLUSTER
+#define AB_EXP_U_CLUSTER 1 // (2 spills at 64 registers: slower, profiles/r02_c1_c2_phase_profile.log)
+#endif
 constexpr u32 TILE_COARSE = 128; // coarse search index entries (tiles of up to 4096 arcs)
 #ifndef AB_PRUNE_Q
 #define AB_PRUNE_Q 4
@@ -311,6 +316,7 @@ template <int CL> struct Fmt16SC : Fmt16<false, true> {
 typedef Fmt16SC<2> Fmt16SC2;
 typedef Fmt16SC<4> Fmt16SC4;
 typedef Fmt16SC<8> Fmt16SC8;
+template <typename F> __host__ __device__ constexpr int exp_u() { return F::cluster > 1 ? AB_EXP_U_CLUSTER : EXP_U; }
 
 struct ChanState {
   ab_channel_info info; // info.store_len = records appended this utterance (reference len(store))
@@ -678,7 +684,7 @@ __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
 // Built with -DAB_PROFILE only (scripts/, never the shipped library): thread 0
 // accumulates SM clock cycles per phase; the kernel adds them to P.prof.
 enum { PF_START = 0, PF_ROW, PF_EMIT_X, PF_EMIT_S, PF_EPS_X, PF_EPS_S, PF_PRUNE_SCAN, PF_PRUNE_SEL,
-       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_N = 16 };
+       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_EPOCH, PF_EMIT_BAR, PF_EPS_BAR, PF_ADV_BAR, PF_WALK, PF_NHYP, PF_XLIST, PF_XCAND, PF_XRELAX, PF_N = 21 };
 #ifdef AB_PROFILE
 #define PROF_MARK(sh, id)                                                                          \
   do {                                                                                             \
@@ -730,8 +736,17 @@ struct Counters {
   u32 out_sel;          // cluster prune: survivors after the split-bucket selection
 };
 
+// A partial hypothesis picked but not yet walked (cluster: deferred to the
+// next frame's emitting pass, see emit_pending_warp).
+struct PendHyp {
+  double cost;
+  long long frame;
+  int out_idx, bp, depth, hits;
+};
+
 struct Shared {
   Counters cnt;    // this channel's counters (leader CTA of a cluster)
+  PendHyp pend;    // (leader CTA) the deferred partial hypothesis
   Counters *lead;  // the leader's counters (cluster mode: a DSMEM address)
   u32 sel;
   u32 cum;
@@ -1182,7 +1197,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 //      into the cost add), one batched relaxation.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const uint4 *list, u32 n_in,
-                       u32 row0) {
+                       u32 row0, bool skip0 = false) {
   constexpr u32 TILE = BLOCK * Q;
   // 1024-thread CTAs (one channel alone on its SM, C1 / C2): warp-private
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
@@ -1217,10 +1232,12 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   u32 *w_src = t_src + wid * WT;
   double *w_cost = t_cost + wid * WT;
   // a cluster's warps share the inputs: warp (rank, wid) is global warp gw of CL * NW
-  constexpr u32 GW = NW * F::cluster;
-  const u32 gw = crank<F>() * NW + wid;
+  // (skip0: the cluster's warp 0 is busy elsewhere, the others share the inputs)
+  const u32 GW = NW * F::cluster - (skip0 ? 1u : 0u);
+  const u32 gw0 = crank<F>() * NW + wid;
+  const u32 gw = skip0 ? gw0 - 1u : gw0;
   const u32 per = n_in >= GW * WT ? WT : max(1u, (n_in + GW - 1) / GW);
-  for (u32 base = gw * per; base < n_in; base += GW * per) {
+  for (u32 base = gw * per; base < n_in && !(skip0 && gw0 == 0); base += GW * per) {
     const u32 ne = min(per, n_in - base);
     u32 idx[Q], st[Q], a0[Q], cnt[Q];
 #pragma unroll
@@ -1272,6 +1289,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       if (lane >= (u32)o) incl += y;
     }
     const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    PROF_MARK(sh, PF_XLIST);
     u32 run = incl - tsum;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -1330,7 +1348,9 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         rflags[u] = 0;
         if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
       }
+      PROF_MARK(sh, PF_XCAND);
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
+      PROF_MARK(sh, PF_XRELAX);
     }
     __syncwarp();
   }
@@ -1589,7 +1609,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
       GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
     }
     csync<F>();
-    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
+    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
     csync<F>();
     apply_kills<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_X);
@@ -1649,9 +1669,12 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
     }
     rounds++;
     if (chan_t0<F>()) GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
-    expand<BLOCK, exp_q<BLOCK>(), EXP_U, false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
+    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
+    PROF_MARK(sh, PF_EPS_X);
+    PROF_COUNT(sh, PF_ROUNDS, 1);
     csync<F>();
     const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
+    PROF_MARK(sh, PF_EPS_BAR);
     if (GC<F>(sh).error) return;
     if (e.n_cand == 0 || e.n_app == 0) break; // decoder.py:263-265, 285-287
     lo = hi;
@@ -2259,9 +2282,19 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
   csync<F>();
 }
 
-// advance_frame (decoder.py:341-411) for frame row C.row.
+// The leader's warp 0 writes the deferred partial hypothesis (the other
+// warps go on; the caller's next cluster barrier publishes it).
+template <typename F, typename S>
+__device__ __forceinline__ void flush_pending(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &pend) {
+  if (pend && crank<F>() == 0 && threadIdx.x < 32) emit_pending_warp(P, C, sh);
+  pend = false;
+}
+
+// advance_frame (decoder.py:341-411) for frame row C.row.  pend: a deferred
+// partial hypothesis of the previous frame (cluster), written during this
+// frame's emitting pass (or before the collector moves its records).
 template <int BLOCK, typename F, typename S>
-__device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
+__device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &pend) {
   ChanState *cs = C.cs;
   if (cs->info.status != AB_IDLE && cs->info.status != AB_DECODING) {
     if (chan_t0<F>()) set_error<F>(sh, E_STATUS);
@@ -2270,6 +2303,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   }
   // one frame appends at most flog_cap records: collect first if they might not fit
   if (!cs->info.fresh && (unsigned long long)GC<F>(sh).rec_n + P.flog_cap > P.arena_cap) {
+    flush_pending(P, C, sh, pend); // (gc_arena begins with a cluster barrier)
     gc_arena<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_GC);
     if ((unsigned long long)GC<F>(sh).rec_n + P.flog_cap > P.arena_cap) {
@@ -2282,6 +2316,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   // (no barrier: the channel state read below was written before the
   // previous frame's last cluster barrier; next_epoch() has the next one)
   if (cs->info.fresh) {
+    flush_pending(P, C, sh, pend); // (none: a partial is deferred only while the utterance goes on)
     materialize_start<BLOCK>(P, C, sh);
     if constexpr (F::cluster > 1) { // one row (the start token) so far
       const u32 hi0 = GC<F>(sh).eps_n;
@@ -2332,7 +2367,11 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       C.ucut = filt ? hint + C.slack + m : INFINITY;
     }
     next_epoch<BLOCK>(P, C, sh);
-    expand<BLOCK, exp_q<BLOCK>(), EXP_U, true>(P, C, sh, nullptr, n_tok, 0u);
+    PROF_MARK(sh, PF_EPOCH);
+    const bool skip0 = pend; // global warp 0 (the leader's warp 0) writes the pending hypothesis
+    flush_pending(P, C, sh, pend);
+    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), true>(P, C, sh, nullptr, n_tok, 0u, skip0);
+    PROF_MARK(sh, PF_EMIT_X);
     csync<F>();
     u32 n_app, eps_hi, row0_eps;
     if constexpr (F::cluster > 1) {
@@ -2349,7 +2388,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
       if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
       csync<F>();
     }
-    PROF_MARK(sh, PF_EMIT_X);
+    PROF_MARK(sh, PF_EMIT_BAR);
     if (GC<F>(sh).error) return;
     bool ok = true;
     if (n_app == 0) {
@@ -2360,7 +2399,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     } else {
       if constexpr (F::cluster > 1) {
         epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
-        PROF_MARK(sh, PF_EPS_X);
+        PROF_MARK(sh, PF_EPS_S);
       }
       else epsilon_rounds<BLOCK>(P, C, sh, 0u, eps_hi, n_app);
       if (GC<F>(sh).error) return;
@@ -2384,37 +2423,75 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     cs->info.total_frames += 1;
   }
   csync<F>();
+  PROF_MARK(sh, PF_ADV_BAR);
 }
 
 // Traceback with prefix sharing against the channel's previous hypothesis
-// path (EmissionStore.backtrace, decoder.py:95-102), then hypothesis output.
+// path (EmissionStore.backtrace, decoder.py:95-102), by one thread: the new
+// path's records and words from depth down to the first record the previous
+// path has at the same depth; reserves the new words.  False: E_CAP (set).
+template <typename F, typename S>
+__device__ bool hyp_walk(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx, int bp, int depth,
+                         int &shared_words, long long &words_off) {
+  ChanState *cs = C.cs;
+  if ((u32)depth > P.path_cap) {
+    set_error<F>(sh, E_CAP);
+    return false;
+  }
+  int rec = bp, d = depth;
+  const int plen = cs->path_len;
+  PROF_COUNT(sh, PF_NHYP, 1);
+  // (one dependent load per step: the record and the previous path's entry
+  // at the same depth are loaded together)
+  while (d > 0) {
+    const int2 r = C.arena[rec];
+    if (d <= plen && C.path_rec[d - 1] == rec) break;
+    PROF_COUNT(sh, PF_WALK, 1);
+    C.path_rec[d - 1] = rec;
+    C.path_words[d - 1] = r.x;
+    rec = r.y;
+    --d;
+  }
+  shared_words = d;
+  cs->path_len = depth;
+  const long long need = depth - d;
+  const long long off = P.words_used[C.b];
+  if (off + need > P.words_stride || out_idx >= P.hyp_stride) {
+    set_error<F>(sh, E_CAP);
+    return false;
+  }
+  P.words_used[C.b] = off + need;
+  words_off = (long long)C.b * P.words_stride + off;
+  return true;
+}
+
+template <typename F, typename S>
+__device__ __forceinline__ void write_hyp(const DecodeParams &P, const Chan<F, S> &C, int out_idx, int kind,
+                                          int fallback, double cost, long long frame, int hits, int s0, int depth,
+                                          long long off) {
+  DevHyp h;
+  h.cost = cost;
+  h.frame = frame;
+  h.kind = kind;
+  h.fallback = fallback;
+  h.hits = hits;
+  h.shared = s0;
+  h.n_words = depth;
+  h.pad = 0;
+  h.words_off = off;
+  P.hyps[(size_t)C.b * P.hyp_stride + out_idx] = h;
+}
+
+// Hypothesis output by the whole CTA.
 template <int BLOCK, typename F, typename S>
 __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx, int kind, int fallback,
                          double cost, int bp, int depth, int hits) {
-  ChanState *cs = C.cs;
   if (threadIdx.x == 0) {
-    int shared_words = 0;
-    if ((u32)depth > P.path_cap) {
-      set_error<F>(sh, E_CAP);
-    } else {
-      int rec = bp, d = depth;
-      const int plen = cs->path_len;
-      while (d > 0) {
-        if (d <= plen && C.path_rec[d - 1] == rec) break;
-        C.path_rec[d - 1] = rec;
-        const int2 r = C.arena[rec];
-        C.path_words[d - 1] = r.x;
-        rec = r.y;
-        --d;
-      }
-      shared_words = d;
-      cs->path_len = depth;
-      const long long need = depth - shared_words;
-      const long long off = P.words_used[C.b];
-      if (off + need > P.words_stride || out_idx >= P.hyp_stride) set_error<F>(sh, E_CAP);
-      else P.words_used[C.b] = off + need;
-      sh.shared_words = shared_words;
-      sh.words_off = (long long)C.b * P.words_stride + off;
+    int s0 = 0;
+    long long off = 0;
+    if (hyp_walk(P, C, sh, out_idx, bp, depth, s0, off)) {
+      sh.shared_words = s0;
+      sh.words_off = off;
     }
   }
   __syncthreads();
@@ -2422,35 +2499,29 @@ __device__ void emit_hyp(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int o
   const int s0 = sh.shared_words;
   const long long off = sh.words_off;
   for (int i = s0 + threadIdx.x; i < depth; i += BLOCK) P.words[off + (i - s0)] = C.path_words[i];
-  if (threadIdx.x == 0) {
-    DevHyp h;
-    h.cost = cost;
-    h.frame = cs->info.total_frames;
-    h.kind = kind;
-    h.fallback = fallback;
-    h.hits = hits;
-    h.shared = s0;
-    h.n_words = depth;
-    h.pad = 0;
-    h.words_off = off;
-    P.hyps[(size_t)C.b * P.hyp_stride + out_idx] = h;
-  }
+  if (threadIdx.x == 0)
+    write_hyp(P, C, out_idx, kind, fallback, cost, C.cs->info.total_frames, hits, s0, depth, off);
   __syncthreads();
 }
 
-// partial_hypothesis (decoder.py:414-423).
+// The best token (partial_hypothesis, decoder.py:414-423), by the whole CTA:
+// false if the channel is dead (E_DEAD set).
 template <int BLOCK, typename F, typename S>
-__device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx) {
+__device__ bool partial_pick(const DecodeParams &P, Chan<F, S> &C, Shared &sh, PendHyp &h) {
   ChanState *cs = C.cs;
+  h.frame = cs->info.total_frames;
   if (cs->info.fresh) {
-    emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, 0.0, -1, 0, 0);
-    return;
+    h.cost = 0.0;
+    h.bp = -1;
+    h.depth = 0;
+    h.hits = 0;
+    return true;
   }
   const u32 n = (u32)cs->info.num_active;
   if (n == 0) {
     if (threadIdx.x == 0) set_error<F>(sh, E_DEAD);
     __syncthreads();
-    return;
+    return false;
   }
   // the best (cost, state) token: prune found it (best_tok), else one pass
   int bi = cs->best_tok;
@@ -2466,7 +2537,39 @@ __device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int ou
     block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
   }
   const TokInfo t = C.tok_info[bi];
-  emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, C.tok_cost[bi], t.bp, t.depth, t.hits);
+  h.cost = C.tok_cost[bi];
+  h.bp = t.bp;
+  h.depth = t.depth;
+  h.hits = t.hits;
+  return true;
+}
+
+// partial_hypothesis (decoder.py:414-423).
+template <int BLOCK, typename F, typename S>
+__device__ void partial(const DecodeParams &P, Chan<F, S> &C, Shared &sh, int out_idx) {
+  PendHyp h;
+  if (partial_pick<BLOCK>(P, C, sh, h)) emit_hyp<BLOCK>(P, C, sh, out_idx, AB_PARTIAL, 0, h.cost, h.bp, h.depth, h.hits);
+}
+
+// A cluster's deferred partial hypothesis (decode_kernel): picked at the end
+// of its frame by the leader CTA, walked and written by the leader's warp 0
+// while the rest of the cluster runs the next frame's emitting pass (its
+// records and token provenance are not touched before that pass ends).
+template <typename F, typename S>
+__device__ void emit_pending_warp(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
+  const PendHyp &h = sh.pend;
+  const u32 lane = threadIdx.x & 31u;
+  int s0 = 0, ok = 0;
+  long long off = 0;
+  if (lane == 0) ok = hyp_walk(P, C, sh, h.out_idx, h.bp, h.depth, s0, off) ? 1 : 0;
+  __syncwarp();
+  ok = __shfl_sync(0xFFFFFFFFu, ok, 0);
+  if (!ok) return;
+  s0 = __shfl_sync(0xFFFFFFFFu, s0, 0);
+  off = __shfl_sync(0xFFFFFFFFu, off, 0);
+  for (int i = s0 + (int)lane; i < h.depth; i += 32) P.words[off + (i - s0)] = C.path_words[i];
+  if (lane == 0) write_hyp(P, C, h.out_idx, AB_PARTIAL, 0, h.cost, h.frame, h.hits, s0, h.depth, off);
+  __syncwarp();
 }
 
 // finalize (decoder.py:426-460): best final token by (cost + final, state),
@@ -2738,6 +2841,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
     if (was_finished && chan_t0<F>()) cs->info.status = AB_IDLE; // decoder.py:488-489
     csync<F>();
     int t = 0;
+    bool pend = false; // a deferred partial hypothesis (cluster)
     for (; t < T; ++t) {
       if (P.mode == AB_MODE_STREAM) {
         // a frame adds at most 1 + max_eps words to any path (a fresh channel's
@@ -2746,7 +2850,7 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
         const long long E = min((long long)max(P.max_eps, 0), (long long)P.path_cap);
         const long long bound =
             min((long long)(cs->info.fresh ? E : cs->max_depth) + 2 + E, (long long)P.path_cap);
-        if (P.words_used[b] + 2 * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
+        if (P.words_used[b] + (pend ? 3 : 2) * bound > P.words_stride || n_out + 2 > P.hyp_stride) {
           if (t == 0 && chan_t0<F>()) set_error<F>(sh, E_CAP); // no progress possible
           break;
         }
@@ -2774,15 +2878,32 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       }
       __syncthreads(); // (the row and next_row are this CTA's)
       PROF_MARK(sh, PF_ROW);
-      advance<BLOCK>(P, C, sh);
+      advance<BLOCK>(P, C, sh, pend);
       if (GC<F>(sh).error) break;
       if (P.mode == AB_MODE_STREAM) {
         // hypotheses: the leader CTA alone (every CTA counts them)
         if (cs->info.frame_index % P.partial_every == 0) {
-          if (lead) partial<BLOCK>(P, C, sh, n_out);
-          ++n_out;
-          csync<F>();
-          if (GC<F>(sh).error) break;
+          // a cluster defers the traceback to the next frame's emitting pass
+          // while the utterance goes on (every CTA decides alike)
+          const bool defer = F::cluster > 1 && t + 1 < T && cs->info.trailing_silence < P.endpoint_silence_frames &&
+                             (cs->info.fresh || cs->info.num_active > 0);
+          if (defer) {
+            if (lead) {
+              PendHyp h;
+              partial_pick<BLOCK>(P, C, sh, h);
+              if (threadIdx.x == 0) {
+                h.out_idx = n_out;
+                sh.pend = h; // (read by this CTA's warp 0, behind a CTA barrier)
+              }
+            }
+            pend = true;
+            ++n_out;
+          } else {
+            if (lead) partial<BLOCK>(P, C, sh, n_out);
+            ++n_out;
+            csync<F>();
+            if (GC<F>(sh).error) break;
+          }
         }
         if (cs->info.trailing_silence >= P.endpoint_silence_frames) { // detect_endpoint 463-464
           if (chan_t0<F>()) cs->info.status = AB_ENDPOINTED;
@@ -2795,6 +2916,10 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
       }
       // (no barrier: advance() and each hypothesis end with one)
       PROF_MARK(sh, PF_HYP);
+    }
+    if (pend) { // the last deferred hypothesis
+      flush_pending(P, C, sh, pend);
+      csync<F>();
     }
     if (sh.row_pending) { // a prefetched row nobody will read: let it land before the buffer is reused
       mbar_wait(&sh.row_bar, sh.row_phase);
