@@ -666,6 +666,41 @@ __device__ __forceinline__ u32 agg_reserve(u32 *counter, u32 n) {
   return grp.shfl(base, 0) + excl;
 }
 
+// agg_reserve of two counters packed in one 64-bit word (low, high halves):
+// one atomic per group for both (a cluster's counters are a peer's shared
+// memory, where every atomic is a round trip).
+__device__ __forceinline__ void agg_reserve2(unsigned long long *counter, u32 n_lo, u32 n_hi, u32 &base_lo,
+                                             u32 &base_hi) {
+  const u32 act = __activemask();
+  const int lane = threadIdx.x & 31;
+  if (__all_sync(act, n_lo <= 1u && n_hi <= 1u)) {
+    const u32 ml = __ballot_sync(act, n_lo != 0), mh = __ballot_sync(act, n_hi != 0);
+    const u32 m = ml | mh;
+    if (!m) {
+      base_lo = base_hi = 0;
+      return;
+    }
+    const int leader = __ffs(m) - 1;
+    unsigned long long b = 0;
+    if (lane == leader) b = atomicAdd(counter, (unsigned long long)__popc(ml) | ((unsigned long long)__popc(mh) << 32));
+    b = __shfl_sync(act, b, leader);
+    const u32 lt = (1u << lane) - 1u;
+    base_lo = (u32)b + (u32)__popc(ml & lt);
+    base_hi = (u32)(b >> 32) + (u32)__popc(mh & lt);
+    return;
+  }
+  namespace cg = cooperative_groups;
+  cg::coalesced_group grp = cg::coalesced_threads();
+  const u32 el = cg::exclusive_scan(grp, n_lo, cg::plus<u32>());
+  const u32 eh = cg::exclusive_scan(grp, n_hi, cg::plus<u32>());
+  const u32 tl = grp.shfl(el + n_lo, grp.size() - 1), th = grp.shfl(eh + n_hi, grp.size() - 1);
+  unsigned long long b = 0;
+  if (grp.thread_rank() == 0 && (tl | th)) b = atomicAdd(counter, (unsigned long long)tl | ((unsigned long long)th << 32));
+  b = grp.shfl(b, 0);
+  base_lo = (u32)b + el;
+  base_hi = (u32)(b >> 32) + eh;
+}
+
 // warp-aggregated append to a shared counter: one smem atomic per warp.
 // Must be reached by every lane of the warp (pred may differ).
 __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
@@ -684,7 +719,7 @@ __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
 // Built with -DAB_PROFILE only (scripts/, never the shipped library): thread 0
 // accumulates SM clock cycles per phase; the kernel adds them to P.prof.
 enum { PF_START = 0, PF_ROW, PF_EMIT_X, PF_EMIT_S, PF_EPS_X, PF_EPS_S, PF_PRUNE_SCAN, PF_PRUNE_SEL,
-       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_EPOCH, PF_EMIT_BAR, PF_EPS_BAR, PF_ADV_BAR, PF_WALK, PF_NHYP, PF_XLIST, PF_XCAND, PF_XRELAX, PF_N = 21 };
+       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_EPOCH, PF_EMIT_BAR, PF_EPS_BAR, PF_ADV_BAR, PF_WALK, PF_NHYP, PF_XLIST, PF_XCAND, PF_XRELAX, PF_PHIST, PF_PROWS, PF_N = 23 };
 #ifdef AB_PROFILE
 #define PROF_MARK(sh, id)                                                                          \
   do {                                                                                             \
@@ -720,7 +755,15 @@ struct Counters {
   // with one CTA per channel): a cluster reads a pass's slot after the pass's
   // barrier and resets the slot of the pass after next, so a pass needs one
   // cluster barrier
-  u32 n_new, n_app[3], n_cand[3], rec_n, flog_n;
+  // frontier rows so far | epsilon-frontier entries so far (eps_n), in one
+  // 64-bit word: a warp reserves both with one atomic (agg_reserve2)
+  union {
+    struct {
+      u32 flog_n, eps_n;
+    };
+    unsigned long long fe_n;
+  };
+  u32 n_new, n_app[3], n_cand[3], rec_n;
   unsigned long long rec_logical;
   unsigned long long min_ck; // cheapest application of the current frame
   int error;
@@ -728,7 +771,6 @@ struct Counters {
   unsigned long long cnt_tok, cnt_emit, cnt_eps;
   int n_rec_frame; // emission records of the frame (olabel != 0 applications)
   u32 n_kill[1];   // kill queue length of the current round (one CTA per channel)
-  u32 eps_n;       // entries in the channel's epsilon-frontier list this frame
   u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
@@ -1065,7 +1107,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
     ld_cg_entry(&C.table[slot], key, vck, vg, vinfo);
   }
   if (!value_better(ck, g, row0, C.etag, vck, vg, vinfo)) return;
-  const u32 row = atomicAdd(&GC<F>(sh).flog_n, 1u);
+  const u32 row = (u32)atomicAdd(&GC<F>(sh).fe_n, 1ull);
   if (row >= P.flog_cap) {
     set_error<F>(sh, E_CAP);
     return;
@@ -1073,7 +1115,7 @@ __device__ __noinline__ void relax_probe(const DecodeParams &P, const Chan<F, S>
   C.flog_state[row] = d | (ecode_of(dc) << CODE_SHIFT);
   C.flog_ck[row] = ck;
   if (rflags & ROW_EPS) {
-    const u32 epos = atomicAdd(&GC<F>(sh).eps_n, 1u);
+    const u32 epos = (u32)(atomicAdd(&GC<F>(sh).fe_n, 1ull << 32) >> 32);
     C.eps_list[epos] = make_uint4(row, d | (xcode_of(dc) << CODE_SHIFT), (u32)ck, (u32)(ck >> 32));
   }
   store_aux<1024, F>(C.flog_aux, row, aux_src(src, rflags, g), lab_ol, lab_il);
@@ -1140,16 +1182,16 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
     nw += want[u] ? 1u : 0u;
   }
   if (!nw) return;
-  u32 row = agg_reserve(&GC<F>(sh).flog_n, nw);
+  u32 ne = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
+  u32 row, ep_at;
+  agg_reserve2(&GC<F>(sh).fe_n, nw, ne, row, ep_at);
   if (row + nw > P.flog_cap) {
     set_error<F>(sh, E_CAP);
     return;
   }
   u32 rows[U], ninfo[U];
-  u32 ne = 0;
-#pragma unroll
-  for (int u = 0; u < U; ++u) ne += (want[u] && (rflags[u] & ROW_EPS)) ? 1u : 0u;
-  u32 ep_at = agg_reserve(&GC<F>(sh).eps_n, ne);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     rows[u] = 0;
@@ -1631,6 +1673,7 @@ __device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Share
 struct PassEnd {
   u32 row0_next; // rows so far: the next pass's first row
   u32 n_cand, n_app, eps_n;
+  int error;
 };
 
 // After a pass's barrier: its counts, then the next pass's slot; the slot of
@@ -1640,10 +1683,11 @@ __device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared
   const u32 p = sh.rpar;
   Counters &G = GC<F>(sh);
   PassEnd e;
-  e.row0_next = G.flog_n;
+  e.row0_next = G.flog_n; // (the leader's counters: remote loads, issued together)
   e.n_cand = G.n_cand[p];
   e.n_app = G.n_app[p];
   e.eps_n = G.eps_n;
+  e.error = G.error;
   const u32 nx = p == 2 ? 0u : p + 1u;
   if (chan_t0<F>()) {
     const u32 z = nx == 2 ? 0u : nx + 1u;
@@ -1675,7 +1719,7 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
     csync<F>();
     const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
     PROF_MARK(sh, PF_EPS_BAR);
-    if (GC<F>(sh).error) return;
+    if (e.error) return;
     if (e.n_cand == 0 || e.n_app == 0) break; // decoder.py:263-265, 285-287
     lo = hi;
     hi = e.eps_n;
@@ -1867,6 +1911,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     csync<F>();
     return false;
   }
+  PROF_MARK(sh, PF_PHIST);
   if (tid == 0 && sh.next_row) { // the score row is read by the emitting pass only, which is now final
     bulk_row_load(const_cast<S *>(C.row), sh.next_row, (u32)(P.L * sizeof(S)), &sh.row_bar);
     sh.row_pending = 1;
@@ -1961,6 +2006,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     n_tok += tot_s;
     n_mem += tot_m;
   }
+  PROF_MARK(sh, PF_PROWS);
   if constexpr (direct_kills<F>()) {
     n_rec = __reduce_add_sync(0xFFFFFFFFu, n_rec);
     if ((tid & 31) == 0 && n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, (int)n_rec);
@@ -2374,8 +2420,10 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
     PROF_MARK(sh, PF_EMIT_X);
     csync<F>();
     u32 n_app, eps_hi, row0_eps;
+    int err;
     if constexpr (F::cluster > 1) {
       const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
+      err = e.error;
       n_app = e.n_app;
       eps_hi = e.eps_n;
       row0_eps = e.row0_next;
@@ -2387,9 +2435,10 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
       row0_eps = 0;
       if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
       csync<F>();
+      err = GC<F>(sh).error;
     }
     PROF_MARK(sh, PF_EMIT_BAR);
-    if (GC<F>(sh).error) return;
+    if (err) return;
     bool ok = true;
     if (n_app == 0) {
       // no emitting arcs: every token dies (decoder.py:394-398); a filtered
