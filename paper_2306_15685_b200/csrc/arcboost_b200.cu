@@ -1675,9 +1675,9 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
     cudaMemcpy(pr, P.prof, sizeof(pr), cudaMemcpyDeviceToHost);
     static const char *names[PF_N] = {"start", "row", "emit_x", "emit_s", "eps_x", "eps_s",
                                       "prune_scan", "prune_sel", "prune_out", "hyp", "gc", "rounds",
-                                      "epoch", "emit_bar", "eps_bar", "adv_bar", "walk", "nhyp", "xlist", "xcand", "xrelax", "phist", "prows"};
+                                      "epoch", "emit_bar", "eps_bar", "adv_bar", "walk", "nhyp", "xlist", "xcand", "xrelax", "phist", "prows", "nsel", "nmem", "npass"};
     fprintf(stderr, "AB_PROFILE");
-    for (int q = 0; q < 23; ++q) fprintf(stderr, " %s=%llu", names[q], pr[q]);
+    for (int q = 0; q < 26; ++q) fprintf(stderr, " %s=%llu", names[q], pr[q]);
     fprintf(stderr, "\n");
     cudaMemset(P.prof, 0, sizeof(pr));
   }

@@ -187,6 +187,7 @@ constexpr u32 TILE_COARSE = 128; // coarse search index entries (tiles of up to 
 #define AB_PRUNE_Q 4
 #endif
 constexpr int PRUNE_Q = AB_PRUNE_Q; // rows per thread in flight (prune)
+constexpr u32 RANK_MAX = 256; // prune's split bucket: selection by rank up to this many rows (else radix)
 
 enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
 // LIST contexts of up to LIST_SMEM_MAX arcs: a two-hash Bloom filter of their
@@ -719,7 +720,7 @@ __device__ __forceinline__ u32 warp_append(u32 *counter, bool pred) {
 // Built with -DAB_PROFILE only (scripts/, never the shipped library): thread 0
 // accumulates SM clock cycles per phase; the kernel adds them to P.prof.
 enum { PF_START = 0, PF_ROW, PF_EMIT_X, PF_EMIT_S, PF_EPS_X, PF_EPS_S, PF_PRUNE_SCAN, PF_PRUNE_SEL,
-       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_EPOCH, PF_EMIT_BAR, PF_EPS_BAR, PF_ADV_BAR, PF_WALK, PF_NHYP, PF_XLIST, PF_XCAND, PF_XRELAX, PF_PHIST, PF_PROWS, PF_N = 23 };
+       PF_PRUNE_OUT, PF_HYP, PF_GC, PF_ROUNDS, PF_EPOCH, PF_EMIT_BAR, PF_EPS_BAR, PF_ADV_BAR, PF_WALK, PF_NHYP, PF_XLIST, PF_XCAND, PF_XRELAX, PF_PHIST, PF_PROWS, PF_NSEL, PF_NMEM, PF_NPASS, PF_N = 26 };
 #ifdef AB_PROFILE
 #define PROF_MARK(sh, id)                                                                          \
   do {                                                                                             \
@@ -774,7 +775,12 @@ struct Counters {
   u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
-  u32 out_tok, out_mem; // cluster prune: survivors / split-bucket rows reserved so far
+  union { // cluster prune: survivors | split-bucket rows reserved so far (one atomic reserves both)
+    struct {
+      u32 out_tok, out_mem;
+    };
+    unsigned long long out_tm;
+  };
   u32 out_sel;          // cluster prune: survivors after the split-bucket selection
 };
 
@@ -1833,6 +1839,7 @@ __device__ u64 radix_select(Shared &sh, u32 *hist, u32 n, KeyFn keyf, u64 lo, u6
       return prefix | ((1ull << lowbit) - 1); // the whole bucket survives
     }
     pos = lowbit - 1;
+    PROF_COUNT(sh, PF_NPASS, 1);
   }
 }
 
@@ -1973,8 +1980,10 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     u32 pm = psm >> 16;
     if constexpr (F::cluster > 1) { // output positions reserved on the leader's counters
       if (tid == 0) {
-        sh.out_base_tok = tot_s ? atomicAdd(&GC<F>(sh).out_tok, tot_s) : 0u;
-        sh.out_base_mem = tot_m ? atomicAdd(&GC<F>(sh).out_mem, tot_m) : 0u;
+        const unsigned long long b =
+            tot_sm ? atomicAdd(&GC<F>(sh).out_tm, (unsigned long long)tot_s | ((unsigned long long)tot_m << 32)) : 0ull;
+        sh.out_base_tok = (u32)b;
+        sh.out_base_mem = (u32)(b >> 32);
       }
       __syncthreads();
       ps += sh.out_base_tok;
@@ -2043,9 +2052,43 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     }
     // exact (cost, state) order inside the split bucket (a cluster's leader alone)
     if (crank<F>() == 0) {
+    PROF_COUNT(sh, PF_NSEL, 1);
+    PROF_COUNT(sh, PF_NMEM, n_mem);
     u64 tc = ~0ull;
     u32 ts = 0xFFFFFFFFu;
-    if (need > 0) {
+    // few rows (the usual case): each row's rank by (cost, state) among them,
+    // compared 32 at a time through shuffles from a shared-memory copy
+    const bool by_rank = n_mem <= RANK_MAX && n_mem <= BLOCK * (u32)exp_q<BLOCK>();
+    u32 rank = 0xFFFFFFFFu;
+    if (need > 0 && by_rank) {
+      u64 *rk = reinterpret_cast<u64 *>(C.t_cost);
+      u32 *rs = C.t_a0;
+      u64 k = ~0ull;
+      u32 s = 0xFFFFFFFFu;
+      if ((u32)tid < n_mem) {
+        k = C.scr_key[tid];
+        s = scr_state[tid] & ROW_STATE;
+        rk[tid] = k;
+        rs[tid] = s;
+      }
+      __syncthreads();
+      if (((u32)tid & ~31u) < n_mem) { // warps holding rows
+        const u32 lane = (u32)tid & 31u;
+        rank = 0;
+        for (u32 c = 0; c < n_mem; c += 32) {
+          const bool in = c + lane < n_mem;
+          const u64 kc = in ? rk[c + lane] : ~0ull;
+          const u32 sc = in ? rs[c + lane] : 0xFFFFFFFFu;
+#pragma unroll 8
+          for (int o = 0; o < 32; ++o) {
+            const u64 ko = __shfl_sync(0xFFFFFFFFu, kc, o);
+            const u32 so = __shfl_sync(0xFFFFFFFFu, sc, o);
+            rank += (ko < k || (ko == k && so < s)) ? 1u : 0u;
+          }
+        }
+      }
+      PROF_COUNT(sh, PF_NPASS, 0);
+    } else if (need > 0) {
       u32 nd = need;
       u64 lo = ~0ull, hi = 0ull;
       for (u32 m = tid; m < n_mem; m += BLOCK) {
@@ -2085,7 +2128,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
         k = C.scr_key[m];
         s = scr_state[m];
         r = *(mem_row - 1 - m);
-        keep = k < tc || (k == tc && (s & ROW_STATE) <= ts);
+        keep = by_rank ? rank < need : (k < tc || (k == tc && (s & ROW_STATE) <= ts));
       }
       u32 total;
       const u32 p = n_tok + block_excl_scan<BLOCK>(keep ? 1u : 0u, total, sh.scan);
@@ -2224,8 +2267,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     GC<F>(sh).max_depth = 0; // finish_tokens()
     GC<F>(sh).best_last_il = 0;
     C.cs->best_tok = -1;
-    GC<F>(sh).out_tok = 0;
-    GC<F>(sh).out_mem = 0;
+    GC<F>(sh).out_tm = 0;
     GC<F>(sh).n_new = 0;
     GC<F>(sh).n_app[0] = GC<F>(sh).n_app[1] = GC<F>(sh).n_app[2] = 0;
     GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = GC<F>(sh).n_cand[2] = 0;
