@@ -69,6 +69,7 @@ struct HostCtx {
   u32 *d_neg = nullptr;    // its neg Bloom filters (NEG_BLOCK_WORDS)
   u32 neg_count = 0;       // states they flag
   u32 *d_hq = nullptr;     // or 2-bit per-state slack (dense contexts)
+  u32 *d_fbits = nullptr, *d_fbits_x = nullptr; // dense contexts: per record position, "hq of the destination > 0"
   double hq_unit = 0.0;
 };
 
@@ -86,6 +87,7 @@ struct ab_graph {
   // contexts are stored by record position, so the kernel's boost lookup is
   // addressed before the arc record arrives (issued next to the record load)
   std::vector<u32> arc_pos;
+  std::vector<u32> arc_dst;      // next state of every arc (dense contexts' slack flags by position)
   uint64_t e_tot = 0, x_tot = 0; // records in the emitting / epsilon arrays
   // epsilon subgraph on the host (arc ids increasing; reverse adjacency by
   // destination) for the epsilon slack of a weighting (eps_slack)
@@ -302,6 +304,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
   g->e_tot = e_tot;
   g->x_tot = x_tot;
   g->arc_pos.resize(num_arcs);
+  g->arc_dst.resize(num_arcs);
   // a record's next-state word carries the destination's degree codes
   // (decode_kernel.cuh CODE_SHIFT): the kernel never loads the degree array
   auto codes = [&](int t) -> u32 {
@@ -312,6 +315,7 @@ extern "C" int ab_graph_create(int32_t device, int32_t start, int32_t num_states
     u32 pe = e_beg[s], px = x_beg[s];
     for (int64_t a = row_offsets[s]; a < row_offsets[s + 1]; ++a) {
       const int dst = next_states[a];
+      g->arc_dst[a] = (u32)dst;
       const bool dst_eps = x_cnt[dst + 1] > x_cnt[dst];
       const u32 nsw = (u32)dst | codes(dst);
       if (ilabels[a] != 0) {
@@ -404,6 +408,10 @@ extern "C" void ab_graph_destroy(ab_graph *g) {
     cudaFree(c.d_bits_x);
     cudaFree(c.d_neg);
     cudaFree(c.d_hq);
+  cudaFree(c.d_fbits);
+  cudaFree(c.d_fbits_x);
+    cudaFree(c.d_fbits);
+    cudaFree(c.d_fbits_x);
   }
   cudaFree(g->d_ctxs);
   cudaFree(g->e_rng);
@@ -538,6 +546,8 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].neg = c.d_neg;
     h[i].hq = c.d_hq;
     h[i].hq_unit = c.hq_unit;
+    h[i].fbits = c.d_fbits;
+    h[i].fbits_x = c.d_fbits_x;
   }
   if (h.size() > g->d_ctxs_cap) {
     cudaFree(g->d_ctxs);
@@ -599,6 +609,22 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   if (!hq.empty()) {
     CK(cudaMalloc(&c.d_hq, hq.size() * sizeof(u32)));
     CK(cudaMemcpy(c.d_hq, hq.data(), hq.size() * sizeof(u32), cudaMemcpyHostToDevice));
+    // which records lead to such a state, by record position: read next to
+    // the record (one coalesced word per 32 records), so only those
+    // candidates look their destination's slack up
+    const size_t we = (size_t)(g->e_tot + 31) / 32 + 1, wx = (size_t)(g->x_tot + 31) / 32 + 1;
+    std::vector<u32> fe(we, 0), fx(wx, 0);
+    for (int64_t a = 0; a < g->num_arcs; ++a) {
+      const u32 d = g->arc_dst[a];
+      if (!((hq[d >> 4] >> ((d & 15) * 2)) & 3u)) continue;
+      const u32 p = g->arc_pos[a];
+      if (p & 0x80000000u) fx[(p & 0x7FFFFFFFu) >> 5] |= 1u << (p & 31);
+      else fe[p >> 5] |= 1u << (p & 31);
+    }
+    CK(cudaMalloc(&c.d_fbits, we * sizeof(u32)));
+    CK(cudaMemcpy(c.d_fbits, fe.data(), we * sizeof(u32), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c.d_fbits_x, wx * sizeof(u32)));
+    CK(cudaMemcpy(c.d_fbits_x, fx.data(), wx * sizeof(u32), cudaMemcpyHostToDevice));
   }
   CK(cudaMalloc(&c.d_neg, NEG_BLOCK_WORDS * sizeof(u32)));
   CK(cudaMemcpy(c.d_neg, negb.data(), NEG_BLOCK_WORDS * sizeof(u32), cudaMemcpyHostToDevice));
@@ -694,6 +720,8 @@ extern "C" int ab_context_release(ab_graph *g, int32_t handle) {
   cudaFree(c.d_bits_x);
   cudaFree(c.d_neg);
   cudaFree(c.d_hq);
+  cudaFree(c.d_fbits);
+  cudaFree(c.d_fbits_x);
   c = HostCtx();
   return sync_ctx_table(g);
 }

@@ -242,6 +242,7 @@ struct CtxDesc {
   // for 5M states, L2-resident), read for band candidates only
   const u32 *hq;
   double hq_unit;
+  const u32 *fbits, *fbits_x; // with hq: per record position, "the destination's hq > 0"
 };
 
 // Arc record formats.  Fmt16: f32 weight, 16-bit labels (one 16 B load).
@@ -902,6 +903,7 @@ template <typename F, typename S> struct Chan {
   const u32 *neg; // shared-memory copy of the context's (or graph's) slack Bloom filter
   u32 neg_fold; // log2(NEG_WORDS / the launch's filter words)
   const u32 *hq; // or the context's per-state 2-bit slack (CtxDesc::hq)
+  const u32 *fbits, *fbits_x; // (with hq) records whose destination has a slack, by position
   double hq_unit;
   // expansion tile (shared memory)
   u32 *t_a0;
@@ -939,6 +941,11 @@ template <bool EMIT, typename F, typename S>
 __device__ __forceinline__ u32 boost_word(const Chan<F, S> &C, u32 a) {
   return C.ctx_mode == CTX_BITSET ? __ldg(&(EMIT ? C.ctx_bits : C.ctx_bits_x)[a >> 5]) : 0u;
 }
+// Slack-flag word of a dense context for the record at position a (ditto).
+template <bool EMIT, typename F, typename S>
+__device__ __forceinline__ u32 slack_word(const Chan<F, S> &C, u32 a) {
+  return C.hq ? __ldg(&(EMIT ? C.fbits : C.fbits_x)[a >> 5]) : 0u;
+}
 
 // BiasingContext.boosted_mask (biasing.py:108-117) in the representation the
 // context store chose for this context; bw = boost_word of the record.
@@ -974,7 +981,7 @@ __device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 a, u32 bw, u
 // destination without epsilon arcs has no epsilon path, hence no slack).
 template <bool EMIT, typename F, typename S>
 __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double w, u32 il, u32 ol, u32 g, u32 d,
-                                          u32 a, u32 bw, u64 &ck, u32 &rflags) {
+                                          u32 a, u32 bw, u32 fw, u64 &ck, u32 &rflags) {
   const bool bst = is_boosted(C, a, bw, g & G_MASK, ol);
   const double we = bst ? w + C.discount : w;
   const double cand = EMIT ? (cj + we) + (double)C.row[il - 1] : cj + we;
@@ -983,6 +990,7 @@ __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double
   if (cand <= C.ucut0) return true;
   if (!(cand <= C.ucut) || !(g & G_DEST_EPS)) return false;
   if (C.hq) {
+    if (!((fw >> (a & 31u)) & 1u)) return false; // no slack at this destination
     const u32 q = (__ldg(C.hq + (d >> 4)) >> ((d & 15u) * 2u)) & 3u;
     return q && cand <= C.ucut0 + (double)q * C.hq_unit;
   }
@@ -1373,15 +1381,17 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = w_cost[lo];
         }
       }
-      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U];
+      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U], fw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         d[u] = g[u] = il[u] = ol[u] = 0;
         w[u] = 0.0;
         bw[u] = 0;
+        fw[u] = 0;
         if (on[u]) {
           bw[u] = boost_word<EMIT>(C, a[u]);
+          fw[u] = slack_word<EMIT>(C, a[u]);
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
@@ -1394,7 +1404,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       for (int u = 0; u < U; ++u) {
         ck[u] = 0;
         rflags[u] = 0;
-        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
+        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], fw[u], ck[u], rflags[u]);
       }
       PROF_MARK(sh, PF_XCAND);
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
@@ -1513,15 +1523,17 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
           cj[u] = t_cost[lo];
         }
       }
-      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U];
+      u32 d[U], dc[U], g[U], il[U], ol[U], bw[U], fw[U];
       double w[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         d[u] = g[u] = il[u] = ol[u] = 0;
         w[u] = 0.0;
         bw[u] = 0;
+        fw[u] = 0;
         if (on[u]) {
           bw[u] = boost_word<EMIT>(C, a[u]);
+          fw[u] = slack_word<EMIT>(C, a[u]);
           if (EMIT) F::emit(arcs, a[u], d[u], g[u], w[u], il[u], ol[u]);
           else F::eps(arcs, a[u], d[u], g[u], w[u], ol[u]);
         }
@@ -1534,7 +1546,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       for (int u = 0; u < U; ++u) {
         ck[u] = 0;
         rflags[u] = 0;
-        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], ck[u], rflags[u]);
+        if (on[u]) on[u] = candidate<EMIT>(C, cj[u], w[u], il[u], ol[u], g[u], d[u], a[u], bw[u], fw[u], ck[u], rflags[u]);
       }
       relax_batch<BLOCK, U>(P, C, sh, acc, on, d, dc, ck, g, src, rflags, ol, il, row0);
     }
@@ -2797,6 +2809,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.slack_rounds = P.slack0_rounds;
     C.hq = nullptr;
     C.hq_unit = 0.0;
+    C.fbits = C.fbits_x = nullptr;
     C.neg_fold = 0;
     C.ucut0 = C.ucut = INFINITY;
     C.neg = sh_neg;
@@ -2835,6 +2848,8 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
         C.slack_rounds = d.slack_rounds;
         C.hq = d.hq;
         C.hq_unit = d.hq_unit;
+        C.fbits = d.fbits;
+        C.fbits_x = d.fbits_x;
       }
       C.ctx_list = d.list;
     }
