@@ -131,7 +131,7 @@ struct ab_decoder {
   uint4 *flog_aux = nullptr;
   uint4 *eps_list = nullptr;
   u32 *app_list = nullptr;
-  u32 *flog_kill = nullptr; // kill words of the cluster kernels (allocated with the first cluster launch)
+  u32 *flog_kill = nullptr; // kill words (decode_kernel.cuh KW_*)
   u64 *scr_key = nullptr;
   u32 *scr_row = nullptr;
   int2 *arena = nullptr;
@@ -756,7 +756,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
     const uint64_t tk = std::min<uint64_t>(S, MAX_TOKENS);
     const uint64_t fl = cap.frontier_rows > 0 ? (uint64_t)cap.frontier_rows : std::max<uint64_t>(65536, 2 * tk);
     const uint64_t ar = cap.arena_records > 0 ? (uint64_t)cap.arena_records : std::max<uint64_t>(1ull << 19, 8 * fl);
-    const double per_ch_other = (double)tk * (4 + 8 + 16 + 16) + (double)fl * (4 + 8 + 16 + 16 + 4 + 8 + 4) +
+    const double per_ch_other = (double)tk * (4 + 8 + 16 + 16) + (double)fl * (4 + 8 + 16 + 16 + 4 + 4 + 8 + 4) +
                                 (double)ar * (2 * 8 + 2 * 4.0 / 32);
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
@@ -808,7 +808,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
       dmalloc(&d->flog_ck, C * d->flog_cap, acc) ||
       dmalloc(&d->flog_aux, C * d->flog_cap, acc) || dmalloc(&d->eps_list, C * d->flog_cap, acc) ||
 
-      dmalloc(&d->app_list, C * d->flog_cap, acc) ||
+      dmalloc(&d->app_list, C * d->flog_cap, acc) || dmalloc(&d->flog_kill, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_key, C * d->flog_cap, acc) ||
       dmalloc(&d->scr_row, C * d->flog_cap, acc) ||
       dmalloc(&d->arena, 2 * C * d->arena_cap, acc) ||
@@ -824,6 +824,7 @@ extern "C" int ab_decoder_create(ab_graph *g, const ab_capacity *capin, int32_t 
   if ((hslots && cudaMemset(d->table, 0, hslots * sizeof(Entry)) != cudaSuccess) ||
       (dslots && cudaMemset(d->vals, 0, dslots * 2 * sizeof(u64)) != cudaSuccess) ||
       cudaMemset(d->chans, 0, C * sizeof(ChanState)) != cudaSuccess ||
+      cudaMemset(d->flog_kill, 0, C * d->flog_cap * sizeof(u32)) != cudaSuccess || // (no valid tag)
       cudaEventCreate(&d->ev0) != cudaSuccess || cudaEventCreate(&d->ev1) != cudaSuccess) {
     ab_decoder_destroy(d);
     return fail(AB_ERR_CUDA, "decoder init failed");
@@ -1602,14 +1603,6 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       const int clu = (g->fmt16 && block == 1024 && !s64) ? pick_cluster(m) : 1;
       const size_t part = ((size_t)P.table_cap + clu - 1) / clu * 16; // a cluster CTA's table share
       const bool use_clu = clu > 1 && smem_table_fits<float>(smem, (size_t)P.table_cap / clu + 1);
-      if (use_clu && !d->flog_kill) { // kill words (zero: no valid tag) for every slot
-        size_t acc = 0;
-        const size_t nk = (size_t)d->max_ch * d->flog_cap;
-        if (dmalloc(&d->flog_kill, nk, acc) || cudaMemsetAsync(d->flog_kill, 0, nk * sizeof(u32), st) != cudaSuccess)
-          return fail(AB_ERR_CUDA, "kill-word allocation failed");
-        d->bytes += acc;
-      }
-      P.flog_kill = d->flog_kill;
       if (use_clu)
         le = clu == 8 ? launch_decode_cluster<8>(P, m, smem + part, st)
            : clu == 4 ? launch_decode_cluster<4>(P, m, smem + part, st)

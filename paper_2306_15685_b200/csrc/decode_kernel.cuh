@@ -45,7 +45,6 @@ constexpr int TAG_SHIFT = 19;
 constexpr u32 TAG_MASK = 0x1FFFu;
 constexpr u32 VROW_MASK = (1u << TAG_SHIFT) - 1;
 constexpr u32 MAX_ROWS = 1u << TAG_SHIFT;  // frontier rows per channel-frame
-constexpr u32 KILL_DISP = 0x80000000u;     // kill-queue entry: the row was displaced
 // arc records carry the destination's "has epsilon arcs" flag in bit 31 of the
 // arc id; every candidate into one destination has the same flag, so the
 // (cost, arc id) order inside a slot is unchanged (graphs have < 2^31 arcs)
@@ -54,19 +53,18 @@ constexpr u32 G_MASK = 0x7FFFFFFFu;
 constexpr u32 G_START = 0xFFFFFFFFu; // frontier row of the utterance-start token
 constexpr u32 MAX_TOKENS = 1u << 17;            // distinct tokens per channel-frame
 constexpr u32 MAX_HASH_SLOTS = 1u << 22;        // hashed token-table slots per channel
-// frontier row word: state | ecode (below) | DISP | DEAD
+// a row's state as read back: state | ecode (below) | DISP | DEAD
 constexpr u32 ROW_DEAD = 0x80000000u;  // superseded by a later round (an application, not a token)
 constexpr u32 ROW_DISP = 0x40000000u;  // displaced in its own round (not an application)
 constexpr u32 ROW_STATE = 0x07FFFFFFu;
-// A cluster's rows keep DEAD / DISP in a separate kill word per row, written
-// once, by the thread whose CAS replaced the row, with the epoch tag: (tag <<
-// 2) | KW_*.  No kill queue and no pass applying it, so a cluster's pass needs
-// one barrier (the listing of the next pass reads DISP behind it; DEAD is
-// read by prune only).  Their row state words carry ROW_REC at bit 30 (the
-// row has an output label: an emission record unless displaced).
+// DEAD / DISP live in a separate kill word per row, written once, by the
+// thread whose CAS replaced the row, with the epoch tag: (tag << 2) | KW_*.
+// No kill queue and no pass applying it, so a pass needs one barrier (the
+// next pass's listing reads DISP behind it; DEAD is read by prune only).  The
+// stored row state word carries ROW_REC at bit 30 (the row has an output
+// label: an emission record unless displaced).
 constexpr u32 KW_DEAD = 1u, KW_DISP = 2u;
 constexpr u32 ROW_REC = 0x40000000u;
-template <typename F> __host__ __device__ constexpr bool direct_kills() { return F::cluster > 1; }
 // a candidate's flags (registers; boost / output label also go to the row's aux word)
 constexpr u32 ROW_EPS = 0x20000000u;   // the state has epsilon out-arcs
 constexpr u32 ROW_BOOST = 0x10000000u; // the winning arc is boosted
@@ -143,12 +141,6 @@ template <int BLOCK, typename F> __device__ __forceinline__ void store_aux(uint4
   else st_row<BLOCK>(aux + row, make_uint4(x, 0u, ol, il));
 }
 template <typename F> __device__ __forceinline__ void load_aux(const uint4 *aux, u32 row, u32 &x, u32 &ol, u32 &il);
-// whether a frontier row's arc has an output label (an emission record)
-template <typename F, typename C_> __device__ __forceinline__ bool row_hasol(const C_ &C, u32 row) {
-  u32 x, ol, il;
-  load_aux<F>(C.flog_aux, row, x, ol, il);
-  return (x & AUX_HASOL) != 0;
-}
 template <typename F> __device__ __forceinline__ void load_aux(const uint4 *aux, u32 row, u32 &x, u32 &ol, u32 &il) {
   if constexpr (F::aux8) {
     const uint2 a = reinterpret_cast<const uint2 *>(aux)[row];
@@ -772,7 +764,6 @@ struct Counters {
   int max_depth;
   unsigned long long cnt_tok, cnt_emit, cnt_eps;
   int n_rec_frame; // emission records of the frame (olabel != 0 applications)
-  u32 n_kill[1];   // kill queue length of the current round (one CTA per channel)
   u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
@@ -876,7 +867,7 @@ template <typename F, typename S> struct Chan {
   uint4 *eps_list;
   TokInfo *tok_info_alt; // the other half of the channel's provenance buffer
   u32 *app_list;
-  u32 *kill; // the channel's kill words (direct_kills)
+  u32 *kill; // the channel's kill words (KW_*)
   u64 *scr_key;
   u32 *scr_row;
   int2 *arena; // live half
@@ -1020,11 +1011,11 @@ template <typename F, typename S> __device__ __forceinline__ u64 *val_at(const C
 // frontier row {state | flags, cost key, (source, arc id)} at a freshly
 // reserved index, then installs (cost, arc, round | tag | row) by CAS.  The
 // value therefore always names the row of the slot's current winner; a CAS
-// that replaces a winner of the same round queues that row as displaced
-// (not an application), one that replaces an earlier round's winner queues it
-// as superseded (an application, no longer a token).  The queue is applied
-// after the round's barrier, so the rows of a round are final without a
-// second pass over the table.
+// that replaces a winner of the same round marks that row displaced (not an
+// application), one that replaces an earlier round's winner marks it
+// superseded (an application, no longer a token), in the row's kill word, so
+// the rows of a round are final at the round's barrier without a second pass
+// over the table.
 __device__ __forceinline__ bool value_better(u64 ck, u32 g, u32 row0, u32 etag, u64 vck, u32 vg,
                                              u32 vinfo) {
   const bool valid = ((vinfo >> TAG_SHIFT) & TAG_MASK) == etag;
@@ -1045,15 +1036,6 @@ template <typename F, typename S> __device__ __forceinline__ u32 kill_flags(cons
   return (w >> 2) != C.etag ? 0u : (w & KW_DEAD) ? ROW_DEAD : ROW_DISP;
 }
 
-// Queues the row a successful CAS replaced (kill list = the applied-slot buffer).
-template <typename F, typename S>
-__device__ __forceinline__ void queue_kill(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 v) {
-  static_assert(!direct_kills<F>(), "a cluster writes kill words");
-  const u32 k = atomicAdd(&GC<F>(sh).n_kill[0], 1u);
-  if (k < P.flog_cap) C.app_list[k] = v;
-  else set_error<F>(sh, E_CAP);
-}
-
 // Outcome of a successful CAS that replaced old_info.
 template <typename F, typename S>
 __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, RelaxAcc &acc,
@@ -1068,8 +1050,7 @@ __device__ __forceinline__ void installed(const DecodeParams &P, const Chan<F, S
   atomicSub(&sh.fhist[hbucket(sh, key_cost(old_ck))], 1u);
   const bool earlier = (old_info & VROW_MASK) < row0;
   acc.n_app += earlier ? 1 : 0;
-  if constexpr (direct_kills<F>()) C.kill[old_info & VROW_MASK] = (etag << 2) | (earlier ? KW_DEAD : KW_DISP);
-  else queue_kill(P, C, sh, (old_info & VROW_MASK) | (earlier ? 0u : KILL_DISP));
+  C.kill[old_info & VROW_MASK] = (etag << 2) | (earlier ? KW_DEAD : KW_DISP);
 }
 
 // CAS retry loop after a lost race; the candidate's row is `row`.  A
@@ -1081,8 +1062,7 @@ __device__ void relax_retry(const DecodeParams &P, const Chan<F, S> &C, Shared &
   const u32 etag = C.etag;
   while (true) {
     if (!value_better(ck, g, row0, etag, vck, vg, vinfo)) {
-      if constexpr (direct_kills<F>()) C.kill[row] = (etag << 2) | KW_DISP;
-      else atomicOr(&C.flog_state[row], ROW_DISP);
+      C.kill[row] = (etag << 2) | KW_DISP;
       atomicSub(&sh.fhist[hbucket(sh, key_cost(ck))], 1u);
       acc.n_rec -= hasol ? 1 : 0;
       return;
@@ -1217,7 +1197,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
                     make_uint4(rows[u], d[u] | (xcode_of(dc[u]) << CODE_SHIFT), (u32)ck[u], (u32)(ck[u] >> 32)));
     }
     st_row<BLOCK>(&C.flog_state[rows[u]], d[u] | (ecode_of(dc[u]) << CODE_SHIFT) |
-                                              ((direct_kills<F>() && (rflags[u] & ROW_HASOL)) ? ROW_REC : 0u));
+                                              ((rflags[u] & ROW_HASOL) ? ROW_REC : 0u));
     st_row<BLOCK>(&C.flog_ck[rows[u]], (unsigned long long)ck[u]);
     store_aux<BLOCK, F>(C.flog_aux, rows[u], aux_src(src[u], rflags[u], g[u]), ol[u], il[u]);
     atomicAdd(&sh.fhist[hbucket(sh, key_cost(ck[u]))], 1u);
@@ -1259,7 +1239,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
   // with other channels, which hide the tile barrier (CTA-wide tiles)
   constexpr bool WARP_TILES = AB_WARP_TILES_MIN_BLOCK > 0 && BLOCK >= AB_WARP_TILES_MIN_BLOCK;
-  constexpr bool DISP_AT_LISTING = true; // displaced rows leave the epsilon frontier at listing
   u32 *t_a0 = C.t_a0;
   u32 *t_pref = C.t_pref;
   u32 *t_src = C.t_src;
@@ -1309,8 +1288,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         } else { // epsilon-frontier entries carry the row's state, flags and cost
           const uint4 e = list[base + j];
           idx[q] = e.x;
-          st[q] = e.y | (direct_kills<F>() ? (kill_flags(C, e.x) & ROW_DISP)
-                         : DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
+          st[q] = e.y | (kill_flags(C, e.x) & ROW_DISP); // displaced after listing
           w_cost[j] = key_cost(((u64)e.w << 32) | e.z);
         }
         w_src[j] = idx[q];
@@ -1321,7 +1299,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       a0[q] = 0;
       cnt[q] = 0;
       // (with the DISP check at listing, the degree load does not wait for it)
-      if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
+      if (idx[q] != 0xFFFFFFFFu) {
         const u32 s = st[q] & ROW_STATE;
         const u32 c = EMIT ? (st[q] >> CODE_SHIFT) & 7u : (st[q] >> CODE_SHIFT) & 3u;
         if (c == (EMIT ? ECODE_OVF : XCODE_OVF)) {
@@ -1446,8 +1424,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
         if (base + j < n_in) {
           const uint4 e = list[base + j];
           idx[q] = e.x;
-          st[q] = e.y | (direct_kills<F>() ? (kill_flags(C, e.x) & ROW_DISP)
-                         : DISP_AT_LISTING ? (C.flog_state[e.x] & ROW_DISP) : 0u); // displaced after listing
+          st[q] = e.y | (kill_flags(C, e.x) & ROW_DISP); // displaced after listing
           cq[q] = key_cost(((u64)e.w << 32) | e.z);
         }
       }
@@ -1457,7 +1434,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       a0[q] = 0;
       cnt[q] = 0;
       // (with the DISP check at listing, the degree load does not wait for it)
-      if (idx[q] != 0xFFFFFFFFu && (EMIT || DISP_AT_LISTING || !(st[q] & ROW_DISP))) {
+      if (idx[q] != 0xFFFFFFFFu) {
         const u32 s = st[q] & ROW_STATE;
         const u32 c = EMIT ? (st[q] >> CODE_SHIFT) & 7u : (st[q] >> CODE_SHIFT) & 3u;
         if (c == (EMIT ? ECODE_OVF : XCODE_OVF)) {
@@ -1563,7 +1540,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     // (each CTA's own minimum: a 64-bit atomicMin into a peer CTA's shared
     // memory is not atomic on sm_100, bench_tools/dsmem_atomics_probe.cu)
     if (mck != ~0ull) atomicMin(&sh.cnt.min_ck, mck);
-    if (n_rec && !direct_kills<F>()) atomicAdd(&GC<F>(sh).n_rec_frame, n_rec); // (direct: prune counts)
     if (n_app) atomicAdd(&GC<F>(sh).n_app[sh.rpar], n_app);
     if (n_new && atomicAdd(&GC<F>(sh).n_new, n_new) + n_new > P.tok_cap) set_error<F>(sh, E_CAP);
   }
@@ -1576,25 +1552,6 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       else GC<F>(sh).cnt_eps += arcs_seen;
     }
   }
-}
-
-// Applies the round's kill queue (after the round's barrier): displaced rows
-// are not applications, superseded ones are applications but not tokens.
-template <int BLOCK, typename F, typename S>
-__device__ void apply_kills(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
-  const u32 n = min(GC<F>(sh).n_kill[0], P.flog_cap);
-  u32 unrec = 0;
-  for (u32 i = crank<F>() * BLOCK + threadIdx.x; i < n; i += BLOCK * F::cluster) {
-    const u32 v = C.app_list[i];
-    const u32 row = v & VROW_MASK;
-    atomicOr(&C.flog_state[row], (v & KILL_DISP) ? ROW_DISP : ROW_DEAD);
-    if (v & KILL_DISP) unrec += row_hasol<F>(C, row) ? 1u : 0u; // a displaced row is no application (no record)
-  }
-  unrec = __reduce_add_sync(0xFFFFFFFFu, unrec); // one shared atomic per warp
-  if ((threadIdx.x & 31) == 0 && unrec) atomicSub(&GC<F>(sh).n_rec_frame, unrec);
-  csync<F>();
-  if (chan_t0<F>()) GC<F>(sh).n_kill[0] = 0;
-  csync<F>();
 }
 
 // Provenance of a surviving frontier row (decoder.py:385-393, 289-295): one
@@ -1648,46 +1605,9 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   return t;
 }
 
-// _epsilon_rounds (decoder.py:250-316).  The frontier of the next round is
-// the previous round's applications (n_front of them); the ones whose state
-// has epsilon arcs are eps_list[lo, hi).
-template <int BLOCK, typename F, typename S>
-__device__ void epsilon_rounds(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
-                               u32 n_front) {
-  int rounds = 0;
-  while (true) {
-    if (!(n_front > 0 && rounds < P.max_eps)) {
-      if (n_front > 0 && chan_t0<F>()) C.cs->info.eps_truncations += 1; // while-else 314-316
-      break;
-    }
-    rounds++;
-    const u32 row0 = GC<F>(sh).flog_n; // rows below were written by earlier rounds of this frame
-    csync<F>();
-    if (chan_t0<F>()) {
-      GC<F>(sh).n_app[0] = 0;
-      GC<F>(sh).n_cand[0] = 0;
-      GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
-    }
-    csync<F>();
-    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
-    csync<F>();
-    apply_kills<BLOCK>(P, C, sh);
-    PROF_MARK(sh, PF_EPS_X);
-    PROF_COUNT(sh, PF_ROUNDS, 1);
-    const u32 n_cand = GC<F>(sh).n_cand[0], n_app = GC<F>(sh).n_app[0];
-    if (GC<F>(sh).error) return;
-    if (n_cand == 0 || n_app == 0) break; // decoder.py:263-265, 285-287
-    lo = hi;
-    hi = GC<F>(sh).eps_n;
-    n_front = n_app;
-  }
-  csync<F>();
-}
-
-
-// --- a cluster's passes: one cluster barrier per pass ----------------------
+// --- passes: one (cluster) barrier per pass -------------------------------
 // What a pass leaves for the next one, read by every CTA after the pass's
-// barrier (kills are written during the pass: direct_kills).
+// barrier (kills are written during the pass: kill words).
 struct PassEnd {
   u32 row0_next; // rows so far: the next pass's first row
   u32 n_cand, n_app, eps_n;
@@ -1718,8 +1638,10 @@ __device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared
   return e;
 }
 
-// _epsilon_rounds (decoder.py:250-316) for a cluster: row0 of each round is
-// passed in (read before the previous pass's last barrier).
+// _epsilon_rounds (decoder.py:250-316).  The frontier of the next round is
+// the previous round's applications (n_front of them); the ones whose state
+// has epsilon arcs are eps_list[lo, hi); row0 of each round is passed in
+// (read after the previous pass's barrier).
 template <int BLOCK, typename F, typename S>
 __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
                                  u32 n_front, u32 row0) {
@@ -1875,7 +1797,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   const u64 best_ck = frame_min_ck<F>(C, sh);
   const double thr = key_cost(best_ck) + P.beam;
   const u64 thr_ck = cost_key(thr);
-  u32 *scr_state = C.app_list; // the kill queue is free until the next frame
+  u32 *scr_state = C.app_list; // (prune scratch)
   // split bucket: the first bucket where the live rows below and in it reach
   // max_active; buckets below the threshold's bucket are entirely in the beam
   const u32 bt = hbucket(sh, thr);
@@ -1936,8 +1858,6 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     sh.row_pending = 1;
   }
   if (chan_t0<F>()) {
-    if (!direct_kills<F>() && GC<F>(sh).n_rec_frame)
-      atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)GC<F>(sh).n_rec_frame);
     const double prev = C.cs->prev_cut;
     const double rise = prev < INFINITY ? cut - prev : 0.0;
     C.cs->cut_rise = fmax(rise, 0.8 * C.cs->cut_rise);
@@ -1949,7 +1869,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
   u32 bs = 0xFFFFFFFFu;
   int bi = -1;
   u32 n_tok = 0, n_mem = 0;
-  u32 n_rec = 0; // direct_kills: the frame's emission records (rows with an output label, not displaced)
+  u32 n_rec = 0; // the frame's emission records (rows with an output label, not displaced)
   u32 *mem_row = C.scr_row + P.flog_cap; // set-aside rows grow down from the top of scr_row
   for (u32 base = crank<F>() * TILE; base < n_rows; base += TILE * F::cluster) {
     // rows base + q * BLOCK + tid: warp-coalesced loads
@@ -1965,7 +1885,7 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       const u32 i = base + (u32)q * BLOCK + (u32)tid;
       ck[q] = i < n_rows ? C.flog_ck[i] : ~0ull;
     }
-    if constexpr (direct_kills<F>()) {
+    {
 #pragma unroll
       for (int q = 0; q < QP; ++q) {
         const u32 i = base + (u32)q * BLOCK + (u32)tid;
@@ -2028,11 +1948,14 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     n_mem += tot_m;
   }
   PROF_MARK(sh, PF_PROWS);
-  if constexpr (direct_kills<F>()) {
+  {
     n_rec = __reduce_add_sync(0xFFFFFFFFu, n_rec);
     if ((tid & 31) == 0 && n_rec) atomicAdd(&GC<F>(sh).n_rec_frame, (int)n_rec);
   }
   block_argmin<BLOCK>(bk, bs, bi, sh.redk, sh.reds, sh.redi);
+  if constexpr (F::cluster == 1) { // (behind block_argmin's barriers)
+    if (tid == 0 && sh.cnt.n_rec_frame) sh.cnt.rec_logical += (unsigned long long)sh.cnt.n_rec_frame;
+  }
   if constexpr (F::cluster > 1) { // the cluster's best and totals
     // (peers read xbest_* and out_tok / out_mem, written again only in the
     // next attempt, behind more barriers: no second barrier here)
@@ -2192,14 +2115,9 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   for (u32 i0 = 0; i0 < n_rows && crank<F>() == 0; i0 += BLOCK) {
     const u32 i = i0 + threadIdx.x;
     u32 st = i < n_rows ? C.flog_state[i] : ROW_DISP;
-    bool rec;
-    if constexpr (direct_kills<F>()) {
-      const u32 kf = i < n_rows ? kill_flags(C, i) : ROW_DISP;
-      rec = (st & ROW_REC) && !(kf & ROW_DISP);
-      st = (st & (ROW_STATE | ECODE_MASK)) | kf;
-    } else {
-      rec = i < n_rows && !(st & ROW_DISP) && row_hasol<F>(C, i);
-    }
+    const u32 kf = i < n_rows ? kill_flags(C, i) : ROW_DISP;
+    const bool rec = (st & ROW_REC) && !(kf & ROW_DISP);
+    st = (st & (ROW_STATE | ECODE_MASK)) | kf;
     const bool live = !(st & (ROW_DEAD | ROW_DISP));
     const u32 nrec = __popc(__ballot_sync(0xFFFFFFFFu, rec));
     if ((threadIdx.x & 31) == 0 && nrec) atomicAdd(&GC<F>(sh).rec_logical, (unsigned long long)nrec);
@@ -2284,7 +2202,6 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     GC<F>(sh).n_app[0] = GC<F>(sh).n_app[1] = GC<F>(sh).n_app[2] = 0;
     GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = GC<F>(sh).n_cand[2] = 0;
     GC<F>(sh).flog_n = 0;
-    GC<F>(sh).n_kill[0] = 0;
     GC<F>(sh).eps_n = 0;
     GC<F>(sh).emit_end = 0;
     GC<F>(sh).n_rec_frame = 0;
@@ -2374,7 +2291,6 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
               f1[1] = {ROW_EPS}, z1[1] = {0u};
     const u64 c1[1] = {cost_key(0.0)};
     relax_batch<1>(P, C, sh, acc, on1, d1, dc1, c1, g1, s1, f1, z1, z1, 0u);
-    GC<F>(sh).n_kill[0] = 0;
     GC<F>(sh).n_app[0] = GC<F>(sh).n_cand[0] = 0; // the closure's first round counts its own
     GC<F>(sh).emit_end = 0;
     sh.cnt.min_ck = cost_key(0.0);
@@ -2418,12 +2334,10 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
   if (cs->info.fresh) {
     flush_pending(P, C, sh, pend); // (none: a partial is deferred only while the utterance goes on)
     materialize_start<BLOCK>(P, C, sh);
-    if constexpr (F::cluster > 1) { // one row (the start token) so far
+    { // utterance-start closure (no prune): one row (the start token) so far
       const u32 hi0 = GC<F>(sh).eps_n;
       csync<F>();
       epsilon_rounds_c<BLOCK>(P, C, sh, 0u, hi0, 1u, 1u);
-    } else {
-      epsilon_rounds<BLOCK>(P, C, sh, 0u, GC<F>(sh).eps_n, 1u); // utterance-start closure, no prune
     }
     if (GC<F>(sh).error) return;
     rows_to_tokens<BLOCK>(P, C, sh); // (clears fresh; ends with a cluster barrier)
@@ -2475,21 +2389,13 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
     csync<F>();
     u32 n_app, eps_hi, row0_eps;
     int err;
-    if constexpr (F::cluster > 1) {
+    {
       const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
       err = e.error;
       n_app = e.n_app;
       eps_hi = e.eps_n;
       row0_eps = e.row0_next;
       if (chan_t0<F>()) GC<F>(sh).emit_end = e.row0_next; // read in resolve_row, behind more barriers
-    } else {
-      apply_kills<BLOCK>(P, C, sh);
-      n_app = GC<F>(sh).n_app[0];
-      eps_hi = GC<F>(sh).eps_n;
-      row0_eps = 0;
-      if (chan_t0<F>()) GC<F>(sh).emit_end = GC<F>(sh).flog_n;
-      csync<F>();
-      err = GC<F>(sh).error;
     }
     PROF_MARK(sh, PF_EMIT_BAR);
     if (err) return;
@@ -2500,11 +2406,8 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
       if (filt) ok = false;
       else if (chan_t0<F>()) cs->info.num_active = 0;
     } else {
-      if constexpr (F::cluster > 1) {
-        epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
-        PROF_MARK(sh, PF_EPS_S);
-      }
-      else epsilon_rounds<BLOCK>(P, C, sh, 0u, eps_hi, n_app);
+      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
+      PROF_MARK(sh, PF_EPS_S);
       if (GC<F>(sh).error) return;
       ok = prune<BLOCK>(P, C, sh);
     }
