@@ -1259,6 +1259,7 @@ static cudaError_t launch_decode_cluster(const DecodeParams &P, int n, size_t sm
   if (smem > attr_set) {
     const size_t want = std::max(dyn_smem_max(), smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = want;
   }
   if (!sms) {
@@ -1297,7 +1298,7 @@ static int pick_cluster(int n) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char *e = getenv("AB_CLUSTER")) {
     const int c = atoi(e);
-    return (c == 2 || c == 4 || c == 8) ? c : 1;
+    return (c == 2 || c == 4 || c == 8 || c == 16) ? c : 1;
   }
   for (int c = 8; c >= 2; c /= 2)
     if ((long long)n * c <= sms) return c;
@@ -1604,7 +1605,8 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
       const size_t part = ((size_t)P.table_cap + clu - 1) / clu * 16; // a cluster CTA's table share
       const bool use_clu = clu > 1 && smem_table_fits<float>(smem, (size_t)P.table_cap / clu + 1);
       if (use_clu)
-        le = clu == 8 ? launch_decode_cluster<8>(P, m, smem + part, st)
+        le = clu == 16 ? launch_decode_cluster<16>(P, m, smem + part, st)
+           : clu == 8 ? launch_decode_cluster<8>(P, m, smem + part, st)
            : clu == 4 ? launch_decode_cluster<4>(P, m, smem + part, st)
                       : launch_decode_cluster<2>(P, m, smem + part, st);
       else if (g->fmt16 && block == 1024 && (s64 ? smem_table_fits<double>(smem, P.table_cap)

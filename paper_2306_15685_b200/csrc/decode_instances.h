@@ -21,7 +21,7 @@
 // small graphs, 1024-thread CTAs: the token table in shared memory
 #define AB_DECODE_F16S(X) X(1024, Fmt16S, float) X(1024, Fmt16S, double)
 // ... a channel per thread-block cluster (C1 / C2: few channels)
-#define AB_DECODE_F16C(X) X(1024, Fmt16SC2, float) X(1024, Fmt16SC4, float) X(1024, Fmt16SC8, float)
+#define AB_DECODE_F16C(X) X(1024, Fmt16SC2, float) X(1024, Fmt16SC4, float) X(1024, Fmt16SC8, float) X(1024, Fmt16SC16, float)
 #define AB_DECODE_ALL(X)                                                                                \
   AB_DECODE_HOT(X) AB_DECODE_F16D(X) AB_DECODE_F16H(X) AB_DECODE_F24D(X) AB_DECODE_F24H(X) AB_DECODE_F16S(X) \
   AB_DECODE_F16C(X)

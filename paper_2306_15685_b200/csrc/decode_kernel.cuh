@@ -310,6 +310,7 @@ template <int CL> struct Fmt16SC : Fmt16<false, true> {
 typedef Fmt16SC<2> Fmt16SC2;
 typedef Fmt16SC<4> Fmt16SC4;
 typedef Fmt16SC<8> Fmt16SC8;
+typedef Fmt16SC<16> Fmt16SC16; // (non-portable cluster size)
 template <typename F> __host__ __device__ constexpr int exp_u() { return F::cluster > 1 ? AB_EXP_U_CLUSTER : EXP_U; }
 
 struct ChanState {
@@ -856,8 +857,8 @@ template <typename F, typename S> struct Chan {
   Entry *table;
   u64 *vals;
   u64 *gvals; // the channel's global direct table (wiped with a shared-memory table)
-  u64 *peer_vals[8]; // cluster: every CTA's part of the shared-memory table (generic DSMEM addresses)
-  Shared *peer_sh[8]; // cluster: every CTA's Shared (histograms, per-CTA best tokens)
+  u64 *peer_vals[F::cluster]; // cluster: every CTA's part of the shared-memory table (generic DSMEM addresses)
+  Shared *peer_sh[F::cluster]; // cluster: every CTA's Shared (histograms, per-CTA best tokens)
   u32 *tok_state;
   double *tok_cost;
   TokInfo *tok_info;
@@ -1569,6 +1570,47 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   base.hits = 0;
   base.last_il = 0;
   const u32 emit_end = GC<F>(sh).emit_end;
+  if constexpr (F::cluster > 1) {
+    // (a cluster's record counter is the leader's: one warp-aggregated
+    // reservation after a counting walk, then the records on a second walk
+    // over the same, now cached, aux words)
+    int hits = 0, nrec = 0;
+    u32 il = 0, cur = row;
+    while (true) {
+      u32 ax_x, ax_ol, ax_il;
+      load_aux<F>(C.flog_aux, cur, ax_x, ax_ol, ax_il);
+      if (ax_x & AUX_START) break;
+      hits += (ax_x & AUX_BOOST) ? 1 : 0;
+      nrec += (ax_x & AUX_HASOL) ? 1 : 0;
+      if (cur < emit_end) {
+        il = ax_il;
+        base = prev_tok[ax_x & AUX_SRC];
+        break;
+      }
+      cur = ax_x & AUX_SRC;
+    }
+    const u32 r0 = agg_reserve(&GC<F>(sh).rec_n, (u32)nrec);
+    if (nrec && r0 + (u32)nrec > P.arena_cap) {
+      set_error<F>(sh, E_CAP);
+      nrec = 0;
+    }
+    cur = row;
+    for (int j = 0; j < nrec;) {
+      u32 ax_x, ax_ol, ax_il;
+      load_aux<F>(C.flog_aux, cur, ax_x, ax_ol, ax_il);
+      if (ax_x & AUX_HASOL) { // record r0 + j (newest first) -> the next older one
+        C.arena[r0 + j] = make_int2((int)ax_ol, j + 1 < nrec ? (int)(r0 + j + 1) : base.bp);
+        ++j;
+      }
+      cur = ax_x & AUX_SRC;
+    }
+    TokInfo t;
+    t.hits = base.hits + hits;
+    t.depth = base.depth + nrec;
+    t.last_il = (int)il;
+    t.bp = nrec ? (int)r0 : base.bp;
+    return t;
+  }
   int hits = 0, nrec = 0, newest = -1, pend = -1;
   u32 pend_ol = 0, il = 0;
   u32 cur = row;
