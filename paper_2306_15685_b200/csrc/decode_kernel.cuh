@@ -857,6 +857,7 @@ template <typename F, typename S> struct Chan {
   Entry *table;
   u64 *vals;
   u64 *gvals; // the channel's global direct table (wiped with a shared-memory table)
+  double prev_best, prev_cut, cut_rise; // this CTA's copy of ChanState's (every CTA updates it alike)
   u64 *peer_vals[F::cluster]; // cluster: every CTA's part of the shared-memory table (generic DSMEM addresses)
   Shared *peer_sh[F::cluster]; // cluster: every CTA's Shared (histograms, per-CTA best tokens)
   u32 *tok_state;
@@ -1899,11 +1900,18 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     bulk_row_load(const_cast<S *>(C.row), sh.next_row, (u32)(P.L * sizeof(S)), &sh.row_bar);
     sh.row_pending = 1;
   }
-  if (chan_t0<F>()) {
-    const double prev = C.cs->prev_cut;
+  if (tid == 0) { // every CTA keeps the cutoff history (its own copy; the channel state for later launches)
+    Chan<F, S> &M = const_cast<Chan<F, S> &>(C);
+    const double prev = M.prev_cut;
     const double rise = prev < INFINITY ? cut - prev : 0.0;
-    C.cs->cut_rise = fmax(rise, 0.8 * C.cs->cut_rise);
-    C.cs->prev_cut = cut;
+    M.cut_rise = fmax(rise, 0.8 * M.cut_rise);
+    M.prev_cut = cut;
+    M.prev_best = key_cost(best_ck);
+    if (crank<F>() == 0) {
+      C.cs->cut_rise = M.cut_rise;
+      C.cs->prev_cut = cut;
+      C.cs->prev_best = M.prev_best;
+    }
   }
   // pass over the rows: survivors (bucket < split) -> token list; split
   // bucket within the beam -> set aside; best (cost, state)
@@ -2118,10 +2126,8 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
     }
     if (F::cluster > 1 && tid == 0) GC<F>(sh).out_sel = n_tok;
     }
-    if constexpr (F::cluster > 1) {
-      csync<F>();
-      n_tok = GC<F>(sh).out_sel;
-    }
+    csync<F>(); // the selected rows are tokens
+    if constexpr (F::cluster > 1) n_tok = GC<F>(sh).out_sel;
   } else if (n_mem > 0) { // the whole split bucket survives (split across a cluster's CTAs)
     const u32 n0 = n_tok;
     for (u32 m = crank<F>() * BLOCK + tid; m < n_mem; m += BLOCK * F::cluster) {
@@ -2130,8 +2136,9 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       C.scr_row[n0 + m] = *(mem_row - 1 - m);
     }
     n_tok += n_mem;
+    csync<F>();
   }
-  csync<F>();
+  // (no split bucket: the row pass's tokens were published by its barrier)
   PROF_MARK(sh, PF_PRUNE_SEL);
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, bi);
   if (chan_t0<F>()) {
@@ -2139,7 +2146,6 @@ __device__ bool prune(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
       C.cs->info.trailing_silence += 1;
     else
       C.cs->info.trailing_silence = 0;
-    C.cs->prev_best = key_cost(best_ck);
   }
   // (the channel state written above is read after advance()'s last barrier)
   PROF_MARK(sh, PF_PRUNE_OUT);
@@ -2179,11 +2185,17 @@ __device__ void rows_to_tokens(const DecodeParams &P, const Chan<F, S> &C, Share
   }
   csync<F>();
   finish_tokens<BLOCK>(P, C, sh, n_tok, C.scr_row, -1);
-  if (chan_t0<F>()) {
-    C.cs->prev_best = key_cost(frame_min_ck<F>(C, sh));
-    C.cs->prev_cut = INFINITY; // the start closure is not pruned: no cutoff to start from
-    C.cs->cut_rise = 0.0;
-    C.cs->info.fresh = 0;
+  if (threadIdx.x == 0) {
+    Chan<F, S> &M = const_cast<Chan<F, S> &>(C);
+    M.prev_best = key_cost(frame_min_ck<F>(C, sh));
+    M.prev_cut = INFINITY; // the start closure is not pruned: no cutoff to start from
+    M.cut_rise = 0.0;
+    if (crank<F>() == 0) {
+      C.cs->prev_best = M.prev_best;
+      C.cs->prev_cut = INFINITY;
+      C.cs->cut_rise = 0.0;
+      C.cs->info.fresh = 0;
+    }
   }
   csync<F>();
 }
@@ -2229,7 +2241,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
   if (threadIdx.x == 0) {
     C.epoch = e;
     C.etag = e & TAG_MASK;
-    sh.hbase = C.cs->prev_best - P.beam;
+    sh.hbase = C.prev_best - P.beam;
     sh.hscale = HIST_PER_BEAM / P.beam;
     sh.cnt.min_ck = ~0ull; // every CTA's own frame minimum (frame_min_ck)
     sh.rpar = 0;
@@ -2404,7 +2416,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
   // candidate and the reference's len(store) / eps_truncations).
   const unsigned long long c_tok = GC<F>(sh).cnt_tok, c_emit = GC<F>(sh).cnt_emit, c_eps = GC<F>(sh).cnt_eps;
   const long long eps_tr = cs->info.eps_truncations;
-  bool filt = !P.exact && cs->prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
+  bool filt = !P.exact && C.prev_cut < INFINITY && C.slack < INFINITY && P.beam < INFINITY &&
               P.max_eps <= C.slack_rounds;
   // (a peer may still read the status above: IDLE or DECODING, both pass)
   if (chan_t0<F>() && cs->info.status != AB_DECODING) cs->info.status = AB_DECODING;
@@ -2412,7 +2424,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
     __syncthreads();
     if (threadIdx.x == 0) {
       const double hint = !filt ? INFINITY
-                          : attempt == 0 ? cs->prev_cut + fmax(cs->cut_rise, P.hint_min) + P.hint_extra +
+                          : attempt == 0 ? C.prev_cut + fmax(C.cut_rise, P.hint_min) + P.hint_extra +
                                                (cs->info.frame_index < P.hint_warm_frames ? P.hint_warm : 0.0)
                                          : GC<F>(sh).cut_fail;
       sh.cut_hint = hint;
@@ -2742,6 +2754,9 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.path_words = P.path_words + s * P.path_cap;
     C.row = sh_row;
     C.epoch = C.cs->epoch;
+    C.prev_best = C.cs->prev_best;
+    C.prev_cut = C.cs->prev_cut;
+    C.cut_rise = C.cs->cut_rise;
     C.etag = C.epoch & TAG_MASK;
     C.ctx_mode = CTX_NONE;
     C.discount = 0.0;
