@@ -500,13 +500,13 @@ static double eps_slack(ab_graph *g, const std::vector<u32> &boosted, double dis
   // too many states for the Bloom filter to stay sparse: 2-bit per-state slack
   const bool dense = hq && n_neg > HQ_MIN_STATES;
   if (dense) {
-    hq->assign(((size_t)g->num_states + 15) / 16, 0u);
-    *hq_unit = -lo * (1.0 + 1e-9) / 3.0 + 1e-12;
+    hq->assign(((size_t)g->num_states + HQ_PER_WORD - 1) / HQ_PER_WORD, 0u);
+    *hq_unit = -lo * (1.0 + 1e-9) / (double)HQ_MAX + 1e-12;
   }
   for (u32 s : touched) {
     if (dense && h[s] < 0.0) { // rounded up: a conservative per-state slack
-      const u32 q = (u32)std::min(3.0, std::ceil(-h[s] * (1.0 + 1e-9) / *hq_unit + 1e-9));
-      (*hq)[s >> 4] |= std::max(q, 1u) << ((s & 15) * 2);
+      const u32 q = (u32)std::min((double)HQ_MAX, std::ceil(-h[s] * (1.0 + 1e-9) / *hq_unit + 1e-9));
+      (*hq)[s / HQ_PER_WORD] |= std::max(q, 1u) << ((s % HQ_PER_WORD) * HQ_BITS);
     }
     if (h[s] < 0.0) {
       (*neg_bits)[neg_h1(s) >> 5] |= 1u << (neg_h1(s) & 31);
@@ -616,7 +616,7 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
     std::vector<u32> fe(we, 0), fx(wx, 0);
     for (int64_t a = 0; a < g->num_arcs; ++a) {
       const u32 d = g->arc_dst[a];
-      if (!((hq[d >> 4] >> ((d & 15) * 2)) & 3u)) continue;
+      if (!hq_get(hq.data(), d)) continue;
       const u32 p = g->arc_pos[a];
       if (p & 0x80000000u) fx[(p & 0x7FFFFFFFu) >> 5] |= 1u << (p & 31);
       else fe[p >> 5] |= 1u << (p & 31);

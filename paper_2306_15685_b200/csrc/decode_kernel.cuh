@@ -99,6 +99,13 @@ constexpr int CTX_SMEM_WORDS = 4096;        // sparse contexts / label bitmaps (
 #endif
 constexpr u32 NEG_WORDS = AB_NEG_WORDS;
 constexpr size_t HQ_MIN_STATES = 24 * 1024; // more such states: per-state slack bytes instead
+#ifndef AB_HQ_BITS
+#define AB_HQ_BITS 2 // bits of per-state slack (2 or 8)
+#endif
+constexpr u32 HQ_BITS = AB_HQ_BITS, HQ_PER_WORD = 32 / HQ_BITS, HQ_MAX = (1u << HQ_BITS) - 1;
+__host__ __device__ __forceinline__ u32 hq_get(const u32 *hq, u32 s) {
+  return (hq[s / HQ_PER_WORD] >> ((s % HQ_PER_WORD) * HQ_BITS)) & HQ_MAX;
+}
 constexpr int NEG_SHIFT = 32 - 5 - __builtin_ctz(NEG_WORDS); // hashes of log2(32 * NEG_WORDS) bits
 // A context stores the filter at NEG_WORDS and folded to every smaller power
 // of two down to NEG_MIN_WORDS (bit j of the half-size filter = OR of bits 2j,
@@ -984,7 +991,7 @@ __device__ __forceinline__ bool candidate(const Chan<F, S> &C, double cj, double
   if (!(cand <= C.ucut) || !(g & G_DEST_EPS)) return false;
   if (C.hq) {
     if (!((fw >> (a & 31u)) & 1u)) return false; // no slack at this destination
-    const u32 q = (__ldg(C.hq + (d >> 4)) >> ((d & 15u) * 2u)) & 3u;
+    const u32 q = (__ldg(C.hq + d / HQ_PER_WORD) >> ((d % HQ_PER_WORD) * HQ_BITS)) & HQ_MAX;
     return q && cand <= C.ucut0 + (double)q * C.hq_unit;
   }
   return neg_test(C.neg, d, C.neg_fold);
