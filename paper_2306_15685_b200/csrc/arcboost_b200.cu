@@ -60,7 +60,8 @@ struct HostCtx {
   int mode = CTX_SLIST; // device CTX_* code
   int abi_mode = AB_CTX_LIST;
   u32 words = 0;
-  u32 *d_list = nullptr;
+  u32 *d_list = nullptr;   // the arc ids as an open-addressing set (list_slot; ~0 = empty)
+  u32 list_mask = 0;       // its size - 1
   u32 *d_hash = nullptr; // CTX_SLIST: Bloom filter of the ids (words words)
   u32 *d_bits = nullptr;   // CTX_BITSET: emitting record positions; CTX_LABELS: olabel bitmap
   u32 *d_bits_x = nullptr; // CTX_BITSET: epsilon record positions
@@ -536,7 +537,7 @@ static int sync_ctx_table(ab_graph *g) {
     h[i].k = c.live ? c.k : 0;
     h[i].mode = c.mode;
     h[i].words = c.words;
-    h[i].pad = 0;
+    h[i].lmask = c.list_mask;
     h[i].list = c.d_list;
     h[i].hash = c.d_hash;
     h[i].bits = c.d_bits;
@@ -629,8 +630,19 @@ extern "C" int ab_context_register(ab_graph *g, const int64_t *arc_indices, int6
   CK(cudaMalloc(&c.d_neg, NEG_BLOCK_WORDS * sizeof(u32)));
   CK(cudaMemcpy(c.d_neg, negb.data(), NEG_BLOCK_WORDS * sizeof(u32), cudaMemcpyHostToDevice));
   c.mode = mode == AB_CTX_LABELS ? CTX_LABELS : mode == AB_CTX_BITSET ? CTX_BITSET : CTX_SLIST;
-  CK(cudaMalloc(&c.d_list, std::max<size_t>(list.size(), 1) * sizeof(u32)));
-  if (!list.empty()) CK(cudaMemcpy(c.d_list, list.data(), list.size() * sizeof(u32), cudaMemcpyHostToDevice));
+  { // the ids as a hash set (load <= 1/2, linear probing): one or two loads per lookup
+    u32 hs = 2;
+    while (hs < 2 * list.size()) hs <<= 1;
+    std::vector<u32> set(hs, 0xFFFFFFFFu);
+    for (u32 a : list) {
+      u32 h = list_slot(a, hs - 1);
+      while (set[h] != 0xFFFFFFFFu && set[h] != a) h = (h + 1) & (hs - 1);
+      set[h] = a;
+    }
+    c.list_mask = hs - 1;
+    CK(cudaMalloc(&c.d_list, hs * sizeof(u32)));
+    CK(cudaMemcpy(c.d_list, set.data(), hs * sizeof(u32), cudaMemcpyHostToDevice));
+  }
   if (mode == AB_CTX_LIST && c.k <= LIST_SMEM_MAX) { // shared-memory Bloom filter (else global search only)
     u32 words = 64;
     while (words < c.k) words <<= 1; // 32 bits per arc

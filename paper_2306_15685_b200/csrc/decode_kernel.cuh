@@ -100,7 +100,7 @@ constexpr int CTX_SMEM_WORDS = 4096;        // sparse contexts / label bitmaps (
 constexpr u32 NEG_WORDS = AB_NEG_WORDS;
 constexpr size_t HQ_MIN_STATES = 24 * 1024; // more such states: per-state slack bytes instead
 #ifndef AB_HQ_BITS
-#define AB_HQ_BITS 2 // bits of per-state slack (2 or 8)
+#define AB_HQ_BITS 8 // bits of per-state slack (2 or 8; 8 with the per-position flags: profiles/r02_hq_bits_ab.log)
 #endif
 constexpr u32 HQ_BITS = AB_HQ_BITS, HQ_PER_WORD = 32 / HQ_BITS, HQ_MAX = (1u << HQ_BITS) - 1;
 __host__ __device__ __forceinline__ u32 hq_get(const u32 *hq, u32 s) {
@@ -191,12 +191,14 @@ constexpr u32 RANK_MAX = 256; // prune's split bucket: selection by rank up to t
 enum { CTX_NONE = 0, CTX_SLIST = 1, CTX_GLIST = 2, CTX_BITSET = 3, CTX_LABELS = 4 };
 // LIST contexts of up to LIST_SMEM_MAX arcs: a two-hash Bloom filter of their
 // ids in shared memory (32 bits per arc, rounded up to a power of two: false
-// positives ~0.2%, so a warp rarely has a lane that goes further), the sorted
-// ids in global memory (through L1) searched for the filter's hits.  Shared
+// positives ~0.2%, so a warp rarely has a lane that goes further), and the
+// ids as a hash set in global memory (load <= 1/2: one or two loads) probed
+// for the filter's hits; larger lists probe the set alone.  Shared
 // memory not taken stays L1 (the kernel is sensitive to it).
 constexpr u32 LIST_SMEM_MAX = 2048;
 __host__ __device__ __forceinline__ u32 list_b1(u32 g, u32 nbits) { return ((g * 2654435761u) >> 7) & (nbits - 1u); }
 __host__ __device__ __forceinline__ u32 list_b2(u32 g, u32 nbits) { return ((g * 0x85EBCA6Bu) >> 9) & (nbits - 1u); }
+__host__ __device__ __forceinline__ u32 list_slot(u32 g, u32 mask) { return ((g ^ (g >> 15)) * 0x2C1B3C6Du >> 8) & mask; }
 
 // Token provenance carried with every token (decoder.py:58-62 + last_il 138).
 struct __align__(16) TokInfo {
@@ -227,8 +229,8 @@ struct CtxDesc {
   u32 k;     // arcs in the context
   int mode;  // CTX_*
   u32 words; // CTX_LABELS: bitmap words
-  u32 pad;
-  const u32 *list; // sorted arc ids
+  u32 lmask; // list: hash set size - 1
+  const u32 *list; // the arc ids as an open-addressing hash set (list_slot, ~0 = empty)
   const u32 *hash; // CTX_SLIST: Bloom filter of the ids (words words)
   const u32 *bits;   // CTX_BITSET: bit per emitting record position, CTX_LABELS: olabel bitmap
   const u32 *bits_x; // CTX_BITSET: bit per epsilon record position
@@ -889,8 +891,8 @@ template <typename F, typename S> struct Chan {
   // context
   double discount;
   int ctx_mode;
-  const u32 *ctx_list;
-  u32 ctx_k;
+  const u32 *ctx_list; // hash set of the context's arc ids
+  u32 ctx_k, ctx_lmask;
   const u32 *ctx_bits;
   const u32 *ctx_bits_x;
   u32 ctx_words;
@@ -955,21 +957,19 @@ __device__ __forceinline__ bool is_boosted(const Chan<F, S> &C, u32 a, u32 bw, u
   case CTX_NONE: return false;
   case CTX_LABELS: return ol < C.ctx_words * 32u && ((C.ctx_bits[ol >> 5] >> (ol & 31)) & 1u);
   case CTX_BITSET: return (bw >> (a & 31)) & 1u;
-  case CTX_SLIST: { // Bloom filter (shared), then the sorted ids (global) for its few hits
+  case CTX_SLIST: { // Bloom filter (shared), then the id set (global) for its few hits
     const u32 nb = C.ctx_words * 32u, b1 = list_b1(g, nb), b2 = list_b2(g, nb);
     if (!((C.ctx_bits[b1 >> 5] >> (b1 & 31)) & (C.ctx_bits[b2 >> 5] >> (b2 & 31)) & 1u)) return false;
   } // fall through
   default: {
-    const u32 *a = C.ctx_list; // CTX_GLIST: binary search of the sorted ids in global memory
-    u32 lo = 0, hi = C.ctx_k;
-    while (lo < hi) {
-      u32 mid = (lo + hi) >> 1;
-      u32 v = a[mid];
+    // CTX_GLIST (and the filter's hits): the hash set in global memory
+    if (C.ctx_k == 0) return false;
+    const u32 *a = C.ctx_list;
+    for (u32 h = list_slot(g, C.ctx_lmask);; h = (h + 1) & C.ctx_lmask) {
+      const u32 v = __ldg(a + h);
       if (v == g) return true;
-      if (v < g) lo = mid + 1;
-      else hi = mid;
+      if (v == 0xFFFFFFFFu) return false;
     }
-    return false;
   }
   }
 }
@@ -2768,6 +2768,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     C.ctx_mode = CTX_NONE;
     C.discount = 0.0;
     C.ctx_k = 0;
+    C.ctx_lmask = 0;
     C.ctx_words = 0;
     C.ctx_list = nullptr;
     C.ctx_bits = nullptr;
@@ -2806,6 +2807,7 @@ __device__ void setup_channel(Chan<F, S> &C, const DecodeParams &P, int b, S *sh
     if (threadIdx.x == 0) {
       C.discount = d.discount;
       C.ctx_k = d.k;
+      C.ctx_lmask = d.lmask;
       C.ctx_mode = mode;
       C.ctx_words = d.words;
       C.ctx_bits = (mode == CTX_LABELS || mode == CTX_SLIST) ? sh_ctx : d.bits;

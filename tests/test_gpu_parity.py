@@ -509,7 +509,7 @@ def test_cutoff_engages_and_changes_nothing_observable():
     assert sum(ch._page.get(ch._slot).cut_redos for ch in ch_m) > 0
 
 
-@pytest.mark.parametrize("cluster", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("cluster", ["1", "2", "4", "8", "16"])
 def test_cluster_sizes_agree(cluster, exact, monkeypatch):
     """A channel decoded by a thread-block cluster (table split
     over DSMEM, counters in the leader) gives the oracle's hypotheses and,
