@@ -755,10 +755,9 @@ enum {
 // memory; a channel decoded by a thread-block cluster (Fmt::cluster > 1, C1 /
 // C2) keeps them in the leader CTA's, reached over DSMEM (GC()).
 struct Counters {
-  // n_app / n_cand: per pass, by pass index mod 3 (Shared::rpar; always 0
-  // with one CTA per channel): a cluster reads a pass's slot after the pass's
-  // barrier and resets the slot of the pass after next, so a pass needs one
-  // cluster barrier
+  // n_app / n_cand: per pass, by pass index mod 3 (every thread tracks it):
+  // a pass's slot is read after the pass's barrier and the slot of the pass
+  // after next reset then, so a pass needs one (cluster) barrier
   // frontier rows so far | epsilon-frontier entries so far (eps_n), in one
   // 64-bit word: a warp reserves both with one atomic (agg_reserve2)
   union {
@@ -804,7 +803,6 @@ struct Shared {
   u64 xbest_k; // cluster prune: this CTA's best (cost, state) row, read by its peers
   u32 xbest_s;
   int xbest_i;
-  u32 rpar;        // counter slot of the current pass (cluster: pass index mod 3; else 0)
   int shared_words;
   long long words_off;
   // scan / reduce scratch
@@ -1242,7 +1240,7 @@ __device__ __forceinline__ void relax_batch(const DecodeParams &P, const Chan<F,
 //      into the cost add), one batched relaxation.
 template <int BLOCK, int Q, int U, bool EMIT, typename F, typename S>
 __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, const uint4 *list, u32 n_in,
-                       u32 row0, bool skip0 = false) {
+                       u32 row0, u32 slot, bool skip0 = false) {
   constexpr u32 TILE = BLOCK * Q;
   // 1024-thread CTAs (one channel alone on its SM, C1 / C2): warp-private
   // sub-tiles, no CTA barrier inside the pass; smaller CTAs share their SM
@@ -1400,7 +1398,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     __syncwarp();
   }
   if (lane == 0 && arcs_seen) {
-    atomicAdd(&GC<F>(sh).n_cand[sh.rpar], arcs_seen);
+    atomicAdd(&GC<F>(sh).n_cand[slot], arcs_seen);
     atomicAdd(EMIT ? &GC<F>(sh).cnt_emit : &GC<F>(sh).cnt_eps, (unsigned long long)arcs_seen);
   }
   } else {
@@ -1549,14 +1547,14 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
     // (each CTA's own minimum: a 64-bit atomicMin into a peer CTA's shared
     // memory is not atomic on sm_100, bench_tools/dsmem_atomics_probe.cu)
     if (mck != ~0ull) atomicMin(&sh.cnt.min_ck, mck);
-    if (n_app) atomicAdd(&GC<F>(sh).n_app[sh.rpar], n_app);
+    if (n_app) atomicAdd(&GC<F>(sh).n_app[slot], n_app);
     if (n_new && atomicAdd(&GC<F>(sh).n_new, n_new) + n_new > P.tok_cap) set_error<F>(sh, E_CAP);
   }
   static_assert(F::cluster == 1 || WARP_TILES, "a cluster's channel uses warp tiles");
   if (tid == 0 && crank<F>() == 0) {
     if (EMIT) GC<F>(sh).cnt_tok += n_in; // epsilon rounds count their whole frontier (epsilon_rounds)
     if (!WARP_TILES) {
-      GC<F>(sh).n_cand[sh.rpar] += arcs_seen;
+      GC<F>(sh).n_cand[slot] += arcs_seen;
       if (EMIT) GC<F>(sh).cnt_emit += arcs_seen;
       else GC<F>(sh).cnt_eps += arcs_seen;
     }
@@ -1664,11 +1662,11 @@ struct PassEnd {
   int error;
 };
 
-// After a pass's barrier: its counts, then the next pass's slot; the slot of
-// the pass after next (last read before this pass's barrier) is reset here.
+// After a pass's barrier: the counts of the pass (counter slot p = pass index
+// mod 3, which every thread tracks); the slot of the pass after next (last
+// read before this pass's barrier) is reset here.
 template <int BLOCK, typename F, typename S>
-__device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh) {
-  const u32 p = sh.rpar;
+__device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 p) {
   Counters &G = GC<F>(sh);
   PassEnd e;
   e.row0_next = G.flog_n; // (the leader's counters: remote loads, issued together)
@@ -1676,15 +1674,11 @@ __device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared
   e.n_app = G.n_app[p];
   e.eps_n = G.eps_n;
   e.error = G.error;
-  const u32 nx = p == 2 ? 0u : p + 1u;
   if (chan_t0<F>()) {
-    const u32 z = nx == 2 ? 0u : nx + 1u;
+    const u32 z = p == 0 ? 2u : p - 1u; // (p + 2) mod 3
     G.n_cand[z] = 0;
     G.n_app[z] = 0;
   }
-  __syncthreads(); // every thread of the CTA has read rpar
-  if (threadIdx.x == 0) sh.rpar = nx;
-  __syncthreads();
   return e;
 }
 
@@ -1694,7 +1688,7 @@ __device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared
 // (read after the previous pass's barrier).
 template <int BLOCK, typename F, typename S>
 __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 lo, u32 hi,
-                                 u32 n_front, u32 row0) {
+                                 u32 n_front, u32 row0, u32 slot) {
   int rounds = 0;
   while (true) {
     if (!(n_front > 0 && rounds < P.max_eps)) {
@@ -1703,11 +1697,12 @@ __device__ void epsilon_rounds_c(const DecodeParams &P, const Chan<F, S> &C, Sha
     }
     rounds++;
     if (chan_t0<F>()) GC<F>(sh).cnt_tok += n_front; // token expansions of the reference's round
-    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), false>(P, C, sh, C.eps_list + lo, hi - lo, row0);
+    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), false>(P, C, sh, C.eps_list + lo, hi - lo, row0, slot);
     PROF_MARK(sh, PF_EPS_X);
     PROF_COUNT(sh, PF_ROUNDS, 1);
     csync<F>();
-    const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
+    const PassEnd e = pass_end_c<BLOCK>(P, C, sh, slot);
+    slot = slot == 2 ? 0u : slot + 1u;
     PROF_MARK(sh, PF_EPS_BAR);
     if (e.error) return;
     if (e.n_cand == 0 || e.n_app == 0) break; // decoder.py:263-265, 285-287
@@ -2251,7 +2246,6 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.hbase = C.prev_best - P.beam;
     sh.hscale = HIST_PER_BEAM / P.beam;
     sh.cnt.min_ck = ~0ull; // every CTA's own frame minimum (frame_min_ck)
-    sh.rpar = 0;
   }
   if (chan_t0<F>()) {
     C.cs->epoch = e;
@@ -2398,7 +2392,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
     { // utterance-start closure (no prune): one row (the start token) so far
       const u32 hi0 = GC<F>(sh).eps_n;
       csync<F>();
-      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, hi0, 1u, 1u);
+      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, hi0, 1u, 1u, 0u);
     }
     if (GC<F>(sh).error) return;
     rows_to_tokens<BLOCK>(P, C, sh); // (clears fresh; ends with a cluster barrier)
@@ -2445,13 +2439,13 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
     PROF_MARK(sh, PF_EPOCH);
     const bool skip0 = pend; // global warp 0 (the leader's warp 0) writes the pending hypothesis
     flush_pending(P, C, sh, pend);
-    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), true>(P, C, sh, nullptr, n_tok, 0u, skip0);
+    expand<BLOCK, exp_q<BLOCK>(), exp_u<F>(), true>(P, C, sh, nullptr, n_tok, 0u, 0u, skip0);
     PROF_MARK(sh, PF_EMIT_X);
     csync<F>();
     u32 n_app, eps_hi, row0_eps;
     int err;
     {
-      const PassEnd e = pass_end_c<BLOCK>(P, C, sh);
+      const PassEnd e = pass_end_c<BLOCK>(P, C, sh, 0u);
       err = e.error;
       n_app = e.n_app;
       eps_hi = e.eps_n;
@@ -2467,7 +2461,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
       if (filt) ok = false;
       else if (chan_t0<F>()) cs->info.num_active = 0;
     } else {
-      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps);
+      epsilon_rounds_c<BLOCK>(P, C, sh, 0u, eps_hi, n_app, row0_eps, 1u);
       PROF_MARK(sh, PF_EPS_S);
       if (GC<F>(sh).error) return;
       ok = prune<BLOCK>(P, C, sh);
@@ -2865,7 +2859,6 @@ __global__ void __launch_bounds__(BLOCK, (AB_MINB * 256 / BLOCK) > 0 ? (AB_MINB 
                                         (row_in_smem ? ((size_t)P.L * sizeof(S) + 15) / 16 * 16 : 0));
   uint4 *sh_table = reinterpret_cast<uint4 *>(sh_neg + P.neg_words);
   if (threadIdx.x == 0) {
-    sh.rpar = 0;
     mbar_init(&sh.row_bar);
     sh.row_phase = 0;
     sh.row_pending = 0;
