@@ -48,8 +48,9 @@ enum {
   AB_MODE_STREAM = 1   /* _decode_one: partial cadence, endpointing, final (decoder.py:474-501) */
 };
 /* context lookup representation (ab_context_register mode):
-   LIST    sorted arc ids, binary search (shared memory when k <= 2048)
-   BITSET  one bit per arc in HBM
+   LIST    the arc ids as a hash set in HBM, behind a Bloom filter in shared
+           memory when k <= 2048
+   BITSET  one bit per arc (by device record position) in HBM
    LABELS  one bit per output label in shared memory; only valid (and only
            chosen by AUTO) when the context is exactly the set of arcs whose
            olabel lies in some label set, e.g. single-word entities */
