@@ -1197,7 +1197,8 @@ static void fill_params(ab_decoder *d, DecodeParams &P) {
 }
 
 #ifndef AB_STAGE_CHUNKS
-#define AB_STAGE_CHUNKS 4 // host-score chunks per ab_decode call (copy/decode overlap)
+#define AB_STAGE_FIRST_DIV 32 // host scores: the first chunk is 1/32 of the call's frames
+#define AB_STAGE_GROWTH 6     // and each next one up to 6x the previous (copy/decode overlap)
 #endif
 
 static size_t dyn_smem_max() { return (CTX_SMEM_WORDS + NEG_WORDS) * sizeof(u32) + SCORE_SMEM_MAX_BYTES; }
@@ -1478,17 +1479,27 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   const size_t esz = s64 ? 8 : 4;
   (void)rows;
   int rc;
-  // Host scores (the end-to-end path): frames [f0, f0 + Tc) of every channel
-  // are staged chunk by chunk into two device buffers on a copy stream; the
-  // copy of chunk c + 1 overlaps the decode of chunk c.  Utterances continue
+  // Host scores (the end-to-end path): frames [cb[c], cb[c + 1]) of every
+  // channel are staged chunk by chunk into two device buffers on a copy
+  // stream; the copy of chunk c + 1 overlaps the decode of chunk c.  Utterances continue
   // across chunks; only the last chunk finalizes (decoder.py:498-501).
   const bool host = !a->scores_on_device;
-  int K = 1;
-  int64_t Tc = maxT;
+  // chunk c holds frames [cb[c], cb[c + 1]): a short first chunk (its copy is
+  // the only one not under a decode), then each up to AB_STAGE_GROWTH times
+  // the previous (a frame of every channel decodes ~7x slower than it copies)
+  std::vector<int64_t> cb{0};
   if (host && maxT > 0) {
-    K = (int)std::min<int64_t>(maxT, AB_STAGE_CHUNKS);
-    Tc = (maxT + K - 1) / K;
+    int64_t len = std::max<int64_t>(1, (maxT + AB_STAGE_FIRST_DIV - 1) / AB_STAGE_FIRST_DIV);
+    while (cb.back() < maxT) {
+      cb.push_back(std::min<int64_t>(maxT, cb.back() + len));
+      len *= AB_STAGE_GROWTH;
+    }
+  } else {
+    cb.push_back(maxT);
   }
+  const int K = (int)cb.size() - 1;
+  int64_t Tc = 0; // the longest chunk: the staging buffers' rows per channel
+  for (int c = 0; c < K; ++c) Tc = std::max<int64_t>(Tc, cb[c + 1] - cb[c]);
   const size_t rowb = (size_t)g->L * esz;
   const size_t bufsz = host ? (size_t)n * (size_t)Tc * rowb : 0;
   if (host) {
@@ -1504,16 +1515,16 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   auto stage = [&](int c) -> int {
     unsigned char *dst = (unsigned char *)d->d_stage + (size_t)(c & 1) * bufsz;
     const unsigned char *src = (const unsigned char *)a->scores;
-    const int64_t f0 = (int64_t)c * Tc;
+    const int64_t f0 = cb[c], tc = cb[c + 1] - cb[c];
     // one 2D copy when the channels' rows are equally strided and disjoint
-    bool full = uniform && stride >= Tc * (int64_t)g->L;
-    for (int i = 0; i < n && full; ++i) full = frames[i] - f0 >= Tc;
+    bool full = uniform && stride >= tc * (int64_t)g->L;
+    for (int i = 0; i < n && full; ++i) full = frames[i] - f0 >= tc;
     if (full && n > 0) {
       CK(cudaMemcpy2DAsync(dst, Tc * rowb, src + ((size_t)soff[0] + (size_t)f0 * g->L) * esz,
-                           (size_t)stride * esz, Tc * rowb, n, cudaMemcpyHostToDevice, d->copy_stream));
+                           (size_t)stride * esz, tc * rowb, n, cudaMemcpyHostToDevice, d->copy_stream));
     } else {
       for (int i = 0; i < n; ++i) {
-        const int64_t fr = std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), Tc);
+        const int64_t fr = std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), tc);
         if (fr > 0)
           CK(cudaMemcpyAsync(dst + (size_t)i * Tc * rowb, src + ((size_t)soff[i] + (size_t)f0 * g->L) * esz,
                              (size_t)fr * rowb, cudaMemcpyHostToDevice, d->copy_stream));
@@ -1564,7 +1575,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   float total_ms = 0.f;
   if (host && (rc = stage(0))) return rc;
   for (int c = 0; c < K; ++c) {
-  const int64_t f0 = (int64_t)c * Tc;
+  const int64_t f0 = cb[c], tc = cb[c + 1] - cb[c];
   const bool last = c == K - 1;
   P.final_chunk = last ? 1 : 0;
   if (host) {
@@ -1576,7 +1587,7 @@ extern "C" int ab_decode(ab_decoder *d, const ab_decode_args *a) {
   act.clear();
   for (int i = 0; i < n; ++i) {
     if (d->res_err[i]) continue;
-    const int64_t fr = host ? std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), Tc) : frames[i];
+    const int64_t fr = host ? std::min<int64_t>(std::max<int64_t>(frames[i] - f0, 0), tc) : frames[i];
     if (fr > 0 || last) act.push_back(i);
     remaining[i] = (int)fr;
     cur_off[i] = host ? (long long)i * Tc * g->L : soff[i];
