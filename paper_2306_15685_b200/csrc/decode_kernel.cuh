@@ -98,7 +98,10 @@ constexpr int CTX_SMEM_WORDS = 4096;        // sparse contexts / label bitmaps (
 #define AB_NEG_WORDS 4096
 #endif
 constexpr u32 NEG_WORDS = AB_NEG_WORDS;
-constexpr size_t HQ_MIN_STATES = 24 * 1024; // more such states: per-state slack bytes instead
+#ifndef AB_HQ_MIN_STATES
+#define AB_HQ_MIN_STATES (24 * 1024)
+#endif
+constexpr size_t HQ_MIN_STATES = AB_HQ_MIN_STATES; // more such states: per-state slack instead
 #ifndef AB_HQ_BITS
 #define AB_HQ_BITS 8 // bits of per-state slack (2 or 8; 8 with the per-position flags: profiles/r02_hq_bits_ab.log)
 #endif
