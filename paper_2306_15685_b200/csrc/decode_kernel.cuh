@@ -776,7 +776,6 @@ struct Counters {
   int max_depth;
   unsigned long long cnt_tok, cnt_emit, cnt_eps;
   int n_rec_frame; // emission records of the frame (olabel != 0 applications)
-  u32 emit_end;    // rows below come from the emitting pass (their source is a token)
   int best_last_il;
   double cut_fail; // a failed attempt's own cutoff (the next attempt's hint)
   union { // cluster prune: survivors | split-bucket rows reserved so far (one atomic reserves both)
@@ -798,6 +797,9 @@ struct PendHyp {
 
 struct Shared {
   Counters cnt;    // this channel's counters (leader CTA of a cluster)
+  u32 emit_end;    // rows below come from the emitting pass (their source is a token); every CTA's copy
+  u32 pe_row0, pe_n_cand, pe_n_app, pe_eps_n; // pass_end_c: the leader's counts, read once per CTA
+  int pe_error;
   PendHyp pend;    // (leader CTA) the deferred partial hypothesis
   Counters *lead;  // the leader's counters (cluster mode: a DSMEM address)
   u32 sel;
@@ -1566,7 +1568,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
 
 // Provenance of a surviving frontier row (decoder.py:385-393, 289-295): one
 // walk over the row's source links back to the token of the previous frame
-// (rows below GC<F>(sh).emit_end are the emitting pass's; their source is a token
+// (rows below sh.emit_end are the emitting pass's; their source is a token
 // index) or to the utterance start.  Each arc with olabel != 0 on the way
 // gets an emission record; a record is written once the next older record of
 // the chain is known, so the chain is walked only once.
@@ -1578,7 +1580,7 @@ __device__ TokInfo resolve_row(const DecodeParams &P, const Chan<F, S> &C, Share
   base.depth = 0;
   base.hits = 0;
   base.last_il = 0;
-  const u32 emit_end = GC<F>(sh).emit_end;
+  const u32 emit_end = sh.emit_end;
   if constexpr (F::cluster > 1) {
     // (a cluster's record counter is the leader's: one warp-aggregated
     // reservation after a counting walk, then the records on a second walk
@@ -1671,17 +1673,25 @@ struct PassEnd {
 template <int BLOCK, typename F, typename S>
 __device__ PassEnd pass_end_c(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, u32 p) {
   Counters &G = GC<F>(sh);
-  PassEnd e;
-  e.row0_next = G.flog_n; // (the leader's counters: remote loads, issued together)
-  e.n_cand = G.n_cand[p];
-  e.n_app = G.n_app[p];
-  e.eps_n = G.eps_n;
-  e.error = G.error;
-  if (chan_t0<F>()) {
-    const u32 z = p == 0 ? 2u : p - 1u; // (p + 2) mod 3
-    G.n_cand[z] = 0;
-    G.n_app[z] = 0;
+  if (threadIdx.x == 0) { // (the leader's counters: one thread per CTA loads them)
+    sh.pe_row0 = G.flog_n;
+    sh.pe_n_cand = G.n_cand[p];
+    sh.pe_n_app = G.n_app[p];
+    sh.pe_eps_n = G.eps_n;
+    sh.pe_error = G.error;
+    if (crank<F>() == 0) {
+      const u32 z = p == 0 ? 2u : p - 1u; // (p + 2) mod 3
+      G.n_cand[z] = 0;
+      G.n_app[z] = 0;
+    }
   }
+  __syncthreads();
+  PassEnd e;
+  e.row0_next = sh.pe_row0;
+  e.n_cand = sh.pe_n_cand;
+  e.n_app = sh.pe_n_app;
+  e.eps_n = sh.pe_eps_n;
+  e.error = sh.pe_error;
   return e;
 }
 
@@ -2249,6 +2259,7 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     sh.hbase = C.prev_best - P.beam;
     sh.hscale = HIST_PER_BEAM / P.beam;
     sh.cnt.min_ck = ~0ull; // every CTA's own frame minimum (frame_min_ck)
+    sh.emit_end = 0;
   }
   if (chan_t0<F>()) {
     C.cs->epoch = e;
@@ -2261,7 +2272,6 @@ __device__ void next_epoch(const DecodeParams &P, Chan<F, S> &C, Shared &sh) {
     GC<F>(sh).n_cand[0] = GC<F>(sh).n_cand[1] = GC<F>(sh).n_cand[2] = 0;
     GC<F>(sh).flog_n = 0;
     GC<F>(sh).eps_n = 0;
-    GC<F>(sh).emit_end = 0;
     GC<F>(sh).n_rec_frame = 0;
   }
   csync<F>();
@@ -2350,7 +2360,6 @@ __device__ void materialize_start(const DecodeParams &P, Chan<F, S> &C, Shared &
     const u64 c1[1] = {cost_key(0.0)};
     relax_batch<1>(P, C, sh, acc, on1, d1, dc1, c1, g1, s1, f1, z1, z1, 0u);
     GC<F>(sh).n_app[0] = GC<F>(sh).n_cand[0] = 0; // the closure's first round counts its own
-    GC<F>(sh).emit_end = 0;
     sh.cnt.min_ck = cost_key(0.0);
   }
   csync<F>();
@@ -2453,7 +2462,7 @@ __device__ void advance(const DecodeParams &P, Chan<F, S> &C, Shared &sh, bool &
       n_app = e.n_app;
       eps_hi = e.eps_n;
       row0_eps = e.row0_next;
-      if (chan_t0<F>()) GC<F>(sh).emit_end = e.row0_next; // read in resolve_row, behind more barriers
+      if (threadIdx.x == 0) sh.emit_end = e.row0_next; // read in resolve_row, behind more barriers
     }
     PROF_MARK(sh, PF_EMIT_BAR);
     if (err) return;
