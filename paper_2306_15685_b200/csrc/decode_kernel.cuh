@@ -380,8 +380,8 @@ struct DecodeParams {
   uint4 *eps_list; // [channel][flog_cap] {row, state | flags, cost key}: rows whose state has
                    // epsilon arcs, in write order (the next round's frontier)
   u32 flog_cap;
-  u32 *app_list;
-  u32 *flog_kill; // [channel][flog_cap] kill words (cluster kernels; else null)
+  u32 *app_list;  // [channel][flog_cap] prune scratch (split-bucket row states)
+  u32 *flog_kill; // [channel][flog_cap] kill words (KW_*)
   u64 *scr_key;
   u32 *scr_row;
   int2 *arena;   // [channel][2][arena_cap]: live half + GC to-space
