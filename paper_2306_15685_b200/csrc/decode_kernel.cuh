@@ -576,12 +576,16 @@ template <int BLOCK> __device__ __forceinline__ u32 block_excl_scan(u32 v, u32 &
 
 // Exclusive scan of Q values per thread in q-major order (element (q, t) at
 // position q * BLOCK + t): the order of coalesced loads i = base + q * BLOCK +
-// tid.  One barrier round like block_excl_scan; sh needs Q * BLOCK / 32 words.
+// tid.  One barrier: every warp scans the warp totals itself; consecutive
+// calls alternate between two scratch halves (par), so a warp that is ahead
+// never overwrites totals a slower warp is still reading (a barrier separates
+// a call from the one two calls later).  sh needs 2 * 32 words.
 template <int BLOCK, int Q>
-__device__ __forceinline__ void block_excl_scan_q(const u32 (&v)[Q], u32 (&ex)[Q], u32 &total, u32 *sh) {
+__device__ __forceinline__ void block_excl_scan_q(const u32 (&v)[Q], u32 (&ex)[Q], u32 &total, u32 *sh, u32 par) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NW = BLOCK / 32;
   static_assert(Q * NW <= 32, "scan scratch");
+  u32 *t = sh + (par & 1u) * 32u;
   u32 x[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -591,26 +595,22 @@ __device__ __forceinline__ void block_excl_scan_q(const u32 (&v)[Q], u32 (&ex)[Q
       const u32 y = __shfl_up_sync(0xffffffffu, x[q], o);
       if (lane >= o) x[q] += y;
     }
-    if (lane == 31) sh[q * NW + wid] = x[q];
+    if (lane == 31) t[q * NW + wid] = x[q];
   }
   __syncthreads();
-  if (wid == 0) {
-    u32 w = lane < Q * NW ? sh[lane] : 0;
+  u32 w = lane < Q * NW ? t[lane] : 0u;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < Q * NW) sh[lane] = w;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, w, o);
+    if (lane >= o) w += y;
   }
-  __syncthreads();
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int k = q * NW + wid;
-    ex[q] = (k ? sh[k - 1] : 0u) + x[q] - v[q];
+    const u32 before = __shfl_sync(0xffffffffu, w, (k + 31) & 31); // inclusive prefix of k - 1
+    ex[q] = (k ? before : 0u) + x[q] - v[q];
   }
-  total = sh[Q * NW - 1];
-  __syncthreads();
+  total = __shfl_sync(0xffffffffu, w, Q * NW - 1);
 }
 
 // (key, state) lexicographic argmin over a block; returns the winner's idx.
@@ -811,7 +811,7 @@ struct Shared {
   int shared_words;
   long long words_off;
   // scan / reduce scratch
-  u32 scan[32];
+  u32 scan[64]; // (block_excl_scan_q: two halves)
   u64 redk[32];
   u32 reds[32];
   int redi[32];
@@ -1461,7 +1461,7 @@ __device__ void expand(const DecodeParams &P, const Chan<F, S> &C, Shared &sh, c
       }
     }
     u32 total, pref[Q];
-    block_excl_scan_q<BLOCK, Q>(cnt, pref, total, sh.scan);
+    block_excl_scan_q<BLOCK, Q>(cnt, pref, total, sh.scan, base / TILE);
     // coarse index of the arc -> input search: the input owning arc 32 b
     // (written by the input whose range holds it) bounds every arc of block b
     const bool coarse = total <= 32u * TILE_COARSE;
